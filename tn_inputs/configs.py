@@ -1,0 +1,86 @@
+"""The five BASELINE.json workloads (C1..C5) and the seeded inputs they need.
+
+Recipe: U_ref = Trotter circuit of the config's spin
+chain compressed to chi (tn_inputs.reference); circuit gates G_k Haar-random
+U(4) from stream (cfg, "gates", k); tangent directions V_k = G_k S_k with S_k
+skew-Hermitian Gaussian from stream (cfg, "directions", b*K + k) -- a tangent
+vector by construction, same law as P_G(Z) for Gaussian Z (X14).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import rng
+from .models import Model, layer_pairs, trotter_layers
+
+
+@dataclass(frozen=True)
+class Config:
+    cid: int
+    name: str
+    n: int
+    depth: int
+    chi: int
+    model: Model
+    t: float
+    steps: int
+    order: int
+    batch: int
+    first_offset: int = 0
+    extra: dict = field(default_factory=dict)
+
+
+CONFIGS = {
+    1: Config(1, "C1-tfim-n6", 6, 4, 64, Model("tfim", {"J": 1.0, "h": 0.75}), 1.0, 12, 1, 1),
+    2: Config(2, "C2-xxx-n16", 16, 8, 64, Model("xxx", {"J": 1.0}), 0.5, 10, 2, 16),
+    3: Config(3, "C3-tfim-n32", 32, 12, 128, Model("tfim", {"J": 1.0, "h": 1.0, "g": 0.3}), 1.0, 20, 2, 64),
+    4: Config(4, "C4-xxz-n50", 50, 16, 256, Model("xxz", {"Delta": 0.5, "hz": 0.2}), 1.0, 25, 2, 64),
+    5: Config(5, "C5-tfim-n128", 128, 24, 256, Model("tfim", {"J": 1.0, "h": 0.9, "g": 0.4}), 2.0, 40, 2, 1,
+              extra={"problems": 32, "outer": 10, "max_hvp": 20}),
+}
+
+
+def brickwall_sites(n: int, depth: int, first_offset: int = 0):
+    """Left site of every gate, layer-major, left->right (X5)."""
+    out = []
+    for ell in range(1, depth + 1):
+        off = (first_offset + ell - 1) % 2
+        out.extend(i for i, _ in layer_pairs(n, off))
+    return out
+
+
+def num_gates(n: int, depth: int, first_offset: int = 0) -> int:
+    return len(brickwall_sites(n, depth, first_offset))
+
+
+def haar_gates(cid: int, K: int) -> np.ndarray:
+    return np.stack([rng.haar_u4(rng.stream_key(cid, "gates", k)) for k in range(K)])
+
+
+def tangent_directions(cid: int, gates: np.ndarray, batch: int, offset: int = 0) -> np.ndarray:
+    K = gates.shape[0]
+    out = np.empty((batch, K, 4, 4), dtype=np.complex128)
+    for b in range(batch):
+        for k in range(K):
+            s = rng.skew_gaussian(rng.stream_key(cid, "directions", (offset + b) * K + k))
+            out[b, k] = gates[k] @ s
+    return out
+
+
+def reference_layers(cfg: Config):
+    return trotter_layers(cfg.model, cfg.n, cfg.t, cfg.steps, cfg.order)
+
+
+def reference_mpo(cfg: Config, device="cpu"):
+    from .reference import reference_mpo as _build
+    return _build(reference_layers(cfg), cfg.n, cfg.chi, device=device)
+
+
+def small_case(cid: int, n: int, depth: int, chi: int, batch: int = 2, model: Model | None = None,
+               t: float = 0.6, steps: int = 3, order: int = 2, first_offset: int = 0) -> Config:
+    """A reduced workload for oracle-speed tests (same recipe, smaller sizes)."""
+    m = model or Model("tfim", {"J": 1.0, "h": 0.9, "g": 0.4})
+    return Config(cid, f"small-{cid}-n{n}-D{depth}-chi{chi}", n, depth, chi, m, t, steps, order, batch,
+                  first_offset)
