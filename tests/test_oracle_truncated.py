@@ -1,0 +1,102 @@
+"""Pins for the truncated definition: O2 (dense, explicit Schmidt projectors)
+and O3 (MPO sweeps, channel-form tangents) -- two structurally independent
+realisations of SURVEY.md §8(c.2) -- plus reduction to the exact O1."""
+import numpy as np
+import pytest
+
+from oracle import common as cm
+from oracle import dense as O
+from oracle import mpo as M
+from tn_inputs import configs as C
+from tn_inputs.reference import mpo_bonds, mpo_to_dense_operator, reference_mpo
+
+
+def setup(n, D, cid, nb=2, offset=0, ref_chi=4096):
+    cfg = C.small_case(cid, n, D, ref_chi, batch=nb, first_offset=offset)
+    ref = reference_mpo(C.reference_layers(cfg), n, ref_chi)
+    refs = [a.numpy() for a in ref]
+    U = mpo_to_dense_operator(ref) * 2 ** (n / 2)
+    sites = C.brickwall_sites(n, D, offset)
+    G = C.haar_gates(cid, len(sites))
+    V = C.tangent_directions(cid, G, nb)
+    return refs, mpo_bonds(ref), U, sites, G, V
+
+
+def rel(a, b):
+    return np.linalg.norm(np.ravel(a - b)) / np.linalg.norm(np.ravel(b))
+
+
+@pytest.mark.parametrize("n,D,offset", [(4, 4, 0), (5, 4, 1), (6, 3, 0)])
+def test_untruncated_equals_exact(n, D, offset):
+    refs, bonds, U, sites, G, V = setup(n, D, 40 + n, offset=offset)
+    T, E, H = O.alg1(n, sites, G, U, V[0])
+    o2 = O.DenseTruncated(n, D, 10 ** 6, G, O.op_to_vec(U / 2 ** (n / 2), n), bonds, V, offset)
+    o3 = M.MPOOracle(n, D, 10 ** 6, G, refs, V, offset)
+    for o in (o2, o3):
+        assert abs(o.T - T) < 1e-14
+        assert rel(o.gradient_T(), E) < 1e-13
+        assert rel(o.hvp_T(0), H) < 1e-13
+
+
+@pytest.mark.parametrize("n,D,chi,offset", [(6, 4, 4, 0), (7, 5, 8, 0), (6, 5, 6, 1), (8, 4, 16, 0)])
+def test_mpo_sweeps_equal_dense_definition_with_truncation(n, D, chi, offset):
+    refs, bonds, U, sites, G, V = setup(n, D, 50 + n + chi, offset=offset)
+    o2 = O.DenseTruncated(n, D, chi, G, O.op_to_vec(U / 2 ** (n / 2), n), bonds, V, offset)
+    o3 = M.MPOOracle(n, D, chi, G, refs, V, offset)
+    disc = [1 - np.sum(d["sigma"][:d["r"]] ** 2) / np.sum(d["sigma"] ** 2) for d in o2.diag]
+    assert max(disc) > 1e-3                      # truncation really active
+    assert abs(o2.T - o3.T) < 1e-13 * max(1, abs(o2.T))
+    assert rel(o3.gradient_T(), o2.gradient_T()) < 1e-12
+    for b in range(2):
+        assert rel(o3.hvp_T(b), o2.hvp_T(b)) < 1e-11
+    assert o3.diag["remainder"] < 1e-10         # before/after-chain reduction exact
+
+
+def test_truncated_hvp_is_linear_in_the_direction():
+    n, D, chi = 7, 4, 8
+    refs, bonds, U, sites, G, V = setup(n, D, 61, nb=2)
+    a, b = 0.7 - 0.2j, -1.3
+    Vc = np.concatenate([V, (a * V[0] + b * V[1])[None]], 0)
+    o3 = M.MPOOracle(n, D, chi, G, refs, Vc)
+    H = [o3.hvp_T(i) for i in range(3)]
+    assert rel(H[2], a * H[0] + b * H[1]) < 1e-13
+
+
+def test_tangent_bond_bound_two_chi():
+    """Tangent Schmidt rank <= 2 chi at every cut (App. D),
+    chi = the intermediate states' maximum bond: the reference
+    is compressed to chi as in the configs."""
+    n, D, chi = 7, 6, 4
+    refs, bonds, U, sites, G, V = setup(n, D, 62, ref_chi=chi)
+    o2 = O.DenseTruncated(n, D, chi, G, O.op_to_vec(U / 2 ** (n / 2), n), bonds, V)
+    for states in (o2.DB[1:], [o2.DT[ell] for ell in range(1, D)]):
+        for st in states:
+            for x in st:
+                for c in range(1, n):
+                    s = np.linalg.svd(x.reshape(4 ** c, -1), compute_uv=False)
+                    assert np.sum(s > 1e-12 * s[0]) <= 2 * chi
+
+
+def test_layer_euler_identity_under_truncation():
+    """Layer-wise environments are exact within the layer (X9): for each layer
+    T^(ell) = sum_ab G_k E_k for every gate k of that layer."""
+    n, D, chi = 8, 6, 8
+    refs, bonds, U, sites, G, V = setup(n, D, 63, nb=1)
+    o3 = M.MPOOracle(n, D, chi, G, refs, V)
+    E = o3.gradient_T()
+    for ell, ly in enumerate(cm.layers(n, D), start=1):
+        vals = [np.sum(G[k] * E[k]) for k, _ in ly]
+        assert np.abs(np.array(vals) - o3.layer_T[ell - 1]).max() < 1e-14
+
+
+def test_chi_convergence_to_exact():
+    """O3 -> O1 as chi -> the structural maximum (exact at 4^(n/2))."""
+    n, D = 8, 6
+    refs, bonds, U, sites, G, V = setup(n, D, 64, nb=1)
+    T, E, H = O.alg1(n, sites, G, U, V[0])
+    errs = []
+    for chi in (8, 32, 256):
+        o3 = M.MPOOracle(n, D, chi, G, refs, V)
+        errs.append(rel(o3.hvp_T(0), H))
+    assert errs[0] > errs[1] > 1e-9
+    assert errs[2] < 1e-12
