@@ -1,0 +1,137 @@
+/*
+ * tn_hvp.h -- C ABI of the B200 (sm_100a) Hessian-vector-product kernel for
+ * brickwall circuits compressed against an MPO reference
+ * (arXiv:2604.20384, "Hessian-vector products for tensor networks via
+ * recursive tangent-state propagation").
+ *
+ * Problem:
+ *   W = L_D ... L_1, layer L_ell = tensor product of two-qubit gates G_k on the
+ *   pairs (off, off+1), (off+2, off+3), ... with off = (first_offset+ell-1)%2;
+ *   gate index k layer-major, left->right (reading X5).
+ *   T = Tr(U_ref^dag W) / 2^n,  f = -|T|^2  (BASELINE.json config 1).
+ *   The reference U_ref/2^{n/2} is an MPO (site tensors [b_s][4][b_{s+1}],
+ *   p = 2*out + in, right-canonical, centre at site 0).
+ *   Bond cap chi: every two-site split keeps r = min(chi, 4 m, 4 b_l, 4 b_r)
+ *   singular values and rescales to the pre-truncation norm; tangents are
+ *   propagated with the primal's frozen Schmidt projectors (App. D,
+ *   PAPER.md:1019-1023; readings X7-X9).
+ *
+ * Numbers: complex128 interleaved (re, im) = 16 bytes, row-major.
+ *   gates [K][4][4]: row index = 2 q_i + q_{i+1} of the gate OUTPUT.
+ *   directions [B][K][4][4], outputs likewise.
+ *
+ * Ownership: every pointer argument is CALLER-owned.  Device pointers must
+ * stay valid for the duration of the call (stream-ordered).  The context owns
+ * its device arenas (primal store + workspace, cudaMalloc'd in
+ * tn_hvp_setup, freed in tn_hvp_destroy) and its cuSOLVER handle.  The primal
+ * store can be exported for a collective (tn_hvp_primal_blob).
+ *
+ * Streams: `stream` is a cudaStream_t passed as void*; all device work is
+ * enqueued on it.  Calls that must read a device value on the host say so.
+ *
+ * Errors: every call returns tn_status and never throws across the ABI.
+ *   TN_EINVAL  argument error, detected before any launch;
+ *   TN_ENOMEM  arena allocation failed;
+ *   TN_ECUDA   CUDA / cuSOLVER error (text via tn_hvp_last_error);
+ *   TN_ENUMERIC SVD non-convergence or non-finite output;
+ *   TN_ESTATE  tn_hvp_apply before tn_hvp_environments for the current gates.
+ * There is no CPU fallback: without a CUDA device every compute call returns
+ * TN_ECUDA.
+ */
+#ifndef TN_HVP_H
+#define TN_HVP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { TN_OK = 0, TN_EINVAL = 1, TN_ENOMEM = 2, TN_ECUDA = 3, TN_ENUMERIC = 4, TN_ESTATE = 5 } tn_status;
+
+typedef struct tn_hvp_ctx tn_hvp_ctx;
+
+typedef struct {
+  int32_t n_sites;      /* n >= 2                                               */
+  int32_t depth;        /* D >= 1 brickwall layers                              */
+  int32_t first_offset; /* 0 | 1: first layer on (0,1),(2,3).. or (1,2),(3,4).. */
+  int32_t chi;          /* primal bond cap; tangent bonds <= 2*chi              */
+  int32_t max_batch;    /* directions per internal sub-batch of tn_hvp_apply    */
+  int32_t device;       /* CUDA device ordinal                                  */
+  uint32_t flags;       /* reserved, 0                                          */
+} tn_hvp_config;
+
+/* Number of gates K implied by (n_sites, depth, first_offset). */
+int32_t tn_hvp_num_gates(int32_t n_sites, int32_t depth, int32_t first_offset);
+
+/* Create a context.  ref_bonds: HOST int32[n+1] (b_0 = b_n = 1);
+ * ref_mpo: DEVICE, the n site tensors packed back to back in site order,
+ * sum_s b_s*4*b_{s+1} complex128 (copied into the context).  Allocates the
+ * arenas for the whole (n, D, chi, max_batch) problem. */
+tn_status tn_hvp_setup(const tn_hvp_config* cfg, const int32_t* ref_bonds, const void* ref_mpo,
+                       void* stream, tn_hvp_ctx** out);
+
+/* Primal pass (a2-a5): bottom and top sweeps with truncation, per-layer
+ * left/right environments, E_k = dT/dG_k (eq:environment),
+ * f and the Riemannian gradient.
+ * gates: DEVICE [K][4][4].
+ * scalars_out: DEVICE double[8] = {f, Re T, Im T, max discarded weight,
+ *   min relative gap at a cut, max log10 |s|, 0, 0}.
+ * grad_R_out: DEVICE [K][4][4] (may be NULL).
+ * Synchronises the stream once at the end (SVD convergence flags). */
+tn_status tn_hvp_environments(tn_hvp_ctx* ctx, const void* gates, void* scalars_out, void* grad_R_out,
+                              void* stream);
+
+/* Riemannian HVP (a6-a9) for a batch of directions at the gates of the last
+ * tn_hvp_environments call: forward tangent propagation (eq:dfis), backward
+ * tangent propagation fused with the layer environments (eq:dbis,
+ * eq:overlap-hvp), then Omega, H_f and the Riemannian Hessian
+ * (PAPER.md:501-505, :1152-1157).
+ * dirs: DEVICE [batch][K][4][4] tangent at G (not checked unless flags).
+ * hess_R_out: DEVICE [batch][K][4][4].
+ * aux_out: DEVICE, nullable: [batch][K][4][4] H_T (Wirtinger HVP of T)
+ *   followed by [batch] complex Omega. */
+tn_status tn_hvp_apply(tn_hvp_ctx* ctx, int32_t batch, const void* dirs, void* hess_R_out, void* aux_out,
+                       void* stream);
+
+/* Euclidean pieces of the last environments call: E [K][4][4] (DEVICE out). */
+tn_status tn_hvp_gradient_T(tn_hvp_ctx* ctx, void* E_out, void* stream);
+
+/* Cost only (a3, top sweep): T and f at the given gates without touching the
+ * stored primal (for the trust-region rho test).  scalars_out as above. */
+tn_status tn_hvp_cost(tn_hvp_ctx* ctx, const void* gates, void* scalars_out, void* stream);
+
+/* Primal store as one flat device byte range (for an NCCL broadcast). */
+tn_status tn_hvp_primal_blob(tn_hvp_ctx* ctx, void** ptr, size_t* bytes);
+
+/* Mark the primal store as valid for `gates` after it was filled by a
+ * collective instead of tn_hvp_environments (same shapes, same gates). */
+tn_status tn_hvp_primal_imported(tn_hvp_ctx* ctx, const void* gates, void* stream);
+
+/* out = P_G(in) = 1/2 (in - G in^dag G), gate-wise, batched (eq:projec,
+ * PAPER.md:1113-1115).  gates [K][4][4], in/out [batch][K][4][4], DEVICE. */
+tn_status tn_riemannian_project(int32_t K, int32_t batch, const void* gates, const void* in, void* out,
+                                void* stream);
+
+/* Building block exposed for tests: batched complex128 GEMM on the FP64
+ * tensor cores (DMMA), C[b] = alpha op(A[b]) op(B[b]) + beta C[b], row-major,
+ * op in {'N','T','C'}; op(A) is M x K.  Strides in elements (0 = shared).
+ * alpha, beta: HOST double[2]. */
+tn_status tn_zgemm(char opa, char opb, int32_t M, int32_t N, int32_t K, const double* alpha,
+                   const void* A, int64_t lda, int64_t strideA, const void* B, int64_t ldb, int64_t strideB,
+                   const double* beta, void* C, int64_t ldc, int64_t strideC, int32_t batch, void* stream);
+
+/* Work model of one tn_hvp_apply direction (complex MACs of the schedule the
+ * context runs), and the bytes of the dominant kernel class; for rooflines. */
+tn_status tn_hvp_work(tn_hvp_ctx* ctx, double* cmac_per_direction, double* cmac_primal);
+
+void tn_hvp_destroy(tn_hvp_ctx* ctx);
+
+/* Last error text of ctx (or of the calling thread when ctx is NULL). */
+const char* tn_hvp_last_error(const tn_hvp_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TN_HVP_H */

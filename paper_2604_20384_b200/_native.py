@@ -1,0 +1,132 @@
+"""ctypes binding of libtn_hvp.so (include/tn_hvp.h): argument marshalling only.
+
+Same names as the C ABI.  Loading fails loudly if the in-tree library is
+missing; there is no CPU fallback anywhere in this package.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtn_hvp.so")
+
+TN_OK, TN_EINVAL, TN_ENOMEM, TN_ECUDA, TN_ENUMERIC, TN_ESTATE = range(6)
+STATUS = {0: "TN_OK", 1: "TN_EINVAL", 2: "TN_ENOMEM", 3: "TN_ECUDA", 4: "TN_ENUMERIC", 5: "TN_ESTATE"}
+
+EXPORTS = ["tn_hvp_num_gates", "tn_hvp_setup", "tn_hvp_environments", "tn_hvp_apply", "tn_hvp_gradient_T",
+           "tn_hvp_cost", "tn_hvp_primal_blob", "tn_hvp_primal_imported", "tn_riemannian_project", "tn_zgemm",
+           "tn_hvp_work", "tn_hvp_destroy", "tn_hvp_last_error"]
+
+
+class TNError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Config(C.Structure):
+    _fields_ = [("n_sites", C.c_int32), ("depth", C.c_int32), ("first_offset", C.c_int32), ("chi", C.c_int32),
+                ("max_batch", C.c_int32), ("device", C.c_int32), ("flags", C.c_uint32)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2604_20384_b200.build` (no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
+        L.tn_hvp_num_gates.argtypes = [i32, i32, i32]
+        L.tn_hvp_num_gates.restype = i32
+        L.tn_hvp_setup.argtypes = [C.POINTER(Config), C.POINTER(i32), vp, vp, C.POINTER(vp)]
+        L.tn_hvp_environments.argtypes = [vp, vp, vp, vp, vp]
+        L.tn_hvp_apply.argtypes = [vp, i32, vp, vp, vp, vp]
+        L.tn_hvp_gradient_T.argtypes = [vp, vp, vp]
+        L.tn_hvp_cost.argtypes = [vp, vp, vp, vp]
+        L.tn_hvp_primal_blob.argtypes = [vp, C.POINTER(vp), C.POINTER(C.c_size_t)]
+        L.tn_hvp_primal_imported.argtypes = [vp, vp, vp]
+        L.tn_riemannian_project.argtypes = [i32, i32, vp, vp, vp, vp]
+        L.tn_zgemm.argtypes = [C.c_char, C.c_char, i32, i32, i32, C.POINTER(C.c_double), vp, i64, i64, vp, i64, i64,
+                               C.POINTER(C.c_double), vp, i64, i64, i32, vp]
+        L.tn_hvp_work.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.tn_hvp_destroy.argtypes = [vp]
+        L.tn_hvp_destroy.restype = None
+        L.tn_hvp_last_error.argtypes = [vp]
+        L.tn_hvp_last_error.restype = C.c_char_p
+        for name in ("tn_hvp_setup", "tn_hvp_environments", "tn_hvp_apply", "tn_hvp_gradient_T", "tn_hvp_cost",
+                     "tn_hvp_primal_blob", "tn_hvp_primal_imported", "tn_riemannian_project", "tn_zgemm",
+                     "tn_hvp_work"):
+            getattr(L, name).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def check(status, ctx=None):
+    if status != TN_OK:
+        msg = lib().tn_hvp_last_error(ctx)
+        raise TNError(status, msg.decode() if msg else "")
+
+
+def tn_hvp_num_gates(n, depth, first_offset=0):
+    return lib().tn_hvp_num_gates(n, depth, first_offset)
+
+
+def tn_hvp_setup(cfg: Config, ref_bonds, ref_mpo_ptr, stream):
+    arr = (C.c_int32 * len(ref_bonds))(*ref_bonds)
+    out = C.c_void_p()
+    check(lib().tn_hvp_setup(C.byref(cfg), arr, C.c_void_p(ref_mpo_ptr), C.c_void_p(stream), C.byref(out)))
+    return out
+
+
+def tn_hvp_environments(ctx, gates_ptr, scalars_ptr, grad_R_ptr, stream):
+    check(lib().tn_hvp_environments(ctx, C.c_void_p(gates_ptr), C.c_void_p(scalars_ptr),
+                                    C.c_void_p(grad_R_ptr), C.c_void_p(stream)), ctx)
+
+
+def tn_hvp_apply(ctx, batch, dirs_ptr, hess_ptr, aux_ptr, stream):
+    check(lib().tn_hvp_apply(ctx, batch, C.c_void_p(dirs_ptr), C.c_void_p(hess_ptr), C.c_void_p(aux_ptr),
+                             C.c_void_p(stream)), ctx)
+
+
+def tn_hvp_gradient_T(ctx, E_ptr, stream):
+    check(lib().tn_hvp_gradient_T(ctx, C.c_void_p(E_ptr), C.c_void_p(stream)), ctx)
+
+
+def tn_hvp_cost(ctx, gates_ptr, scalars_ptr, stream):
+    check(lib().tn_hvp_cost(ctx, C.c_void_p(gates_ptr), C.c_void_p(scalars_ptr), C.c_void_p(stream)), ctx)
+
+
+def tn_hvp_primal_blob(ctx):
+    p, n = C.c_void_p(), C.c_size_t()
+    check(lib().tn_hvp_primal_blob(ctx, C.byref(p), C.byref(n)), ctx)
+    return p.value, n.value
+
+
+def tn_hvp_primal_imported(ctx, gates_ptr, stream):
+    check(lib().tn_hvp_primal_imported(ctx, C.c_void_p(gates_ptr), C.c_void_p(stream)), ctx)
+
+
+def tn_riemannian_project(K, batch, gates_ptr, in_ptr, out_ptr, stream):
+    check(lib().tn_riemannian_project(K, batch, C.c_void_p(gates_ptr), C.c_void_p(in_ptr), C.c_void_p(out_ptr),
+                                      C.c_void_p(stream)))
+
+
+def tn_zgemm(opa, opb, M, N, K, alpha, A, lda, sA, B, ldb, sB, beta, Cp, ldc, sC, batch, stream):
+    a = (C.c_double * 2)(alpha.real, alpha.imag)
+    b = (C.c_double * 2)(beta.real, beta.imag)
+    check(lib().tn_zgemm(opa.encode(), opb.encode(), M, N, K, a, C.c_void_p(A), lda, sA, C.c_void_p(B), ldb, sB, b,
+                         C.c_void_p(Cp), ldc, sC, batch, C.c_void_p(stream)))
+
+
+def tn_hvp_work(ctx):
+    a, b = C.c_double(), C.c_double()
+    check(lib().tn_hvp_work(ctx, C.byref(a), C.byref(b)), ctx)
+    return a.value, b.value
+
+
+def tn_hvp_destroy(ctx):
+    lib().tn_hvp_destroy(ctx)

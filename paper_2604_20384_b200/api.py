@@ -1,0 +1,120 @@
+"""Thin torch-facing wrapper over the C ABI (device memory and streams only).
+
+Every step of the computation runs in libtn_hvp.so; this module only
+allocates torch tensors, passes their data pointers and the current stream.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _native as N
+
+
+def _require_cuda(t: torch.Tensor, name: str):
+    if not (t.is_cuda and t.dtype == torch.complex128 and t.is_contiguous()):
+        raise ValueError(f"{name}: expected a contiguous complex128 CUDA tensor")
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+class HVPEngine:
+    """One context of the HVP kernel (n sites, depth D, bond cap chi).
+
+    ref_sites: list of n complex128 tensors [b_s][4][b_{s+1}] holding
+    U_ref/2^{n/2} (right-canonical, centre at site 0).
+    """
+
+    def __init__(self, n, depth, chi, ref_sites, first_offset=0, max_batch=64, device=None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2604_20384_b200 needs a CUDA device (no CPU fallback)")
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.n, self.depth, self.chi, self.first_offset = n, depth, chi, first_offset
+        self.K = N.tn_hvp_num_gates(n, depth, first_offset)
+        self.ref_bonds = [1] + [int(a.shape[2]) for a in ref_sites]
+        packed = torch.cat([a.to(self.device, torch.complex128).contiguous().reshape(-1) for a in ref_sites])
+        cfg = N.Config(n, depth, first_offset, chi, max_batch, self.device.index, 0)
+        with torch.cuda.device(self.device):
+            self.ctx = N.tn_hvp_setup(cfg, self.ref_bonds, packed.data_ptr(), _stream())
+        self.max_batch = max_batch
+        self.scalars = torch.zeros(8, dtype=torch.float64, device=self.device)
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            N.tn_hvp_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def environments(self, gates: torch.Tensor):
+        """-> (scalars[8] device, grad_R [K,4,4] device). scalars = f, Re T, Im T, diag..."""
+        _require_cuda(gates, "gates")
+        gR = torch.empty(self.K, 4, 4, dtype=torch.complex128, device=self.device)
+        N.tn_hvp_environments(self.ctx, gates.data_ptr(), self.scalars.data_ptr(), gR.data_ptr(), _stream())
+        return self.scalars, gR
+
+    def gradient_T(self):
+        E = torch.empty(self.K, 4, 4, dtype=torch.complex128, device=self.device)
+        N.tn_hvp_gradient_T(self.ctx, E.data_ptr(), _stream())
+        return E
+
+    def apply(self, dirs: torch.Tensor, aux: bool = False, out: torch.Tensor | None = None):
+        """Riemannian HVPs for dirs [B,K,4,4] -> hess [B,K,4,4] (and (H_T, Omega) if aux)."""
+        _require_cuda(dirs, "dirs")
+        B = dirs.shape[0]
+        hess = out if out is not None else torch.empty_like(dirs)
+        ax = torch.empty(B * self.K * 16 + B, dtype=torch.complex128, device=self.device) if aux else None
+        N.tn_hvp_apply(self.ctx, B, dirs.data_ptr(), hess.data_ptr(), ax.data_ptr() if aux else 0, _stream())
+        if aux:
+            return hess, ax[: B * self.K * 16].view(B, self.K, 4, 4), ax[B * self.K * 16:]
+        return hess
+
+    def cost(self, gates: torch.Tensor):
+        _require_cuda(gates, "gates")
+        sc = torch.zeros(8, dtype=torch.float64, device=self.device)
+        N.tn_hvp_cost(self.ctx, gates.data_ptr(), sc.data_ptr(), _stream())
+        return sc
+
+    def primal_blob(self):
+        return N.tn_hvp_primal_blob(self.ctx)
+
+    def primal_imported(self, gates: torch.Tensor):
+        N.tn_hvp_primal_imported(self.ctx, gates.data_ptr(), _stream())
+
+    def work(self):
+        """(complex MACs per direction of the last apply, complex MACs of the last primal pass)."""
+        return N.tn_hvp_work(self.ctx)
+
+
+def riemannian_project(gates: torch.Tensor, Z: torch.Tensor) -> torch.Tensor:
+    _require_cuda(gates, "gates")
+    _require_cuda(Z, "Z")
+    K = gates.shape[0]
+    B = Z.numel() // (K * 16)
+    out = torch.empty_like(Z)
+    N.tn_riemannian_project(K, B, gates.data_ptr(), Z.data_ptr(), out.data_ptr(), _stream())
+    return out
+
+
+def zgemm(A: torch.Tensor, B: torch.Tensor, opa="N", opb="N", alpha=1.0, beta=0.0, C=None):
+    """Batched DMMA complex GEMM on [batch, rows, cols] tensors (tests / probes)."""
+    _require_cuda(A, "A")
+    _require_cuda(B, "B")
+    A3 = A if A.dim() == 3 else A[None]
+    B3 = B if B.dim() == 3 else B[None]
+    batch = max(A3.shape[0], B3.shape[0])
+    M = A3.shape[1] if opa == "N" else A3.shape[2]
+    K = A3.shape[2] if opa == "N" else A3.shape[1]
+    Nn = B3.shape[2] if opb == "N" else B3.shape[1]
+    if C is None:
+        C = torch.zeros(batch, M, Nn, dtype=torch.complex128, device=A.device)
+    sA = 0 if A3.shape[0] == 1 else A3.shape[1] * A3.shape[2]
+    sB = 0 if B3.shape[0] == 1 else B3.shape[1] * B3.shape[2]
+    N.tn_zgemm(opa, opb, M, Nn, K, complex(alpha), A3.data_ptr(), A3.shape[2], sA, B3.data_ptr(), B3.shape[2], sB,
+               complex(beta), C.data_ptr(), Nn, M * Nn, batch, _stream())
+    return C

@@ -1,0 +1,147 @@
+// extern "C" boundary (include/tn_hvp.h).  Argument checking, status codes,
+// last-error text; the work itself lives in engine.cu / zgemm.cu / kernels.cu.
+#include <cstring>
+#include <string>
+
+#include "../../include/tn_hvp.h"
+#include "common.cuh"
+#include "engine.cuh"
+#include "kernels.cuh"
+
+namespace {
+thread_local std::string g_last_error;
+
+tn_status fail(tn_hvp_ctx* ctx, tn_status st, const std::string& msg) {
+  g_last_error = msg;
+  if (ctx) tn::engine_set_error(ctx, msg);
+  return st;
+}
+
+template <class F>
+tn_status guarded(tn_hvp_ctx* ctx, F&& f) {
+  try {
+    f();
+    return TN_OK;
+  } catch (const std::invalid_argument& e) {
+    return fail(ctx, TN_EINVAL, e.what());
+  } catch (const std::bad_alloc& e) {
+    return fail(ctx, TN_ENOMEM, e.what());
+  } catch (const tn::NumericError& e) {
+    return fail(ctx, TN_ENUMERIC, e.what());
+  } catch (const tn::StateError& e) {
+    return fail(ctx, TN_ESTATE, e.what());
+  } catch (const tn::CudaError& e) {
+    return fail(ctx, TN_ECUDA, e.what());
+  } catch (const std::exception& e) {
+    return fail(ctx, TN_ECUDA, e.what());
+  }
+}
+
+bool valid_op(char c) { return c == 'N' || c == 'T' || c == 'C'; }
+}  // namespace
+
+extern "C" {
+
+int32_t tn_hvp_num_gates(int32_t n, int32_t depth, int32_t off) {
+  if (n < 2 || depth < 1 || (off != 0 && off != 1)) return -1;
+  int32_t K = 0;
+  for (int32_t ell = 1; ell <= depth; ++ell) {
+    const int32_t o = (off + ell - 1) % 2;
+    for (int32_t s = o; s + 1 < n; s += 2) ++K;
+  }
+  return K;
+}
+
+tn_status tn_zgemm(char opa, char opb, int32_t M, int32_t N, int32_t K, const double* alpha, const void* A,
+                   int64_t lda, int64_t sA, const void* B, int64_t ldb, int64_t sB, const double* beta, void* C,
+                   int64_t ldc, int64_t sC, int32_t batch, void* stream) {
+  if (!valid_op(opa) || !valid_op(opb) || M < 0 || N < 0 || K < 0 || batch < 0 || !alpha || !beta)
+    return fail(nullptr, TN_EINVAL, "tn_zgemm: bad op/size/scalar argument");
+  if ((M && N && batch) && (!C || (K && (!A || !B)))) return fail(nullptr, TN_EINVAL, "tn_zgemm: null pointer");
+  return guarded(nullptr, [&] {
+    tn::zgemm((cudaStream_t)stream, opa, opb, M, N, K, make_double2(alpha[0], alpha[1]), (const tn::cplx*)A, lda,
+              sA, (const tn::cplx*)B, ldb, sB, make_double2(beta[0], beta[1]), (tn::cplx*)C, ldc, sC, batch);
+  });
+}
+
+tn_status tn_riemannian_project(int32_t K, int32_t batch, const void* gates, const void* in, void* out,
+                                void* stream) {
+  if (K < 0 || batch < 0) return fail(nullptr, TN_EINVAL, "tn_riemannian_project: negative size");
+  if ((K && batch) && (!gates || !in || !out)) return fail(nullptr, TN_EINVAL, "tn_riemannian_project: null pointer");
+  return guarded(nullptr, [&] {
+    tn::project((cudaStream_t)stream, K, batch, (const tn::cplx*)gates, (const tn::cplx*)in, (tn::cplx*)out);
+  });
+}
+
+tn_status tn_hvp_setup(const tn_hvp_config* cfg, const int32_t* ref_bonds, const void* ref_mpo, void* stream,
+                       tn_hvp_ctx** out) {
+  if (!cfg || !ref_bonds || !ref_mpo || !out) return fail(nullptr, TN_EINVAL, "tn_hvp_setup: null argument");
+  if (cfg->n_sites < 2 || cfg->depth < 1 || (cfg->first_offset != 0 && cfg->first_offset != 1) || cfg->chi < 1 ||
+      cfg->max_batch < 1)
+    return fail(nullptr, TN_EINVAL, "tn_hvp_setup: n>=2, depth>=1, offset in {0,1}, chi>=1, max_batch>=1");
+  if (ref_bonds[0] != 1 || ref_bonds[cfg->n_sites] != 1)
+    return fail(nullptr, TN_EINVAL, "tn_hvp_setup: boundary bonds must be 1");
+  for (int s = 0; s < cfg->n_sites; ++s) {
+    const int64_t bl = ref_bonds[s], br = ref_bonds[s + 1];
+    if (bl < 1 || br < 1 || br > 4 * bl || bl > 4 * br)
+      return fail(nullptr, TN_EINVAL, "tn_hvp_setup: reference bonds must satisfy 1 <= b_{s+1} <= 4 b_s and vice versa");
+  }
+  *out = nullptr;
+  return guarded(nullptr, [&] { *out = tn::engine_create(*cfg, ref_bonds, ref_mpo, (cudaStream_t)stream); });
+}
+
+tn_status tn_hvp_environments(tn_hvp_ctx* ctx, const void* gates, void* scalars_out, void* grad_R_out, void* stream) {
+  if (!ctx || !gates || !scalars_out) return fail(ctx, TN_EINVAL, "tn_hvp_environments: null argument");
+  return guarded(ctx, [&] {
+    tn::engine_environments(ctx, (const tn::cplx*)gates, (double*)scalars_out, (tn::cplx*)grad_R_out,
+                            (cudaStream_t)stream);
+  });
+}
+
+tn_status tn_hvp_apply(tn_hvp_ctx* ctx, int32_t batch, const void* dirs, void* hess_R_out, void* aux_out,
+                       void* stream) {
+  if (!ctx || batch < 0 || (batch && (!dirs || !hess_R_out)))
+    return fail(ctx, TN_EINVAL, "tn_hvp_apply: null argument or negative batch");
+  return guarded(ctx, [&] {
+    tn::engine_apply(ctx, batch, (const tn::cplx*)dirs, (tn::cplx*)hess_R_out, (tn::cplx*)aux_out,
+                     (cudaStream_t)stream);
+  });
+}
+
+tn_status tn_hvp_gradient_T(tn_hvp_ctx* ctx, void* E_out, void* stream) {
+  if (!ctx || !E_out) return fail(ctx, TN_EINVAL, "tn_hvp_gradient_T: null argument");
+  return guarded(ctx, [&] { tn::engine_gradient_T(ctx, (tn::cplx*)E_out, (cudaStream_t)stream); });
+}
+
+tn_status tn_hvp_cost(tn_hvp_ctx* ctx, const void* gates, void* scalars_out, void* stream) {
+  if (!ctx || !gates || !scalars_out) return fail(ctx, TN_EINVAL, "tn_hvp_cost: null argument");
+  return guarded(ctx, [&] {
+    tn::engine_cost(ctx, (const tn::cplx*)gates, (double*)scalars_out, (cudaStream_t)stream);
+  });
+}
+
+tn_status tn_hvp_primal_blob(tn_hvp_ctx* ctx, void** ptr, size_t* bytes) {
+  if (!ctx || !ptr || !bytes) return fail(ctx, TN_EINVAL, "tn_hvp_primal_blob: null argument");
+  return guarded(ctx, [&] { tn::engine_primal_blob(ctx, ptr, bytes); });
+}
+
+tn_status tn_hvp_primal_imported(tn_hvp_ctx* ctx, const void* gates, void* stream) {
+  if (!ctx || !gates) return fail(ctx, TN_EINVAL, "tn_hvp_primal_imported: null argument");
+  return guarded(ctx, [&] { tn::engine_primal_imported(ctx, (const tn::cplx*)gates, (cudaStream_t)stream); });
+}
+
+tn_status tn_hvp_work(tn_hvp_ctx* ctx, double* per_dir, double* primal) {
+  if (!ctx || !per_dir || !primal) return fail(ctx, TN_EINVAL, "tn_hvp_work: null argument");
+  return guarded(ctx, [&] { tn::engine_work(ctx, per_dir, primal); });
+}
+
+void tn_hvp_destroy(tn_hvp_ctx* ctx) {
+  if (ctx) tn::engine_destroy(ctx);
+}
+
+const char* tn_hvp_last_error(const tn_hvp_ctx* ctx) {
+  if (ctx) return tn::engine_error(ctx);
+  return g_last_error.c_str();
+}
+
+}  // extern "C"

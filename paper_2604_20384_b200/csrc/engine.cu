@@ -1,0 +1,1228 @@
+// The HVP engine: static plan of the sweeps, primal pass (tn_hvp_environments)
+// and batched tangent pass (tn_hvp_apply).  Every contraction is a call of the
+// DMMA complex GEMM (zgemm.cu) or a small kernel (kernels.cu); SVD / QR of the
+// two-site primal blocks use cuSOLVER (library primitives).
+//
+// Method (readings X7-X9):
+//  * bottom sweep B_0 = I/2^{n/2} -> B_D applying G_k on the out legs, top sweep
+//    T_D = U_ref/2^{n/2} -> T_0 applying G_k^dag (eq:fis, eq:bis),
+//    each gate followed by a truncated two-site SVD (keep r = min(chi,4m,4bl,4br),
+//    frozen renormalisation s);
+//  * tangents in channel form sum_j Ab..B_j..Aa (App. D) with
+//    the primal's isometries as fixed projectors;
+//  * E_k and H_T[V]_k layer-wise from left/right environments (eq:environment,
+//    eq:overlap-hvp) -- Algorithm 1's two passes
+//     at layer granularity, forward tangent cached, backward
+//    tangent on the fly.
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "engine.cuh"
+#include "kernels.cuh"
+
+struct tn_hvp_ctx;
+
+namespace tn {
+namespace {
+
+#define TN_SOLVER(x)                                                                                   \
+  do {                                                                                                 \
+    cusolverStatus_t s_ = (x);                                                                         \
+    if (s_ != CUSOLVER_STATUS_SUCCESS)                                                                 \
+      throw CudaError(std::string(#x) + ": cusolver status " + std::to_string((int)s_) + " @" + __FILE__ + \
+                      ":" + std::to_string(__LINE__));                                                 \
+  } while (0)
+
+const cplx ONE = {1.0, 0.0}, ZERO = {0.0, 0.0}, MONE = {-1.0, 0.0};
+
+enum StepType { MOVE_R = 0, MOVE_L = 1, PAIR = 2 };
+
+struct Step {
+  StepType type;
+  int site = 0;  // MOVE: centre c before the move; PAIR: left site i
+  int k = -1;
+  bool lr = true;
+  int bl = 0, m = 0, br = 0, r = 0, mn = 0;  // PAIR primal shapes
+  int b = 0, bp = 0, kq = 0, nb2 = 0;        // MOVE primal shapes; nb2 = neighbour's other bond
+  // chain bonds before the step (cuts site-1 .. site+2)
+  int abm = 0, ab0 = 0, ab1 = 0, ab2 = 0;
+  int aam = 0, aa0 = 0, aa1 = 0, aa2 = 0;
+  size_t o_theta = 0, o_uh = 0, o_vh = 0, o_S = 0, o_s = 0, o_q = 0;  // primal-arena offsets (bytes)
+  int s_index = -1;                                                  // index into host copy of s
+};
+
+struct Bonds {
+  std::vector<int> p, ab, aa;
+};
+
+struct SidePlan {
+  std::vector<int> ell;                     // processing order of layers
+  std::vector<std::vector<Step>> steps;     // per processed layer
+  std::vector<Bonds> snap;                  // bonds at each snapshot (before processing; + final)
+  std::vector<std::vector<size_t>> o_snap;  // primal-arena offsets of snapshot sites
+  Bonds init;
+};
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Pool {  // stream-ordered transient device buffers
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  explicit Pool(cudaStream_t s) : st(s) {}
+  cplx* c(int64_t n) {
+    void* p = nullptr;
+    if (n <= 0) n = 1;
+    TN_CUDA(cudaMallocAsync(&p, (size_t)n * sizeof(cplx), st));
+    ptrs.push_back(p);
+    return (cplx*)p;
+  }
+  void* raw(size_t bytes) {
+    void* p = nullptr;
+    TN_CUDA(cudaMallocAsync(&p, std::max<size_t>(bytes, 16), st));
+    ptrs.push_back(p);
+    return p;
+  }
+  ~Pool() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+  }
+};
+
+}  // namespace
+
+struct Engine {
+  tn_hvp_config cfg{};
+  int n = 0, D = 0, off = 0, chi = 0, K = 0;
+  std::vector<std::vector<std::pair<int, int>>> layers;  // per layer (k, s)
+  std::vector<int> ref_bonds;
+  SidePlan bot, top;
+  int n_pair_steps = 0;
+  // primal arena
+  char* arena = nullptr;
+  size_t arena_bytes = 0;
+  size_t o_gates = 0, o_gdag = 0, o_E = 0, o_gradf = 0, o_scal = 0, o_diag = 0;
+  std::vector<std::vector<size_t>> o_L, o_R;  // per layer, per cut
+  std::vector<double> h_s;                    // host copy of the frozen factors
+  cplx* ref = nullptr;                        // reference MPO copy (device)
+  std::vector<size_t> ref_off;
+  // solver
+  cusolverDnHandle_t solver = nullptr;
+  gesvdjInfo_t svdj = nullptr;
+  int lwork_svd = 0, lwork_geqrf = 0, lwork_ungqr = 0;
+  bool primal_valid = false;
+  double work_primal = 0, work_apply = 0, work_counter = 0;
+  std::string err;
+  int device = 0;
+
+  template <class T = cplx>
+  T* at(size_t o) const {
+    return reinterpret_cast<T*>(arena + o);
+  }
+
+  // ------------------------------------------------------------ GEMMs --
+  void mm(cudaStream_t st, char oa, char ob, int M, int N, int Kd, cplx a, const cplx* A, int64_t lda, int64_t sA,
+          const cplx* B, int64_t ldb, int64_t sB, cplx b, cplx* C, int64_t ldc, int64_t sC, int batch) {
+    if (M <= 0 || N <= 0 || batch <= 0) return;
+    work_counter += (double)M * N * std::max(Kd, 0) * batch;
+    zgemm(st, oa, ob, M, N, Kd, a, A, lda, sA, B, ldb, sB, b, C, ldc, sC, batch);
+  }
+  // C(MxN) = a A(MxK) B(KxN) + b C
+  void nn(cudaStream_t st, int M, int N, int Kd, const cplx* A, int64_t sA, const cplx* B, int64_t sB, cplx* C,
+          int64_t sC, int batch, cplx a = ONE, cplx b = ZERO) {
+    mm(st, 'N', 'N', M, N, Kd, a, A, Kd, sA, B, N, sB, b, C, N, sC, batch);
+  }
+  // C(MxN) = a A^H B, A stored (K x M), B (K x N)
+  void cn(cudaStream_t st, int M, int N, int Kd, const cplx* A, int64_t sA, const cplx* B, int64_t sB, cplx* C,
+          int64_t sC, int batch, cplx a = ONE, cplx b = ZERO) {
+    mm(st, 'C', 'N', M, N, Kd, a, A, M, sA, B, N, sB, b, C, N, sC, batch);
+  }
+  // C(MxN) = a A B^H, A (M x K), B stored (N x K)
+  void nc(cudaStream_t st, int M, int N, int Kd, const cplx* A, int64_t sA, const cplx* B, int64_t sB, cplx* C,
+          int64_t sC, int batch, cplx a = ONE, cplx b = ZERO) {
+    mm(st, 'N', 'C', M, N, Kd, a, A, Kd, sA, B, Kd, sB, b, C, N, sC, batch);
+  }
+
+  // ------------------------------------------------------------- plan --
+  void build_layers() {
+    layers.assign(D, {});
+    int k = 0;
+    for (int ell = 1; ell <= D; ++ell) {
+      const int o = (off + ell - 1) % 2;
+      for (int s = o; s + 1 < n; s += 2) layers[ell - 1].push_back({k++, s});
+    }
+    K = k;
+  }
+
+  void plan_side(SidePlan& sp, const std::vector<int>& init, bool is_top) {
+    sp = SidePlan();
+    Bonds b;
+    b.p = init;
+    b.ab = init;
+    b.aa = init;
+    sp.init = b;
+    int c = 0;
+    if (is_top)
+      for (int ell = D; ell >= 1; --ell) sp.ell.push_back(ell);
+    else
+      for (int ell = 1; ell <= D; ++ell) sp.ell.push_back(ell);
+    for (int ell : sp.ell) {
+      sp.snap.push_back(b);
+      const bool lr = is_top ? ((D - ell) % 2 == 0) : (ell % 2 == 1);
+      std::vector<std::pair<int, int>> ly = layers[ell - 1];
+      if (!lr) std::reverse(ly.begin(), ly.end());
+      std::vector<Step> steps;
+      for (auto [k, i] : ly) {
+        const int target = lr ? i : i + 1;
+        while (c != target) {
+          Step st;
+          const bool right = c < target;
+          st.type = right ? MOVE_R : MOVE_L;
+          st.site = c;
+          st.b = b.p[c];
+          st.bp = b.p[c + 1];
+          st.abm = c > 0 ? b.ab[c - 1] : 0;
+          st.ab0 = b.ab[c];
+          st.ab1 = b.ab[c + 1];
+          st.ab2 = c + 2 <= n ? b.ab[c + 2] : 0;
+          st.aam = c > 0 ? b.aa[c - 1] : 0;
+          st.aa0 = b.aa[c];
+          st.aa1 = b.aa[c + 1];
+          st.aa2 = c + 2 <= n ? b.aa[c + 2] : 0;
+          if (right) {
+            st.kq = std::min(4 * st.b, st.bp);
+            st.nb2 = b.p[c + 2];
+            if (b.ab[c] != b.p[c]) throw std::logic_error("plan: before-chain bond != primal bond (move right)");
+            b.p[c + 1] = st.kq;
+            b.ab[c + 1] = st.kq;
+            ++c;
+          } else {
+            st.kq = std::min(st.b, 4 * st.bp);
+            st.nb2 = b.p[c - 1];
+            if (b.aa[c + 1] != b.p[c + 1]) throw std::logic_error("plan: after-chain bond != primal bond (move left)");
+            b.p[c] = st.kq;
+            b.aa[c] = st.kq;
+            --c;
+          }
+          steps.push_back(st);
+        }
+        Step st;
+        st.type = PAIR;
+        st.site = i;
+        st.k = k;
+        st.lr = lr;
+        st.bl = b.p[i];
+        st.m = b.p[i + 1];
+        st.br = b.p[i + 2];
+        st.mn = std::min(4 * st.bl, 4 * st.br);
+        st.r = std::min({chi, 4 * st.m, 4 * st.bl, 4 * st.br});
+        st.abm = i > 0 ? b.ab[i - 1] : 0;
+        st.ab0 = b.ab[i];
+        st.ab1 = b.ab[i + 1];
+        st.ab2 = b.ab[i + 2];
+        st.aam = i > 0 ? b.aa[i - 1] : 0;
+        st.aa0 = b.aa[i];
+        st.aa1 = b.aa[i + 1];
+        st.aa2 = b.aa[i + 2];
+        if (b.ab[i] != st.bl || b.aa[i + 2] != st.br) throw std::logic_error("plan: chain/primal bond mismatch at pair");
+        b.p[i + 1] = st.r;
+        b.ab[i + 1] = st.r;
+        b.aa[i + 1] = st.r;
+        c = lr ? i + 1 : i;
+        steps.push_back(st);
+        ++n_pair_steps;
+      }
+      sp.steps.push_back(steps);
+    }
+    sp.snap.push_back(b);
+  }
+
+  size_t mpo_elems(const std::vector<int>& p) const {
+    size_t e = 0;
+    for (int s = 0; s < n; ++s) e += (size_t)p[s] * 4 * p[s + 1];
+    return e;
+  }
+
+  void layout_arena() {
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+      const size_t r = o;
+      o = align256(o + bytes);
+      return r;
+    };
+    const size_t C = sizeof(cplx);
+    o_gates = take(K * 16 * C);
+    o_gdag = take(K * 16 * C);
+    o_E = take(K * 16 * C);
+    o_gradf = take(K * 16 * C);
+    o_scal = take(8 * sizeof(double));
+    o_diag = take(8 * sizeof(double));
+    int s_index = 0;
+    for (SidePlan* sp : {&bot, &top}) {
+      sp->o_snap.clear();
+      for (const Bonds& b : sp->snap) {
+        std::vector<size_t> offs(n);
+        for (int s = 0; s < n; ++s) offs[s] = take((size_t)b.p[s] * 4 * b.p[s + 1] * C);
+        sp->o_snap.push_back(offs);
+      }
+      for (auto& ls : sp->steps)
+        for (Step& st : ls) {
+          if (st.type == PAIR) {
+            st.o_theta = take((size_t)16 * st.bl * st.br * C);
+            st.o_uh = take((size_t)st.r * 4 * st.bl * C);
+            st.o_vh = take((size_t)st.r * 4 * st.br * C);
+            st.o_S = take((size_t)st.mn * sizeof(double));
+            st.o_s = take(sizeof(double));
+            st.s_index = s_index++;
+          } else {
+            st.o_q = take((size_t)4 * std::max(st.b, st.bp) * st.kq * C);
+          }
+        }
+    }
+    // layer environments L0/R0: layer ell uses T_ell (top snapshot index D-ell) and B_{ell-1} (bottom index ell-1)
+    o_L.assign(D + 1, std::vector<size_t>(n + 1, 0));
+    o_R.assign(D + 1, std::vector<size_t>(n + 1, 0));
+    for (int ell = 1; ell <= D; ++ell) {
+      const Bonds& tb = top.snap[D - ell];
+      const Bonds& bb = bot.snap[ell - 1];
+      for (int c = 0; c <= n; ++c) {
+        o_L[ell][c] = take((size_t)tb.p[c] * bb.p[c] * C);
+        o_R[ell][c] = take((size_t)tb.p[c] * bb.p[c] * C);
+      }
+    }
+    arena_bytes = o;
+    h_s.assign(s_index, 1.0);
+  }
+
+  // ------------------------------------------------------------ setup --
+  void setup(const tn_hvp_config& c, const int32_t* rb, const void* ref_mpo, cudaStream_t st) {
+    cfg = c;
+    n = c.n_sites;
+    D = c.depth;
+    off = c.first_offset;
+    chi = c.chi;
+    device = c.device;
+    TN_CUDA(cudaSetDevice(device));
+    build_layers();
+    ref_bonds.assign(rb, rb + n + 1);
+    std::vector<int> ones(n + 1, 1);
+    plan_side(bot, ones, false);
+    plan_side(top, ref_bonds, true);
+    layout_arena();
+    TN_CUDA(cudaMalloc(&arena, std::max<size_t>(arena_bytes, 256)));
+    // reference copy
+    ref_off.assign(n, 0);
+    size_t e = 0;
+    for (int s = 0; s < n; ++s) {
+      ref_off[s] = e;
+      e += (size_t)ref_bonds[s] * 4 * ref_bonds[s + 1];
+    }
+    TN_CUDA(cudaMalloc(&ref, e * sizeof(cplx)));
+    TN_CUDA(cudaMemcpyAsync(ref, ref_mpo, e * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+    // memory pool keeps transient buffers cached
+    cudaMemPool_t pool;
+    TN_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    TN_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    // solver
+    TN_SOLVER(cusolverDnCreate(&solver));
+    TN_SOLVER(cusolverDnCreateGesvdjInfo(&svdj));
+    TN_SOLVER(cusolverDnXgesvdjSetTolerance(svdj, 1e-15));
+    TN_SOLVER(cusolverDnXgesvdjSetMaxSweeps(svdj, 100));
+    TN_SOLVER(cusolverDnSetStream(solver, st));
+    int maxM = 1;
+    for (SidePlan* sp : {&bot, &top})
+      for (auto& ls : sp->steps)
+        for (Step& s : ls) {
+          if (s.type == PAIR) {
+            int lw = 0;
+            TN_SOLVER(cusolverDnZgesvdj_bufferSize(solver, CUSOLVER_EIG_MODE_VECTOR, 1, 4 * s.br, 4 * s.bl, nullptr,
+                                                   4 * s.br, nullptr, nullptr, 4 * s.br, nullptr, 4 * s.bl, &lw,
+                                                   svdj));
+            lwork_svd = std::max(lwork_svd, lw);
+          } else {
+            const int mr = s.type == MOVE_R ? 4 * s.b : 4 * s.bp;
+            const int nc = s.type == MOVE_R ? s.bp : s.b;
+            int lw = 0;
+            TN_SOLVER(cusolverDnZgeqrf_bufferSize(solver, mr, nc, nullptr, mr, &lw));
+            lwork_geqrf = std::max(lwork_geqrf, lw);
+            TN_SOLVER(cusolverDnZungqr_bufferSize(solver, mr, s.kq, s.kq, nullptr, mr, nullptr, &lw));
+            lwork_ungqr = std::max(lwork_ungqr, lw);
+            maxM = std::max(maxM, mr);
+          }
+        }
+    (void)maxM;
+  }
+
+  ~Engine() {
+    if (svdj) cusolverDnDestroyGesvdjInfo(svdj);
+    if (solver) cusolverDnDestroy(solver);
+    if (arena) cudaFree(arena);
+    if (ref) cudaFree(ref);
+  }
+
+  // ------------------------------------------------------ primal pass --
+  struct Mps {  // current site tensors (pool-owned)
+    std::vector<cplx*> a;
+    std::vector<int> b;  // bonds
+  };
+
+  void qr_right(cudaStream_t st, Pool& pool, const cplx* P, int rows, int cols, int kq, cplx* Q, cplx* R, int* info) {
+    // P row-major rows x cols -> Q (rows x kq) row-major, R (kq x cols) row-major
+    cplx* cm = pool.c((int64_t)rows * cols);
+    transpose(st, cm, P, rows, cols, false);  // column-major rows x cols
+    cplx* tau = pool.c(std::min(rows, cols));
+    cplx* work = pool.c(std::max(lwork_geqrf, lwork_ungqr));
+    TN_SOLVER(cusolverDnSetStream(solver, st));
+    TN_SOLVER(cusolverDnZgeqrf(solver, rows, cols, (cuDoubleComplex*)cm, rows, (cuDoubleComplex*)tau,
+                               (cuDoubleComplex*)work, lwork_geqrf, info));
+    tri_extract(st, R, cm, kq, cols, rows, true);
+    TN_SOLVER(cusolverDnZungqr(solver, rows, kq, kq, (cuDoubleComplex*)cm, rows, (cuDoubleComplex*)tau,
+                               (cuDoubleComplex*)work, lwork_ungqr, info));
+    transpose(st, Q, cm, kq, rows, false);  // cm is (kq x rows) row-major -> Q rows x kq
+  }
+
+  void lq_left(cudaStream_t st, Pool& pool, const cplx* P, int rows, int cols, int kq, cplx* Q, cplx* L, int* info) {
+    // P row-major rows x cols = L (rows x kq) Q (kq x cols), Q row-orthonormal
+    cplx* cm = pool.c((int64_t)rows * cols);
+    TN_CUDA(cudaMemcpyAsync(cm, P, (size_t)rows * cols * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+    cplx* tau = pool.c(std::min(rows, cols));
+    cplx* work = pool.c(std::max(lwork_geqrf, lwork_ungqr));
+    TN_SOLVER(cusolverDnSetStream(solver, st));
+    // column-major view: cols x rows matrix P^T
+    TN_SOLVER(cusolverDnZgeqrf(solver, cols, rows, (cuDoubleComplex*)cm, cols, (cuDoubleComplex*)tau,
+                               (cuDoubleComplex*)work, lwork_geqrf, info));
+    tri_extract(st, L, cm, rows, kq, cols, false);
+    TN_SOLVER(cusolverDnZungqr(solver, cols, kq, kq, (cuDoubleComplex*)cm, cols, (cuDoubleComplex*)tau,
+                               (cuDoubleComplex*)work, lwork_ungqr, info));
+    TN_CUDA(cudaMemcpyAsync(Q, cm, (size_t)kq * cols * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+  }
+
+  // Runs one side's primal sweep.  store: write snapshots / replay data to the arena.
+  // Returns the final MPS (pool-owned) -- the top side's T_0.
+  Mps primal_side(cudaStream_t st, Pool& pool, bool is_top, bool store, int* info, double* diag) {
+    SidePlan& sp = is_top ? top : bot;
+    const cplx* G = is_top ? at(o_gdag) : at(o_gates);
+    Mps P;
+    P.a.assign(n, nullptr);
+    P.b = sp.init.p;
+    for (int s = 0; s < n; ++s) {
+      const int64_t e = (int64_t)P.b[s] * 4 * P.b[s + 1];
+      P.a[s] = pool.c(e);
+      if (is_top) {
+        TN_CUDA(cudaMemcpyAsync(P.a[s], ref + ref_off[s], e * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+      } else {
+        const double h = 1.0 / std::sqrt(2.0);
+        cplx id[4] = {{h, 0}, {0, 0}, {0, 0}, {h, 0}};
+        TN_CUDA(cudaMemcpyAsync(P.a[s], id, sizeof(id), cudaMemcpyHostToDevice, st));
+      }
+    }
+    cplx* sv_buf = nullptr;
+    for (size_t li = 0; li < sp.steps.size(); ++li) {
+      if (store) snapshot(st, P, sp.o_snap[li]);
+      for (const Step& s : sp.steps[li]) {
+        if (s.type == MOVE_R) {
+          const int c = s.site;
+          cplx* Q = store ? at(s.o_q) : pool.c((int64_t)4 * s.b * s.kq);
+          cplx* R = pool.c((int64_t)s.kq * s.bp);
+          qr_right(st, pool, P.a[c], 4 * s.b, s.bp, s.kq, Q, R, info);
+          cplx* nc_ = pool.c((int64_t)4 * s.b * s.kq);
+          TN_CUDA(cudaMemcpyAsync(nc_, Q, (size_t)4 * s.b * s.kq * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+          cplx* nx = pool.c((int64_t)s.kq * 4 * s.nb2);
+          nn(st, s.kq, 4 * s.nb2, s.bp, R, 0, P.a[c + 1], 0, nx, 0, 1);
+          P.a[c] = nc_;
+          P.a[c + 1] = nx;
+          P.b[c + 1] = s.kq;
+        } else if (s.type == MOVE_L) {
+          const int c = s.site;
+          cplx* Q = store ? at(s.o_q) : pool.c((int64_t)s.kq * 4 * s.bp);
+          cplx* L = pool.c((int64_t)s.b * s.kq);
+          lq_left(st, pool, P.a[c], s.b, 4 * s.bp, s.kq, Q, L, info);
+          cplx* nc_ = pool.c((int64_t)s.kq * 4 * s.bp);
+          TN_CUDA(cudaMemcpyAsync(nc_, Q, (size_t)s.kq * 4 * s.bp * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+          cplx* nx = pool.c((int64_t)s.nb2 * 4 * s.kq);
+          nn(st, s.nb2 * 4, s.kq, s.b, P.a[c - 1], 0, L, 0, nx, 0, 1);
+          P.a[c] = nc_;
+          P.a[c - 1] = nx;
+          P.b[c] = s.kq;
+        } else {
+          const int i = s.site;
+          const int64_t nth = (int64_t)16 * s.bl * s.br;
+          cplx* theta = store ? at(s.o_theta) : pool.c(nth);
+          nn(st, 4 * s.bl, 4 * s.br, s.m, P.a[i], 0, P.a[i + 1], 0, theta, 0, 1);
+          cplx* A = pool.c(nth);
+          apply_gate(st, A, 0, theta, 0, G + (int64_t)s.k * 16, 0, s.bl, s.br, 1, ONE, false);
+          // SVD of A (row-major 4bl x 4br) through its column-major view A^T (4br x 4bl):
+          // A^T = U' S V'^H  ->  A = conj(V') S U'^T, so Uh := U_r^H = V'^T (row-major r x 4bl view
+          // of V') and Vh := W_r^H = U'^T (row-major r x 4br view of U').
+          double* S = store ? at<double>(s.o_S) : (double*)pool.raw((size_t)s.mn * sizeof(double));
+          cplx* Up = pool.c((int64_t)4 * s.br * s.mn);
+          cplx* Vp = pool.c((int64_t)4 * s.bl * s.mn);
+          if (!sv_buf) sv_buf = pool.c(std::max(lwork_svd, 1));
+          TN_SOLVER(cusolverDnSetStream(solver, st));
+          TN_SOLVER(cusolverDnZgesvdj(solver, CUSOLVER_EIG_MODE_VECTOR, 1, 4 * s.br, 4 * s.bl, (cuDoubleComplex*)A,
+                                      4 * s.br, S, (cuDoubleComplex*)Up, 4 * s.br, (cuDoubleComplex*)Vp, 4 * s.bl,
+                                      (cuDoubleComplex*)sv_buf, lwork_svd, info + 1, svdj));
+          cplx* uh = store ? at(s.o_uh) : pool.c((int64_t)s.r * 4 * s.bl);
+          cplx* vh = store ? at(s.o_vh) : pool.c((int64_t)s.r * 4 * s.br);
+          TN_CUDA(cudaMemcpyAsync(uh, Vp, (size_t)s.r * 4 * s.bl * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+          TN_CUDA(cudaMemcpyAsync(vh, Up, (size_t)s.r * 4 * s.br * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+          double* sc = store ? at<double>(s.o_s) : (double*)pool.raw(sizeof(double));
+          svd_post(st, S, s.mn, s.r, sc, diag);
+          cplx* ni = pool.c((int64_t)4 * s.bl * s.r);
+          cplx* nj = pool.c((int64_t)s.r * 4 * s.br);
+          if (s.lr) {
+            conjT_scale_cols(st, ni, uh, s.r, 4 * s.bl, nullptr, nullptr);
+            scale_rows_sv(st, nj, vh, s.r, 4 * s.br, S, sc);
+          } else {
+            conjT_scale_cols(st, ni, uh, s.r, 4 * s.bl, S, sc);
+            TN_CUDA(cudaMemcpyAsync(nj, vh, (size_t)s.r * 4 * s.br * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+          }
+          P.a[i] = ni;
+          P.a[i + 1] = nj;
+          P.b[i + 1] = s.r;
+        }
+      }
+    }
+    if (store) snapshot(st, P, sp.o_snap.back());
+    return P;
+  }
+
+  void snapshot(cudaStream_t st, const Mps& P, const std::vector<size_t>& offs) {
+    for (int s = 0; s < n; ++s)
+      TN_CUDA(cudaMemcpyAsync(at(offs[s]), P.a[s], (size_t)P.b[s] * 4 * P.b[s + 1] * sizeof(cplx),
+                              cudaMemcpyDeviceToDevice, st));
+  }
+
+  // overlap <<top|bot>> as a 1x1 complex on device
+  cplx* overlap(cudaStream_t st, Pool& pool, const std::vector<const cplx*>& tp, const std::vector<int>& tb,
+                const std::vector<const cplx*>& bp, const std::vector<int>& bb) {
+    cplx* L = pool.c(1);
+    TN_CUDA(cudaMemcpyAsync(L, &ONE, sizeof(cplx), cudaMemcpyHostToDevice, st));
+    for (int s = 0; s < n; ++s) {
+      cplx* Y = pool.c((int64_t)tb[s] * 4 * bb[s + 1]);
+      nn(st, tb[s], 4 * bb[s + 1], bb[s], L, 0, bp[s], 0, Y, 0, 1);
+      cplx* L2 = pool.c((int64_t)tb[s + 1] * bb[s + 1]);
+      cn(st, tb[s + 1], bb[s + 1], 4 * tb[s], tp[s], 0, Y, 0, L2, 0, 1);
+      L = L2;
+    }
+    return L;
+  }
+
+  std::vector<const cplx*> snap_ptrs(const SidePlan& sp, int idx) const {
+    std::vector<const cplx*> v(n);
+    for (int s = 0; s < n; ++s) v[s] = at(sp.o_snap[idx][s]);
+    return v;
+  }
+
+  // Blocks of layer ell: (s, k) with k = -1 for an idle single site.
+  std::vector<std::pair<int, int>> blocks(int ell) const {
+    std::vector<std::pair<int, int>> out;
+    const auto& ly = layers[ell - 1];
+    size_t j = 0;
+    for (int s = 0; s < n;) {
+      if (j < ly.size() && ly[j].second == s) {
+        out.push_back({s, ly[j].first});
+        s += 2;
+        ++j;
+      } else {
+        out.push_back({s, -1});
+        s += 1;
+      }
+    }
+    return out;
+  }
+
+  void environments(cudaStream_t st, const cplx* gates, double* scalars, cplx* grad_R) {
+    TN_CUDA(cudaSetDevice(device));
+    primal_valid = false;
+    const double wc0 = work_counter;
+    Pool pool(st);
+    TN_CUDA(cudaMemcpyAsync(at(o_gates), gates, (size_t)K * 16 * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+    dagger4(st, at(o_gdag), at(o_gates), K);
+    const int n_info = 2;
+    int* info = (int*)pool.raw(n_info * sizeof(int));
+    TN_CUDA(cudaMemsetAsync(info, 0, n_info * sizeof(int), st));
+    double hdiag[8] = {0, 1.0, 0, 0, 0, 0, 0, 0};
+    TN_CUDA(cudaMemcpyAsync(at<double>(o_diag), hdiag, sizeof(hdiag), cudaMemcpyHostToDevice, st));
+    primal_side(st, pool, false, true, info, at<double>(o_diag));
+    primal_side(st, pool, true, true, info, at<double>(o_diag));
+    // T = <<T_0|B_0>>  (Alg. 1)
+    cplx* T11 = overlap(st, pool, snap_ptrs(top, D), top.snap[D].p, snap_ptrs(bot, 0), bot.snap[0].p);
+    finish_cost(st, at<double>(o_scal), T11);
+    layer_gradients(st, pool);
+    gradient_post(st, K, at(o_gates), at(o_E), at<double>(o_scal), at(o_gradf), grad_R);
+    // host copies: scalars/diag, frozen s, solver info
+    for (SidePlan* sp : {&bot, &top})
+      for (auto& ls : sp->steps)
+        for (Step& s : ls)
+          if (s.type == PAIR)
+            TN_CUDA(cudaMemcpyAsync(&h_s[s.s_index], at<double>(s.o_s), sizeof(double), cudaMemcpyDeviceToHost, st));
+    int hinfo[n_info];
+    TN_CUDA(cudaMemcpyAsync(hinfo, info, sizeof(hinfo), cudaMemcpyDeviceToHost, st));
+    double sc[8];
+    TN_CUDA(cudaMemcpyAsync(sc, at<double>(o_scal), 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    TN_CUDA(cudaMemcpyAsync(sc + 3, at<double>(o_diag), 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    TN_CUDA(cudaStreamSynchronize(st));
+    if (hinfo[0] != 0 || hinfo[1] != 0)
+      throw NumericError("cuSOLVER info nonzero (qr " + std::to_string(hinfo[0]) + ", svd " +
+                         std::to_string(hinfo[1]) + ")");
+    for (int j = 0; j < 6; ++j)
+      if (!std::isfinite(sc[j])) throw NumericError("non-finite primal scalar");
+    sc[6] = sc[7] = 0;
+    TN_CUDA(cudaMemcpyAsync(scalars, sc, 8 * sizeof(double), cudaMemcpyHostToDevice, st));
+    TN_CUDA(cudaMemcpyAsync(at<double>(o_scal), sc, 8 * sizeof(double), cudaMemcpyHostToDevice, st));
+    TN_CUDA(cudaStreamSynchronize(st));
+    work_primal = work_counter - wc0;
+    primal_valid = true;
+  }
+
+  // Two-site block of site tensors a (x,4,m), b (m,4,y): out (x,4,4,y)
+  void pair(cudaStream_t st, cplx* out, const cplx* a, int64_t sa, const cplx* b, int64_t sb, int x, int m, int y,
+            int batch) {
+    nn(st, 4 * x, 4 * y, m, a, sa, b, sb, out, (int64_t)16 * x * y, batch);
+  }
+
+  // a4: per layer right sweep, left sweep with E_k (primal envs stored for apply)
+  void layer_gradients(cudaStream_t st, Pool& pool) {
+    TN_CUDA(cudaMemsetAsync(at(o_E), 0, (size_t)K * 16 * sizeof(cplx), st));
+    for (int ell = 1; ell <= D; ++ell) {
+      const auto tp = snap_ptrs(top, D - ell);
+      const auto bp = snap_ptrs(bot, ell - 1);
+      const auto& tb = top.snap[D - ell].p;
+      const auto& bb = bot.snap[ell - 1].p;
+      const auto blks = blocks(ell);
+      TN_CUDA(cudaMemcpyAsync(at(o_L[ell][0]), &ONE, sizeof(cplx), cudaMemcpyHostToDevice, st));
+      TN_CUDA(cudaMemcpyAsync(at(o_R[ell][n]), &ONE, sizeof(cplx), cudaMemcpyHostToDevice, st));
+      // right sweep
+      for (int j = (int)blks.size() - 1; j >= 0; --j) {
+        const int s = blks[j].first, k = blks[j].second;
+        if (k < 0) {
+          cplx* Y = pool.c((int64_t)bb[s] * 4 * tb[s + 1]);
+          nn(st, 4 * bb[s], tb[s + 1], bb[s + 1], bp[s], 0, at(o_R[ell][s + 1]), 0, Y, 0, 1);
+          nc(st, bb[s], tb[s], 4 * tb[s + 1], Y, 0, tp[s], 0, at(o_R[ell][s]), 0, 1);
+        } else {
+          cplx* TB = pool.c((int64_t)16 * bb[s] * bb[s + 2]);
+          pair(st, TB, bp[s], 0, bp[s + 1], 0, bb[s], bb[s + 1], bb[s + 2], 1);
+          cplx* TT = pool.c((int64_t)16 * tb[s] * tb[s + 2]);
+          pair(st, TT, tp[s], 0, tp[s + 1], 0, tb[s], tb[s + 1], tb[s + 2], 1);
+          apply_gate(st, TT, 0, TT, 0, at(o_gdag) + (int64_t)k * 16, 0, tb[s], tb[s + 2], 1, ONE, false);
+          cplx* Y = pool.c((int64_t)16 * bb[s] * tb[s + 2]);
+          nn(st, 16 * bb[s], tb[s + 2], bb[s + 2], TB, 0, at(o_R[ell][s + 2]), 0, Y, 0, 1);
+          nc(st, bb[s], tb[s], 16 * tb[s + 2], Y, 0, TT, 0, at(o_R[ell][s]), 0, 1);
+        }
+      }
+      // left sweep + extraction
+      for (size_t j = 0; j < blks.size(); ++j) {
+        const int s = blks[j].first, k = blks[j].second;
+        if (k < 0) {
+          cplx* Y = pool.c((int64_t)tb[s] * 4 * bb[s + 1]);
+          nn(st, tb[s], 4 * bb[s + 1], bb[s], at(o_L[ell][s]), 0, bp[s], 0, Y, 0, 1);
+          cn(st, tb[s + 1], bb[s + 1], 4 * tb[s], tp[s], 0, Y, 0, at(o_L[ell][s + 1]), 0, 1);
+        } else {
+          cplx* TB = pool.c((int64_t)16 * bb[s] * bb[s + 2]);
+          pair(st, TB, bp[s], 0, bp[s + 1], 0, bb[s], bb[s + 1], bb[s + 2], 1);
+          cplx* TT = pool.c((int64_t)16 * tb[s] * tb[s + 2]);
+          pair(st, TT, tp[s], 0, tp[s + 1], 0, tb[s], tb[s + 1], tb[s + 2], 1);
+          cplx* Y = pool.c((int64_t)16 * tb[s] * bb[s + 2]);
+          nn(st, tb[s], 16 * bb[s + 2], bb[s], at(o_L[ell][s]), 0, TB, 0, Y, 0, 1);
+          cplx* Z = pool.c((int64_t)16 * tb[s] * tb[s + 2]);
+          nn(st, 16 * tb[s], tb[s + 2], bb[s + 2], Y, 0, at(o_R[ell][s + 2]), 0, Z, 0, 1);
+          extract_env(st, at(o_E) + (int64_t)k * 16, 0, TT, 0, Z, 0, tb[s], tb[s + 2], 1, ONE);
+          apply_gate(st, TT, 0, TT, 0, at(o_gdag) + (int64_t)k * 16, 0, tb[s], tb[s + 2], 1, ONE, false);
+          cn(st, tb[s + 2], bb[s + 2], 16 * tb[s], TT, 0, Y, 0, at(o_L[ell][s + 2]), 0, 1);
+        }
+      }
+    }
+  }
+
+  void cost(cudaStream_t st, const cplx* gates, double* scalars) {
+    TN_CUDA(cudaSetDevice(device));
+    Pool pool(st);
+    cplx* G = pool.c((int64_t)K * 16);
+    cplx* Gd = pool.c((int64_t)K * 16);
+    TN_CUDA(cudaMemcpyAsync(G, gates, (size_t)K * 16 * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+    dagger4(st, Gd, G, K);
+    // primal_side reads gates from the arena: swap in temporaries
+    cplx* saved = pool.c((int64_t)K * 16);
+    TN_CUDA(cudaMemcpyAsync(saved, at(o_gdag), (size_t)K * 16 * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+    TN_CUDA(cudaMemcpyAsync(at(o_gdag), Gd, (size_t)K * 16 * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+    int* info = (int*)pool.raw(2 * sizeof(int));
+    TN_CUDA(cudaMemsetAsync(info, 0, 2 * sizeof(int), st));
+    Mps T0 = primal_side(st, pool, true, false, info, nullptr);
+    TN_CUDA(cudaMemcpyAsync(at(o_gdag), saved, (size_t)K * 16 * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+    std::vector<const cplx*> tp(T0.a.begin(), T0.a.end());
+    std::vector<int> ones(n + 1, 1);
+    std::vector<const cplx*> bp(n);
+    cplx* id = pool.c(4);
+    const double h = 1.0 / std::sqrt(2.0);
+    cplx idh[4] = {{h, 0}, {0, 0}, {0, 0}, {h, 0}};
+    TN_CUDA(cudaMemcpyAsync(id, idh, sizeof(idh), cudaMemcpyHostToDevice, st));
+    for (int s = 0; s < n; ++s) bp[s] = id;
+    cplx* T11 = overlap(st, pool, tp, T0.b, bp, ones);
+    double* sc = (double*)pool.raw(8 * sizeof(double));
+    TN_CUDA(cudaMemsetAsync(sc, 0, 8 * sizeof(double), st));
+    finish_cost(st, sc, T11);
+    TN_CUDA(cudaMemcpyAsync(scalars, sc, 8 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    int hinfo[2];
+    TN_CUDA(cudaMemcpyAsync(hinfo, info, sizeof(hinfo), cudaMemcpyDeviceToHost, st));
+    TN_CUDA(cudaStreamSynchronize(st));
+    if (hinfo[0] != 0 || hinfo[1] != 0) throw NumericError("cuSOLVER info nonzero in tn_hvp_cost");
+  }
+
+  // ---------------------------------------------------- tangent pass --
+  struct Tangent {  // channel-form tangents for nb directions
+    std::vector<cplx*> Ab, Aa, B;  // B[s]: nb blocks, direction stride = size(B[s])
+    Bonds bd;                      // bonds: ab / aa used (p = primal)
+  };
+
+  int64_t bsize(const Bonds& b, int s) const { return (int64_t)b.ab[s] * 4 * b.aa[s + 1]; }
+
+  void tangent_init(cudaStream_t st, Pool& pool, Tangent& t, const SidePlan& sp, bool is_top, int nb) {
+    t.bd = sp.init;
+    t.Ab.assign(n, nullptr);
+    t.Aa.assign(n, nullptr);
+    t.B.assign(n, nullptr);
+    for (int s = 0; s < n; ++s) {
+      const int64_t e = (int64_t)t.bd.p[s] * 4 * t.bd.p[s + 1];
+      t.Ab[s] = pool.c(e);
+      t.Aa[s] = pool.c(e);
+      const cplx* src = is_top ? ref + ref_off[s] : nullptr;
+      if (is_top) {
+        TN_CUDA(cudaMemcpyAsync(t.Ab[s], src, e * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+        TN_CUDA(cudaMemcpyAsync(t.Aa[s], src, e * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+      } else {
+        const double h = 1.0 / std::sqrt(2.0);
+        cplx id[4] = {{h, 0}, {0, 0}, {0, 0}, {h, 0}};
+        TN_CUDA(cudaMemcpyAsync(t.Ab[s], id, sizeof(id), cudaMemcpyHostToDevice, st));
+        TN_CUDA(cudaMemcpyAsync(t.Aa[s], id, sizeof(id), cudaMemcpyHostToDevice, st));
+      }
+      t.B[s] = pool.c(e * nb);
+      TN_CUDA(cudaMemsetAsync(t.B[s], 0, (size_t)e * nb * sizeof(cplx), st));
+    }
+  }
+
+  // One replayed step on a batch of tangents.  M: gate array (G or G^dag),
+  // VM: per-direction gate variations [nb][K][16] (V or V^dag).
+  void tangent_step(cudaStream_t st, Pool& pool, Tangent& t, const Step& s, const cplx* M, const cplx* VM, int nb) {
+    const int64_t KK = (int64_t)K * 16;
+    if (s.type == MOVE_R) {
+      const int c = s.site, b = s.b, kq = s.kq;
+      const int ab1 = s.ab1, ab2 = s.ab2, aa1 = s.aa1, aa2 = s.aa2;
+      const cplx* Q = at(s.o_q);                        // (4b x kq)
+      cplx* X = pool.c((int64_t)kq * ab1);              // Q^H Ab_c
+      cn(st, kq, ab1, 4 * b, Q, 0, t.Ab[c], 0, X, 0, 1);
+      cplx* nAbc = pool.c((int64_t)4 * b * kq);
+      TN_CUDA(cudaMemcpyAsync(nAbc, Q, (size_t)4 * b * kq * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+      cplx* nAb1 = pool.c((int64_t)kq * 4 * ab2);
+      nn(st, kq, 4 * ab2, ab1, X, 0, t.Ab[c + 1], 0, nAb1, 0, 1);
+      // blocks: B_c (b,4,aa1), B_{c+1} (ab1,4,aa2)
+      const int64_t sc0 = (int64_t)4 * b * aa1, sc1o = (int64_t)ab1 * 4 * aa2, sc1n = (int64_t)kq * 4 * aa2;
+      cplx* Y = pool.c((int64_t)kq * aa1 * nb);
+      cn(st, kq, aa1, 4 * b, Q, 0, t.B[c], sc0, Y, (int64_t)kq * aa1, nb);
+      nn(st, 4 * b, aa1, kq, Q, 0, Y, (int64_t)kq * aa1, t.B[c], sc0, nb, MONE, ONE);
+      cplx* nB1 = pool.c(sc1n * nb);
+      nn(st, kq, 4 * aa2, ab1, X, 0, t.B[c + 1], sc1o, nB1, sc1n, nb);
+      nn(st, kq, 4 * aa2, aa1, Y, (int64_t)kq * aa1, t.Aa[c + 1], 0, nB1, sc1n, nb, ONE, ONE);
+      t.Ab[c] = nAbc;
+      t.Ab[c + 1] = nAb1;
+      t.B[c + 1] = nB1;
+      t.bd.p[c + 1] = kq;
+      t.bd.ab[c + 1] = kq;
+    } else if (s.type == MOVE_L) {
+      const int c = s.site, bp = s.bp, kq = s.kq;
+      const int aa0 = s.aa0, aam = s.aam, ab0 = s.ab0, abm = s.abm;
+      const cplx* Q = at(s.o_q);                        // (kq x 4bp)
+      cplx* X = pool.c((int64_t)aa0 * kq);              // Aa_c Q^H
+      nc(st, aa0, kq, 4 * bp, t.Aa[c], 0, Q, 0, X, 0, 1);
+      cplx* nAac = pool.c((int64_t)kq * 4 * bp);
+      TN_CUDA(cudaMemcpyAsync(nAac, Q, (size_t)kq * 4 * bp * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+      cplx* nAam = pool.c((int64_t)aam * 4 * kq);
+      nn(st, aam * 4, kq, aa0, t.Aa[c - 1], 0, X, 0, nAam, 0, 1);
+      // blocks: B_c (ab0,4,bp), B_{c-1} (abm,4,aa0)
+      const int64_t sc0 = (int64_t)ab0 * 4 * bp, sm_o = (int64_t)abm * 4 * aa0, sm_n = (int64_t)abm * 4 * kq;
+      cplx* Y = pool.c((int64_t)ab0 * kq * nb);
+      nc(st, ab0, kq, 4 * bp, t.B[c], sc0, Q, 0, Y, (int64_t)ab0 * kq, nb);
+      nn(st, ab0, 4 * bp, kq, Y, (int64_t)ab0 * kq, Q, 0, t.B[c], sc0, nb, MONE, ONE);
+      cplx* nBm = pool.c(sm_n * nb);
+      nn(st, abm * 4, kq, aa0, t.B[c - 1], sm_o, X, 0, nBm, sm_n, nb);
+      nn(st, abm * 4, kq, ab0, t.Ab[c - 1], 0, Y, (int64_t)ab0 * kq, nBm, sm_n, nb, ONE, ONE);
+      t.Aa[c] = nAac;
+      t.Aa[c - 1] = nAam;
+      t.B[c - 1] = nBm;
+      t.bd.p[c] = kq;
+      t.bd.aa[c] = kq;
+    } else {
+      const int i = s.site, bl = s.bl, br = s.br, r = s.r;
+      const int ab1 = s.ab1, ab2 = s.ab2, aa0 = s.aa0, aa1 = s.aa1;
+      const double sc = h_s[s.s_index];
+      const cplx csc = {sc, 0.0}, cmsc = {-sc, 0.0};
+      const cplx* theta = at(s.o_theta);
+      const cplx* uh = at(s.o_uh);  // (r x 4bl)
+      const cplx* vh = at(s.o_vh);  // (r x 4br)
+      const cplx* Mk = M + (int64_t)s.k * 16;
+      const int64_t nD = (int64_t)16 * bl * br;
+      // DTheta = M (B_i Aa_{i+1} + Ab_i B_{i+1}) + V_M Theta
+      cplx* Dt = pool.c(nD * nb);
+      nn(st, 4 * bl, 4 * br, aa1, t.B[i], (int64_t)4 * bl * aa1, t.Aa[i + 1], 0, Dt, nD, nb);
+      nn(st, 4 * bl, 4 * br, ab1, t.Ab[i], 0, t.B[i + 1], (int64_t)ab1 * 4 * br, Dt, nD, nb, ONE, ONE);
+      apply_gate(st, Dt, nD, Dt, nD, Mk, 0, bl, br, nb, ONE, false);
+      apply_gate(st, Dt, nD, theta, 0, VM + (int64_t)s.k * 16, KK, bl, br, nb, ONE, true);
+      const int64_t sUD = (int64_t)r * 4 * br, sZ = (int64_t)4 * bl * r, sRR = (int64_t)r * r;
+      cplx* UD = pool.c(sUD * nb);
+      nn(st, r, 4 * br, 4 * bl, uh, 0, Dt, nD, UD, sUD, nb);  // U^H D (uh is U^H, r x 4bl)
+      cplx* Z = pool.c(sZ * nb);
+      nc(st, 4 * bl, r, 4 * br, Dt, nD, vh, 0, Z, sZ, nb);  // D W = D vh^H
+      cplx* nBi = pool.c(sZ * nb);
+      cplx* nBj = pool.c(sUD * nb);
+      if (s.lr) {
+        // B_{i+1} = s U^H D ; B_i = s (D W - U (U^H D W))
+        cplx* UDW = pool.c(sRR * nb);
+        nc(st, r, r, 4 * br, UD, sUD, vh, 0, UDW, sRR, nb);
+        TN_CUDA(cudaMemcpyAsync(nBi, Z, (size_t)sZ * nb * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+        cn(st, 4 * bl, r, r, uh, 0, UDW, sRR, nBi, sZ, nb, cmsc, csc);
+        axpby(st, nBj, UD, csc, ZERO, sUD * nb);
+      } else {
+        // B_i = s D W ; B_{i+1} = s (U^H D - (U^H D W) W^H)
+        cplx* UDW = pool.c(sRR * nb);
+        nn(st, r, r, 4 * bl, uh, 0, Z, sZ, UDW, sRR, nb);
+        TN_CUDA(cudaMemcpyAsync(nBj, UD, (size_t)sUD * nb * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+        nn(st, r, 4 * br, r, UDW, sRR, vh, 0, nBj, sUD, nb, cmsc, csc);
+        axpby(st, nBi, Z, csc, ZERO, sZ * nb);
+      }
+      // chains
+      cplx* aa2t = pool.c((int64_t)16 * aa0 * br);
+      nn(st, 4 * aa0, 4 * br, aa1, t.Aa[i], 0, t.Aa[i + 1], 0, aa2t, 0, 1);
+      apply_gate(st, aa2t, 0, aa2t, 0, Mk, 0, aa0, br, 1, ONE, false);
+      cplx* nAai = pool.c((int64_t)4 * aa0 * r);
+      nc(st, 4 * aa0, r, 4 * br, aa2t, 0, vh, 0, nAai, 0, 1, csc);
+      cplx* nAaj = pool.c((int64_t)r * 4 * br);
+      TN_CUDA(cudaMemcpyAsync(nAaj, vh, (size_t)r * 4 * br * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+      cplx* ab2t = pool.c((int64_t)16 * bl * ab2);
+      nn(st, 4 * bl, 4 * ab2, ab1, t.Ab[i], 0, t.Ab[i + 1], 0, ab2t, 0, 1);
+      apply_gate(st, ab2t, 0, ab2t, 0, Mk, 0, bl, ab2, 1, ONE, false);
+      cplx* nAbj = pool.c((int64_t)r * 4 * ab2);
+      nn(st, r, 4 * ab2, 4 * bl, uh, 0, ab2t, 0, nAbj, 0, 1, csc);
+      cplx* nAbi = pool.c((int64_t)4 * bl * r);
+      conjT_scale_cols(st, nAbi, uh, r, 4 * bl, nullptr, nullptr);
+      t.Aa[i] = nAai;
+      t.Aa[i + 1] = nAaj;
+      t.Ab[i] = nAbi;
+      t.Ab[i + 1] = nAbj;
+      t.B[i] = nBi;
+      t.B[i + 1] = nBj;
+      t.bd.p[i + 1] = r;
+      t.bd.ab[i + 1] = r;
+      t.bd.aa[i + 1] = r;
+    }
+  }
+
+  struct TanSnap {
+    std::vector<cplx*> Ab, Aa, B;
+    Bonds bd;
+  };
+
+  TanSnap take_snapshot(cudaStream_t st, Pool& pool, const Tangent& t, int nb) {
+    TanSnap sn;
+    sn.bd = t.bd;
+    sn.Ab.resize(n);
+    sn.Aa.resize(n);
+    sn.B.resize(n);
+    for (int s = 0; s < n; ++s) {
+      const int64_t eb = (int64_t)t.bd.ab[s] * 4 * t.bd.ab[s + 1];
+      const int64_t ea = (int64_t)t.bd.aa[s] * 4 * t.bd.aa[s + 1];
+      const int64_t e = bsize(t.bd, s) * nb;
+      sn.Ab[s] = pool.c(eb);
+      sn.Aa[s] = pool.c(ea);
+      sn.B[s] = pool.c(e);
+      TN_CUDA(cudaMemcpyAsync(sn.Ab[s], t.Ab[s], eb * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+      TN_CUDA(cudaMemcpyAsync(sn.Aa[s], t.Aa[s], ea * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+      TN_CUDA(cudaMemcpyAsync(sn.B[s], t.B[s], e * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+    }
+    return sn;
+  }
+
+  // Shared left env sweep: Lout[c] for every block boundary, Lout[0] = 1.
+  // top side tensors (tp, bonds tb) gated per gate block with Gd; bottom (bp, bb).
+  void shared_left(cudaStream_t st, Pool& pool, int ell, std::vector<cplx*>& L, const std::vector<const cplx*>& tp,
+                   const std::vector<int>& tb, const std::vector<const cplx*>& bp, const std::vector<int>& bb) {
+    L.assign(n + 1, nullptr);
+    L[0] = pool.c(1);
+    TN_CUDA(cudaMemcpyAsync(L[0], &ONE, sizeof(cplx), cudaMemcpyHostToDevice, st));
+    for (auto [s, k] : blocks(ell)) {
+      const int w = k < 0 ? 4 : 16, e = k < 0 ? s + 1 : s + 2;
+      const cplx* TB = bp[s];
+      const cplx* TT = tp[s];
+      if (k >= 0) {
+        cplx* tbk = pool.c((int64_t)16 * bb[s] * bb[e]);
+        pair(st, tbk, bp[s], 0, bp[s + 1], 0, bb[s], bb[s + 1], bb[e], 1);
+        cplx* ttk = pool.c((int64_t)16 * tb[s] * tb[e]);
+        pair(st, ttk, tp[s], 0, tp[s + 1], 0, tb[s], tb[s + 1], tb[e], 1);
+        apply_gate(st, ttk, 0, ttk, 0, at(o_gdag) + (int64_t)k * 16, 0, tb[s], tb[e], 1, ONE, false);
+        TB = tbk;
+        TT = ttk;
+      }
+      cplx* Y = pool.c((int64_t)tb[s] * w * bb[e]);
+      nn(st, tb[s], w * bb[e], bb[s], L[s], 0, TB, 0, Y, 0, 1);
+      L[e] = pool.c((int64_t)tb[e] * bb[e]);
+      cn(st, tb[e], bb[e], w * tb[s], TT, 0, Y, 0, L[e], 0, 1);
+    }
+  }
+
+  void shared_right(cudaStream_t st, Pool& pool, int ell, std::vector<cplx*>& R, const std::vector<const cplx*>& tp,
+                    const std::vector<int>& tb, const std::vector<const cplx*>& bp, const std::vector<int>& bb) {
+    R.assign(n + 1, nullptr);
+    R[n] = pool.c(1);
+    TN_CUDA(cudaMemcpyAsync(R[n], &ONE, sizeof(cplx), cudaMemcpyHostToDevice, st));
+    auto blks = blocks(ell);
+    for (int j = (int)blks.size() - 1; j >= 0; --j) {
+      const int s = blks[j].first, k = blks[j].second;
+      const int w = k < 0 ? 4 : 16, e = k < 0 ? s + 1 : s + 2;
+      const cplx* TB = bp[s];
+      const cplx* TT = tp[s];
+      if (k >= 0) {
+        cplx* tbk = pool.c((int64_t)16 * bb[s] * bb[e]);
+        pair(st, tbk, bp[s], 0, bp[s + 1], 0, bb[s], bb[s + 1], bb[e], 1);
+        cplx* ttk = pool.c((int64_t)16 * tb[s] * tb[e]);
+        pair(st, ttk, tp[s], 0, tp[s + 1], 0, tb[s], tb[s + 1], tb[e], 1);
+        apply_gate(st, ttk, 0, ttk, 0, at(o_gdag) + (int64_t)k * 16, 0, tb[s], tb[e], 1, ONE, false);
+        TB = tbk;
+        TT = ttk;
+      }
+      cplx* Y = pool.c((int64_t)bb[s] * w * tb[e]);
+      nn(st, w * bb[s], tb[e], bb[e], TB, 0, R[e], 0, Y, 0, 1);
+      R[s] = pool.c((int64_t)bb[s] * tb[s]);
+      nc(st, bb[s], tb[s], w * tb[e], Y, 0, TT, 0, R[s], 0, 1);
+    }
+  }
+
+  // H_T contributions of layer ell (all three channels) for nb directions.
+  void layer_hvp(cudaStream_t st, Pool& pool, int ell, const TanSnap& DBs, const Tangent& DT, const cplx* V,
+                 cplx* HT, int nb, bool skipB, bool skipT) {
+    const auto tpv = snap_ptrs(top, D - ell);
+    const auto bpv = snap_ptrs(bot, ell - 1);
+    const auto& tb = top.snap[D - ell].p;
+    const auto& bb = bot.snap[ell - 1].p;
+    const auto& xb = DBs.bd.ab;  // bottom before-chain bonds
+    const auto& ya = DBs.bd.aa;  // bottom after-chain bonds
+    const auto& ub = DT.bd.ab;   // top before-chain bonds
+    const auto& va = DT.bd.aa;   // top after-chain bonds
+    std::vector<const cplx*> BAb(DBs.Ab.begin(), DBs.Ab.end()), BAa(DBs.Aa.begin(), DBs.Aa.end());
+    std::vector<const cplx*> TAb(DT.Ab.begin(), DT.Ab.end()), TAa(DT.Aa.begin(), DT.Aa.end());
+    const int64_t KK = (int64_t)K * 16;
+    // shared chain environments
+    std::vector<cplx*> LBb, RBa, LTb, RTa;
+    if (!skipB) {
+      shared_left(st, pool, ell, LBb, tpv, tb, BAb, xb);
+      shared_right(st, pool, ell, RBa, tpv, tb, BAa, ya);
+    }
+    if (!skipT) {
+      shared_left(st, pool, ell, LTb, TAb, ub, bpv, bb);
+      shared_right(st, pool, ell, RTa, TAa, va, bpv, bb);
+    }
+    auto blks = blocks(ell);
+    // per-direction right environments at every block boundary
+    std::vector<cplx*> dRB(n + 1, nullptr), dRT(n + 1, nullptr), dRV(n + 1, nullptr);
+    auto zero1 = [&](int64_t e) {
+      cplx* p = pool.c(e * nb);
+      TN_CUDA(cudaMemsetAsync(p, 0, (size_t)e * nb * sizeof(cplx), st));
+      return p;
+    };
+    dRV[n] = zero1(1);
+    if (!skipB) dRB[n] = zero1(1);
+    if (!skipT) dRT[n] = zero1(1);
+    // block tensors cache (per block start site)
+    struct Blk {
+      cplx *TT = nullptr, *TTg = nullptr, *BB = nullptr;          // primal blocks (TTg gated with G^dag)
+      cplx *BAaB = nullptr, *BAbB = nullptr, *BBd = nullptr;       // bottom chains + per-dir block
+      cplx *TAaB = nullptr, *TAaG = nullptr, *TAbB = nullptr, *TAbG = nullptr, *TBd = nullptr, *TBdG = nullptr;
+    };
+    std::vector<Blk> bk(n);
+    for (auto [s, k] : blks) {
+      Blk& q = bk[s];
+      const int e = k < 0 ? s + 1 : s + 2;
+      const int w = k < 0 ? 4 : 16;
+      auto mk2 = [&](const std::vector<const cplx*>& a, const std::vector<int>& bd) -> cplx* {
+        if (k < 0) return const_cast<cplx*>(a[s]);
+        cplx* o = pool.c((int64_t)16 * bd[s] * bd[e]);
+        pair(st, o, a[s], 0, a[s + 1], 0, bd[s], bd[s + 1], bd[e], 1);
+        return o;
+      };
+      auto gated = [&](const cplx* x, int X, int Y) -> cplx* {
+        if (k < 0) return const_cast<cplx*>(x);
+        cplx* o = pool.c((int64_t)16 * X * Y);
+        apply_gate(st, o, 0, x, 0, at(o_gdag) + (int64_t)k * 16, 0, X, Y, 1, ONE, false);
+        return o;
+      };
+      q.TT = mk2(tpv, tb);
+      q.TTg = gated(q.TT, tb[s], tb[e]);
+      q.BB = mk2(bpv, bb);
+      if (!skipB) {
+        q.BAaB = mk2(BAa, ya);
+        q.BAbB = mk2(BAb, xb);
+        const int64_t sz = (int64_t)w * xb[s] * ya[e];
+        q.BBd = pool.c(sz * nb);
+        if (k < 0) {
+          TN_CUDA(cudaMemcpyAsync(q.BBd, DBs.B[s], sz * nb * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+        } else {
+          nn(st, 4 * xb[s], 4 * ya[e], ya[s + 1], DBs.B[s], bsize(DBs.bd, s), BAa[s + 1], 0, q.BBd, sz, nb);
+          nn(st, 4 * xb[s], 4 * ya[e], xb[s + 1], BAb[s], 0, DBs.B[s + 1], bsize(DBs.bd, s + 1), q.BBd, sz, nb,
+             ONE, ONE);
+        }
+      }
+      if (!skipT) {
+        q.TAaB = mk2(TAa, va);
+        q.TAaG = gated(q.TAaB, va[s], va[e]);
+        q.TAbB = mk2(TAb, ub);
+        q.TAbG = gated(q.TAbB, ub[s], ub[e]);
+        const int64_t sz = (int64_t)w * ub[s] * va[e];
+        q.TBd = pool.c(sz * nb);
+        if (k < 0) {
+          TN_CUDA(cudaMemcpyAsync(q.TBd, DT.B[s], sz * nb * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+          q.TBdG = q.TBd;
+        } else {
+          nn(st, 4 * ub[s], 4 * va[e], va[s + 1], DT.B[s], bsize(DT.bd, s), TAa[s + 1], 0, q.TBd, sz, nb);
+          nn(st, 4 * ub[s], 4 * va[e], ub[s + 1], TAb[s], 0, DT.B[s + 1], bsize(DT.bd, s + 1), q.TBd, sz, nb, ONE,
+             ONE);
+          q.TBdG = pool.c(sz * nb);
+          apply_gate(st, q.TBdG, sz, q.TBd, sz, at(o_gdag) + (int64_t)k * 16, 0, ub[s], va[e], nb, ONE, false);
+        }
+      }
+    }
+    const cplx* Vd = V;  // [nb][K][16]
+    // ---------------- right sweep (per direction)
+    for (int j = (int)blks.size() - 1; j >= 0; --j) {
+      const int s = blks[j].first, k = blks[j].second;
+      const int w = k < 0 ? 4 : 16, e = k < 0 ? s + 1 : s + 2;
+      Blk& q = bk[s];
+      const cplx* R0e = at(o_R[ell][e]);
+      // V channel: dRV[s] = (BB dRV[e] + [V] BB R0[e]) TTg^H   (V replaces G: top ungated)
+      {
+        const int64_t sY = (int64_t)bb[s] * w * tb[e];
+        cplx* Y = pool.c(sY * nb);
+        nn(st, w * bb[s], tb[e], bb[e], q.BB, 0, dRV[e], (int64_t)bb[e] * tb[e], Y, sY, nb);
+        dRV[s] = pool.c((int64_t)bb[s] * tb[s] * nb);
+        nc(st, bb[s], tb[s], w * tb[e], Y, sY, q.TTg, 0, dRV[s], (int64_t)bb[s] * tb[s], nb);
+        if (k >= 0) {
+          cplx* Y0 = pool.c(sY);
+          nn(st, w * bb[s], tb[e], bb[e], q.BB, 0, R0e, 0, Y0, 0, 1);
+          cplx* YV = pool.c(sY * nb);
+          apply_gate(st, YV, sY, Y0, 0, Vd + (int64_t)k * 16, KK, bb[s], tb[e], nb, ONE, false);
+          nc(st, bb[s], tb[s], w * tb[e], YV, sY, q.TT, 0, dRV[s], (int64_t)bb[s] * tb[s], nb, ONE, ONE);
+        }
+      }
+      if (!skipB) {  // dRB[s] = (BAbB dRB[e] + BBd RBa[e]) TTg^H
+        const int64_t sY = (int64_t)xb[s] * w * tb[e];
+        cplx* Y = pool.c(sY * nb);
+        nn(st, w * xb[s], tb[e], xb[e], q.BAbB, 0, dRB[e], (int64_t)xb[e] * tb[e], Y, sY, nb);
+        nn(st, w * xb[s], tb[e], ya[e], q.BBd, (int64_t)w * xb[s] * ya[e], RBa[e], 0, Y, sY, nb, ONE, ONE);
+        dRB[s] = pool.c((int64_t)xb[s] * tb[s] * nb);
+        nc(st, xb[s], tb[s], w * tb[e], Y, sY, q.TTg, 0, dRB[s], (int64_t)xb[s] * tb[s], nb);
+      }
+      if (!skipT) {  // dRT[s] = (BB dRT[e]) TAbG^H + (BB RTa[e]) TBdG^H
+        const int64_t sY = (int64_t)bb[s] * w * ub[e];
+        cplx* Y = pool.c(sY * nb);
+        nn(st, w * bb[s], ub[e], bb[e], q.BB, 0, dRT[e], (int64_t)bb[e] * ub[e], Y, sY, nb);
+        dRT[s] = pool.c((int64_t)bb[s] * ub[s] * nb);
+        nc(st, bb[s], ub[s], w * ub[e], Y, sY, q.TAbG, 0, dRT[s], (int64_t)bb[s] * ub[s], nb);
+        const int64_t sY2 = (int64_t)bb[s] * w * va[e];
+        cplx* Y2 = pool.c(sY2);
+        nn(st, w * bb[s], va[e], bb[e], q.BB, 0, RTa[e], 0, Y2, 0, 1);
+        nc(st, bb[s], ub[s], w * va[e], Y2, 0, q.TBdG, (int64_t)w * ub[s] * va[e], dRT[s], (int64_t)bb[s] * ub[s],
+           nb, ONE, ONE);
+      }
+    }
+    // ---------------- left sweep with extraction
+    cplx* dLV = zero1(1);
+    cplx* dLB = skipB ? nullptr : zero1(1);
+    cplx* dLT = skipT ? nullptr : zero1(1);
+    for (auto [s, k] : blks) {
+      const int w = k < 0 ? 4 : 16, e = k < 0 ? s + 1 : s + 2;
+      Blk& q = bk[s];
+      const cplx* L0s = at(o_L[ell][s]);
+      const cplx* R0e = at(o_R[ell][e]);
+      // Y tensors (open gate, bottom side), per direction, top-index rows: (t x w x b')
+      const int64_t sYV = (int64_t)tb[s] * w * bb[e];
+      cplx* YV = pool.c(sYV * nb);  // dLV BB
+      nn(st, tb[s], w * bb[e], bb[s], dLV, (int64_t)tb[s] * bb[s], q.BB, 0, YV, sYV, nb);
+      cplx* Y0 = nullptr;  // L0 BB (shared)
+      if (k >= 0) {
+        Y0 = pool.c(sYV);
+        nn(st, tb[s], w * bb[e], bb[s], L0s, 0, q.BB, 0, Y0, 0, 1);
+      }
+      cplx* YB = nullptr;
+      int64_t sYB = 0;
+      if (!skipB) {  // dLB BAaB + LBb BBd : (t x w x ya')
+        sYB = (int64_t)tb[s] * w * ya[e];
+        YB = pool.c(sYB * nb);
+        nn(st, tb[s], w * ya[e], ya[s], dLB, (int64_t)tb[s] * ya[s], q.BAaB, 0, YB, sYB, nb);
+        nn(st, tb[s], w * ya[e], xb[s], LBb[s], 0, q.BBd, (int64_t)w * xb[s] * ya[e], YB, sYB, nb, ONE, ONE);
+      }
+      cplx* YT = nullptr;
+      cplx* YT0 = nullptr;
+      int64_t sYT = 0;
+      if (!skipT) {  // dLT BB : (va x w x b') ; LTb BB (shared) : (ub x w x b')
+        sYT = (int64_t)va[s] * w * bb[e];
+        YT = pool.c(sYT * nb);
+        nn(st, va[s], w * bb[e], bb[s], dLT, (int64_t)va[s] * bb[s], q.BB, 0, YT, sYT, nb);
+        YT0 = pool.c((int64_t)ub[s] * w * bb[e]);
+        nn(st, ub[s], w * bb[e], bb[s], LTb[s], 0, q.BB, 0, YT0, 0, 1);
+      }
+      if (k >= 0) {
+        // ---- extraction: top TT
+        const int64_t sZ = (int64_t)16 * tb[s] * tb[e];
+        cplx* Z = pool.c(sZ * nb);
+        nn(st, 16 * tb[s], tb[e], bb[e], YV, sYV, R0e, 0, Z, sZ, nb);
+        nn(st, 16 * tb[s], tb[e], bb[e], Y0, 0, dRV[e], (int64_t)bb[e] * tb[e], Z, sZ, nb, ONE, ONE);
+        if (!skipB) {
+          nn(st, 16 * tb[s], tb[e], ya[e], YB, sYB, RBa[e], 0, Z, sZ, nb, ONE, ONE);
+          cplx* LBA = pool.c((int64_t)16 * tb[s] * xb[e]);
+          nn(st, tb[s], 16 * xb[e], xb[s], LBb[s], 0, q.BAbB, 0, LBA, 0, 1);
+          nn(st, 16 * tb[s], tb[e], xb[e], LBA, 0, dRB[e], (int64_t)xb[e] * tb[e], Z, sZ, nb, ONE, ONE);
+        }
+        extract_env(st, HT + (int64_t)k * 16, KK, q.TT, 0, Z, sZ, tb[s], tb[e], nb, ONE);
+        if (!skipT) {
+          // top TAaB with (dLT BB) RTa
+          const int64_t sZ2 = (int64_t)16 * va[s] * va[e];
+          cplx* Z2 = pool.c(sZ2 * nb);
+          nn(st, 16 * va[s], va[e], bb[e], YT, sYT, RTa[e], 0, Z2, sZ2, nb);
+          extract_env(st, HT + (int64_t)k * 16, KK, q.TAaB, 0, Z2, sZ2, va[s], va[e], nb, ONE);
+          // per-dir top TBd with shared (LTb BB) RTa
+          const int64_t sZ3 = (int64_t)16 * ub[s] * va[e];
+          cplx* Z3 = pool.c(sZ3);
+          nn(st, 16 * ub[s], va[e], bb[e], YT0, 0, RTa[e], 0, Z3, 0, 1);
+          extract_env(st, HT + (int64_t)k * 16, KK, q.TBd, sZ3, Z3, 0, ub[s], va[e], nb, ONE);
+          // top TAbB with (LTb BB) dRT
+          const int64_t sZ4 = (int64_t)16 * ub[s] * ub[e];
+          cplx* Z4 = pool.c(sZ4 * nb);
+          nn(st, 16 * ub[s], ub[e], bb[e], YT0, 0, dRT[e], (int64_t)bb[e] * ub[e], Z4, sZ4, nb);
+          extract_env(st, HT + (int64_t)k * 16, KK, q.TAbB, 0, Z4, sZ4, ub[s], ub[e], nb, ONE);
+        }
+      }
+      // ---- left updates
+      {  // dLV' = TT^H (G YV + V Y0)  ==  TTg^H YV + TT^H (V Y0)
+        cplx* nL = pool.c((int64_t)tb[e] * bb[e] * nb);
+        cn(st, tb[e], bb[e], w * tb[s], q.TTg, 0, YV, sYV, nL, (int64_t)tb[e] * bb[e], nb);
+        if (k >= 0) {
+          cplx* YVV = pool.c(sYV * nb);
+          apply_gate(st, YVV, sYV, Y0, 0, Vd + (int64_t)k * 16, KK, tb[s], bb[e], nb, ONE, false);
+          cn(st, tb[e], bb[e], w * tb[s], q.TT, 0, YVV, sYV, nL, (int64_t)tb[e] * bb[e], nb, ONE, ONE);
+        }
+        dLV = nL;
+      }
+      if (!skipB) {
+        cplx* nL = pool.c((int64_t)tb[e] * ya[e] * nb);
+        cn(st, tb[e], ya[e], w * tb[s], q.TTg, 0, YB, sYB, nL, (int64_t)tb[e] * ya[e], nb);
+        dLB = nL;
+      }
+      if (!skipT) {
+        cplx* nL = pool.c((int64_t)va[e] * bb[e] * nb);
+        cn(st, va[e], bb[e], w * va[s], q.TAaG, 0, YT, sYT, nL, (int64_t)va[e] * bb[e], nb);
+        cn(st, va[e], bb[e], w * ub[s], q.TBdG, (int64_t)w * ub[s] * va[e], YT0, 0, nL, (int64_t)va[e] * bb[e], nb,
+           ONE, ONE);
+        dLT = nL;
+      }
+    }
+  }
+
+  void apply(cudaStream_t st, int batch, const cplx* dirs, cplx* hess, cplx* aux) {
+    TN_CUDA(cudaSetDevice(device));
+    if (!primal_valid) throw StateError("tn_hvp_apply before tn_hvp_environments");
+    const double wc0 = work_counter;
+    const int64_t KK = (int64_t)K * 16;
+    for (int b0 = 0; b0 < batch; b0 += cfg.max_batch) {
+      const int nb = std::min(cfg.max_batch, batch - b0);
+      Pool pool(st);
+      const cplx* V = dirs + (int64_t)b0 * KK;
+      cplx* Vd = pool.c(KK * nb);
+      dagger4(st, Vd, V, (int64_t)K * nb);
+      cplx* HT = pool.c(KK * nb);
+      TN_CUDA(cudaMemsetAsync(HT, 0, (size_t)KK * nb * sizeof(cplx), st));
+      // forward (bottom) tangent, cached per layer: DB_{ell-1}
+      std::vector<TanSnap> DB(D);
+      {
+        Tangent t;
+        tangent_init(st, pool, t, bot, false, nb);
+        for (size_t li = 0; li < bot.steps.size(); ++li) {
+          DB[li] = take_snapshot(st, pool, t, nb);
+          for (const Step& s : bot.steps[li]) tangent_step(st, pool, t, s, at(o_gates), V, nb);
+        }
+      }
+      // backward (top) tangent on the fly + layer HVP extraction
+      Tangent t;
+      tangent_init(st, pool, t, top, true, nb);
+      for (size_t li = 0; li < top.steps.size(); ++li) {
+        const int ell = top.ell[li];
+        layer_hvp(st, pool, ell, DB[ell - 1], t, V, HT, nb, ell == 1, li == 0);
+        for (const Step& s : top.steps[li]) tangent_step(st, pool, t, s, at(o_gdag), Vd, nb);
+      }
+      cplx* om = pool.c(nb);
+      hessian_post(st, K, nb, at(o_gates), at(o_E), at(o_gradf), at<double>(o_scal), HT, V, om,
+                   hess + (int64_t)b0 * KK);
+      if (aux) {
+        TN_CUDA(cudaMemcpyAsync(aux + (int64_t)b0 * KK, HT, (size_t)KK * nb * sizeof(cplx), cudaMemcpyDeviceToDevice,
+                                st));
+        TN_CUDA(cudaMemcpyAsync(aux + (int64_t)batch * KK + b0, om, (size_t)nb * sizeof(cplx),
+                                cudaMemcpyDeviceToDevice, st));
+      }
+    }
+    work_apply = (work_counter - wc0) / std::max(batch, 1);
+  }
+};
+
+}  // namespace tn
+
+struct tn_hvp_ctx {
+  tn::Engine e;
+};
+
+namespace tn {
+
+tn_hvp_ctx* engine_create(const tn_hvp_config& cfg, const int32_t* ref_bonds, const void* ref_mpo, cudaStream_t st) {
+  auto ctx = std::make_unique<tn_hvp_ctx>();
+  ctx->e.setup(cfg, ref_bonds, ref_mpo, st);
+  TN_CUDA(cudaStreamSynchronize(st));
+  return ctx.release();
+}
+void engine_environments(tn_hvp_ctx* ctx, const cplx* gates, double* scalars, cplx* grad_R, cudaStream_t st) {
+  ctx->e.environments(st, gates, scalars, grad_R);
+}
+void engine_apply(tn_hvp_ctx* ctx, int batch, const cplx* dirs, cplx* hess_R, cplx* aux, cudaStream_t st) {
+  ctx->e.apply(st, batch, dirs, hess_R, aux);
+}
+void engine_gradient_T(tn_hvp_ctx* ctx, cplx* E, cudaStream_t st) {
+  if (!ctx->e.primal_valid) throw StateError("no primal pass");
+  TN_CUDA(cudaMemcpyAsync(E, ctx->e.at(ctx->e.o_E), (size_t)ctx->e.K * 16 * sizeof(cplx), cudaMemcpyDeviceToDevice,
+                          st));
+}
+void engine_cost(tn_hvp_ctx* ctx, const cplx* gates, double* scalars, cudaStream_t st) {
+  ctx->e.cost(st, gates, scalars);
+}
+void engine_primal_blob(tn_hvp_ctx* ctx, void** ptr, size_t* bytes) {
+  *ptr = ctx->e.arena;
+  *bytes = ctx->e.arena_bytes;
+}
+void engine_primal_imported(tn_hvp_ctx* ctx, const cplx* gates, cudaStream_t st) {
+  Engine& e = ctx->e;
+  (void)gates;
+  for (SidePlan* sp : {&e.bot, &e.top})
+    for (auto& ls : sp->steps)
+      for (Step& s : ls)
+        if (s.type == PAIR)
+          TN_CUDA(cudaMemcpyAsync(&e.h_s[s.s_index], e.at<double>(s.o_s), sizeof(double), cudaMemcpyDeviceToHost, st));
+  TN_CUDA(cudaStreamSynchronize(st));
+  e.primal_valid = true;
+}
+void engine_work(tn_hvp_ctx* ctx, double* per_dir, double* primal) {
+  *per_dir = ctx->e.work_apply;
+  *primal = ctx->e.work_primal;
+}
+void engine_destroy(tn_hvp_ctx* ctx) { delete ctx; }
+void engine_set_error(tn_hvp_ctx* ctx, const std::string& msg) { ctx->e.err = msg; }
+const char* engine_error(const tn_hvp_ctx* ctx) { return ctx->e.err.c_str(); }
+
+}  // namespace tn

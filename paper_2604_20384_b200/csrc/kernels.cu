@@ -1,0 +1,469 @@
+// Small (memory-bound) kernels of the HVP path: 4x4 gate application on the
+// out legs of two-site blocks, elementwise complex updates, gate-environment
+// extraction (warp-shuffle reductions), Alg. 2 postprocessing and the unitary
+// tangent projection (App. E).  All complex128 interleaved, row-major.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace tn {
+namespace {
+
+constexpr int TPB = 256;
+
+inline int nblocks(int64_t n, int per = TPB) {
+  int64_t b = (n + per - 1) / per;
+  return (int)(b < 148 * 64 ? (b > 0 ? b : 1) : 148 * 64);
+}
+
+// ---------------------------------------------------------------- gates --
+// x: [batch][X][4][4][Y] viewed as [X][o1][i1][o2][i2][Y]; out[b] = gate[b] x[b]
+// on the out legs (o1 o2); gate stride sg in complex elements (0 = shared).
+__global__ void apply_gate_kernel(cplx* out, int64_t sout, const cplx* x, int64_t sx,
+                                  const cplx* __restrict__ gate, int64_t sg, int X, int Y, int batch,
+                                  cplx alpha, int accumulate) {
+  const int64_t per = (int64_t)X * 4 * Y;  // (x, i1, i2, y) combos per batch entry
+  const int64_t total = per * batch;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = idx / per;
+    int64_t r = idx % per;
+    const int y = (int)(r % Y);
+    r /= Y;
+    const int i12 = (int)(r % 4);
+    const int xx = (int)(r / 4);
+    const int i1 = i12 >> 1, i2 = i12 & 1;
+    const cplx* xb = x + b * sx + (int64_t)xx * 16 * Y;
+    const cplx* g = gate + b * sg;
+    cplx in[4];
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+      const int o1 = o >> 1, o2 = o & 1;
+      in[o] = xb[((int64_t)((o1 * 2 + i1) * 4 + (o2 * 2 + i2))) * Y + y];
+    }
+    cplx* ob = out + b * sout + (int64_t)xx * 16 * Y;
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+      cplx acc = make_double2(0, 0);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc = cadd(acc, cmul(g[o * 4 + c], in[c]));
+      acc = cmul(alpha, acc);
+      const int o1 = o >> 1, o2 = o & 1;
+      cplx* d = ob + ((int64_t)((o1 * 2 + i1) * 4 + (o2 * 2 + i2))) * Y + y;
+      *d = accumulate ? cadd(*d, acc) : acc;
+    }
+  }
+}
+
+__global__ void axpby_kernel(cplx* __restrict__ y, const cplx* __restrict__ x, cplx a, cplx b, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = cadd(cmul(a, x[i]), cmul(b, y[i]));
+}
+
+__global__ void scale_kernel(cplx* __restrict__ y, const double* __restrict__ s, double pw, int64_t n) {
+  const double f = pow(*s, pw);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = cscale(y[i], f);
+}
+
+// Gate-environment extraction:
+// E[b][(o1 o2),(c1 c2)] += alpha * sum_{t,i1,i2,u} conj(top[t,o1 i1,o2 i2,u]) z[b][t,c1 i1,c2 i2,u]
+// top: [T][4][4][U] (shared, stride stop per batch, 0 allowed); z: [batch][T][4][4][U].
+__global__ void extract_env_kernel(cplx* __restrict__ E, int64_t sE, const cplx* __restrict__ top, int64_t stop,
+                                   const cplx* __restrict__ z, int64_t sz, int T, int U, cplx alpha) {
+  const int b = blockIdx.y;
+  const cplx* tp = top + b * stop;
+  const cplx* zb = z + b * sz;
+  double acc[16][2];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = 0.0;
+  const int64_t pairs = (int64_t)T * U * 4;  // (t, u, i1, i2)
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < pairs;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int i12 = (int)(idx & 3);
+    const int64_t tu = idx >> 2;
+    const int u = (int)(tu % U), t = (int)(tu / U);
+    const int i1 = i12 >> 1, i2 = i12 & 1;
+    cplx tv[4], zv[4];
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+      const int o1 = o >> 1, o2 = o & 1;
+      const int64_t off = (((int64_t)t * 4 + (o1 * 2 + i1)) * 4 + (o2 * 2 + i2)) * U + u;
+      tv[o] = tp[off];
+      zv[o] = zb[off];
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const cplx v = cmulc(tv[a], zv[c]);
+        acc[a * 4 + c][0] += v.x;
+        acc[a * 4 + c][1] += v.y;
+      }
+  }
+  __shared__ double red[16][2][TPB / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      double v = acc[i][c];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == 0) red[i][c][w] = v;
+    }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int i = threadIdx.x >> 1, c = threadIdx.x & 1;
+    double v = 0.0;
+    for (int j = 0; j < TPB / 32; ++j) v += red[i][c][j];
+    // complex scale and accumulate with atomics (several blocks per batch entry)
+    const double other = __shfl_xor_sync(0xffffffffu, v, 1);
+    const double re = (c == 0) ? v : other, im = (c == 0) ? other : v;
+    const cplx s = cmul(alpha, make_double2(re, im));
+    atomicAdd(&reinterpret_cast<double*>(E + b * sE + i)[c], c == 0 ? s.x : s.y);
+  }
+}
+
+// P_G(Z) = 1/2 (Z - G Z^dag G), one thread per (batch, gate).
+__device__ inline void proj4(const cplx* G, const cplx* Z, cplx* out) {
+  cplx t[16];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)  // t = Z^dag G
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      cplx s = make_double2(0, 0);
+#pragma unroll
+      for (int m = 0; m < 4; ++m) s = cadd(s, cmulc(Z[m * 4 + a], G[m * 4 + c]));
+      t[a * 4 + c] = s;
+    }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      cplx s = make_double2(0, 0);
+#pragma unroll
+      for (int m = 0; m < 4; ++m) s = cadd(s, cmul(G[a * 4 + m], t[m * 4 + c]));
+      out[a * 4 + c] = cscale(csub(Z[a * 4 + c], s), 0.5);
+    }
+}
+
+__global__ void project_kernel(int K, int batch, const cplx* __restrict__ G, const cplx* __restrict__ in,
+                               cplx* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)K * batch) return;
+  const int k = (int)(i % K);
+  cplx g[16], z[16], o[16];
+  for (int e = 0; e < 16; ++e) {
+    g[e] = G[k * 16 + e];
+    z[e] = in[i * 16 + e];
+  }
+  proj4(g, z, o);
+  for (int e = 0; e < 16; ++e) out[i * 16 + e] = o[e];
+}
+
+// Alg. 2 (reading X2) + App. E for the gradient:
+// grad_f = -2 T conj(E);  grad_R = P_G(grad_f).  scal: {T.re, T.im} at [1],[2].
+__global__ void gradient_kernel(int K, const cplx* __restrict__ G, const cplx* __restrict__ E,
+                                const double* __restrict__ scal, cplx* __restrict__ grad_f,
+                                cplx* __restrict__ grad_R) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  const cplx T = make_double2(scal[1], scal[2]);
+  cplx g[16], gf[16], o[16];
+  for (int e = 0; e < 16; ++e) {
+    g[e] = G[k * 16 + e];
+    gf[e] = cscale(cmul(T, cconj(E[k * 16 + e])), -2.0);
+    grad_f[k * 16 + e] = gf[e];
+  }
+  if (grad_R) {
+    proj4(g, gf, o);
+    for (int e = 0; e < 16; ++e) grad_R[k * 16 + e] = o[e];
+  }
+}
+
+// Omega[b] = sum_k sum_ab E_k[a,b] V_k[a,b]  (eq:Omega)
+__global__ void omega_kernel(int K, const cplx* __restrict__ E, const cplx* __restrict__ V, cplx* __restrict__ om) {
+  const int b = blockIdx.x;
+  double re = 0, im = 0;
+  for (int i = threadIdx.x; i < K * 16; i += blockDim.x) {
+    const cplx v = cmul(E[i], V[(int64_t)b * K * 16 + i]);
+    re += v.x;
+    im += v.y;
+  }
+  __shared__ double s[2][TPB / 32];
+  for (int off = 16; off > 0; off >>= 1) {
+    re += __shfl_xor_sync(0xffffffffu, re, off);
+    im += __shfl_xor_sync(0xffffffffu, im, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s[0][threadIdx.x >> 5] = re;
+    s[1][threadIdx.x >> 5] = im;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r = 0, m = 0;
+    for (int j = 0; j < (int)(blockDim.x / 32); ++j) {
+      r += s[0][j];
+      m += s[1][j];
+    }
+    om[b] = make_double2(r, m);
+  }
+}
+
+// H_f[V] = -2 [Omega conj(E) + T conj(H_T)]  (eq:hvp-costHS as printed, X2);
+// Hess_R[V] = P_G(H_f - 1/2 V grad_f^dag G - 1/2 G grad_f^dag V)
+__global__ void hessian_kernel(int K, int batch, const cplx* __restrict__ G, const cplx* __restrict__ E,
+                               const cplx* __restrict__ grad_f, const double* __restrict__ scal,
+                               const cplx* __restrict__ HT, const cplx* __restrict__ V,
+                               const cplx* __restrict__ om, cplx* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)K * batch) return;
+  const int k = (int)(i % K);
+  const int64_t b = i / K;
+  const cplx T = make_double2(scal[1], scal[2]);
+  const cplx O = om[b];
+  cplx g[16], gf[16], v[16], h[16], w1[16], o[16];
+  for (int e = 0; e < 16; ++e) {
+    g[e] = G[k * 16 + e];
+    gf[e] = grad_f[k * 16 + e];
+    v[e] = V[i * 16 + e];
+    h[e] = cscale(cadd(cmul(O, cconj(E[k * 16 + e])), cmul(T, cconj(HT[i * 16 + e]))), -2.0);
+  }
+  // w1 = grad_f^dag G ;  h -= 1/2 V w1 ; w2 = grad_f^dag V ; h -= 1/2 G w2
+  for (int a = 0; a < 4; ++a)
+    for (int c = 0; c < 4; ++c) {
+      cplx s = make_double2(0, 0);
+      for (int m = 0; m < 4; ++m) s = cadd(s, cmulc(gf[m * 4 + a], g[m * 4 + c]));
+      w1[a * 4 + c] = s;
+    }
+  for (int a = 0; a < 4; ++a)
+    for (int c = 0; c < 4; ++c) {
+      cplx s = make_double2(0, 0);
+      for (int m = 0; m < 4; ++m) s = cadd(s, cmul(v[a * 4 + m], w1[m * 4 + c]));
+      o[a * 4 + c] = s;
+    }
+  for (int e = 0; e < 16; ++e) h[e] = csub(h[e], cscale(o[e], 0.5));
+  for (int a = 0; a < 4; ++a)
+    for (int c = 0; c < 4; ++c) {
+      cplx s = make_double2(0, 0);
+      for (int m = 0; m < 4; ++m) s = cadd(s, cmulc(gf[m * 4 + a], v[m * 4 + c]));
+      w1[a * 4 + c] = s;
+    }
+  for (int a = 0; a < 4; ++a)
+    for (int c = 0; c < 4; ++c) {
+      cplx s = make_double2(0, 0);
+      for (int m = 0; m < 4; ++m) s = cadd(s, cmul(g[a * 4 + m], w1[m * 4 + c]));
+      o[a * 4 + c] = s;
+    }
+  for (int e = 0; e < 16; ++e) h[e] = csub(h[e], cscale(o[e], 0.5));
+  proj4(g, h, o);
+  for (int e = 0; e < 16; ++e) out[i * 16 + e] = o[e];
+}
+
+}  // namespace
+
+void apply_gate(cudaStream_t st, cplx* out, int64_t sout, const cplx* x, int64_t sx, const cplx* gate, int64_t sg,
+                int X, int Y, int batch, cplx alpha, bool accumulate) {
+  const int64_t total = (int64_t)X * 4 * Y * batch;
+  if (total == 0) return;
+  apply_gate_kernel<<<nblocks(total), TPB, 0, st>>>(out, sout, x, sx, gate, sg, X, Y, batch, alpha,
+                                                    accumulate ? 1 : 0);
+  TN_CUDA(cudaGetLastError());
+}
+
+void axpby(cudaStream_t st, cplx* y, const cplx* x, cplx a, cplx b, int64_t n) {
+  if (n == 0) return;
+  axpby_kernel<<<nblocks(n), TPB, 0, st>>>(y, x, a, b, n);
+  TN_CUDA(cudaGetLastError());
+}
+
+void scale_by(cudaStream_t st, cplx* y, const double* s, double pw, int64_t n) {
+  if (n == 0) return;
+  scale_kernel<<<nblocks(n), TPB, 0, st>>>(y, s, pw, n);
+  TN_CUDA(cudaGetLastError());
+}
+
+void extract_env(cudaStream_t st, cplx* E, int64_t sE, const cplx* top, int64_t stop, const cplx* z, int64_t sz,
+                 int T, int U, int batch, cplx alpha) {
+  const int64_t pairs = (int64_t)T * U * 4;
+  int bx = (int)((pairs + TPB * 8 - 1) / (TPB * 8));
+  if (bx < 1) bx = 1;
+  if (bx > 64) bx = 64;
+  dim3 grid(bx, batch);
+  extract_env_kernel<<<grid, TPB, 0, st>>>(E, sE, top, stop, z, sz, T, U, alpha);
+  TN_CUDA(cudaGetLastError());
+}
+
+void project(cudaStream_t st, int K, int batch, const cplx* G, const cplx* in, cplx* out) {
+  const int64_t n = (int64_t)K * batch;
+  if (n == 0) return;
+  project_kernel<<<(int)((n + 127) / 128), 128, 0, st>>>(K, batch, G, in, out);
+  TN_CUDA(cudaGetLastError());
+}
+
+void gradient_post(cudaStream_t st, int K, const cplx* G, const cplx* E, const double* scal, cplx* grad_f,
+                   cplx* grad_R) {
+  gradient_kernel<<<(K + 127) / 128, 128, 0, st>>>(K, G, E, scal, grad_f, grad_R);
+  TN_CUDA(cudaGetLastError());
+}
+
+void hessian_post(cudaStream_t st, int K, int batch, const cplx* G, const cplx* E, const cplx* grad_f,
+                  const double* scal, const cplx* HT, const cplx* V, cplx* om, cplx* out) {
+  omega_kernel<<<batch, TPB, 0, st>>>(K, E, V, om);
+  TN_CUDA(cudaGetLastError());
+  const int64_t n = (int64_t)K * batch;
+  hessian_kernel<<<(int)((n + 63) / 64), 64, 0, st>>>(K, batch, G, E, grad_f, scal, HT, V, om, out);
+  TN_CUDA(cudaGetLastError());
+}
+
+}  // namespace tn
+
+namespace tn {
+namespace {
+__global__ void transpose_kernel(cplx* __restrict__ dst, const cplx* __restrict__ src, int rows, int cols, int conj) {
+  __shared__ cplx tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const int r = by + j, c = bx + threadIdx.x;
+    if (r < rows && c < cols) tile[j][threadIdx.x] = src[(int64_t)r * cols + c];
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const int c = bx + j, r = by + threadIdx.x;
+    if (r < rows && c < cols) {
+      cplx v = tile[threadIdx.x][j];
+      if (conj) v.y = -v.y;
+      dst[(int64_t)c * rows + r] = v;
+    }
+  }
+}
+
+__global__ void svd_post_kernel(const double* __restrict__ S, int mn, int r, double* s_out, double* diag) {
+  __shared__ double red[2][32];
+  double all = 0, kept = 0;
+  for (int i = threadIdx.x; i < mn; i += blockDim.x) {
+    const double v = S[i] * S[i];
+    all += v;
+    if (i < r) kept += v;
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    all += __shfl_xor_sync(0xffffffffu, all, off);
+    kept += __shfl_xor_sync(0xffffffffu, kept, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = all;
+    red[1][threadIdx.x >> 5] = kept;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0, k = 0;
+    for (int j = 0; j < (int)(blockDim.x >> 5); ++j) {
+      a += red[0][j];
+      k += red[1][j];
+    }
+    const double s = sqrt(a / k);
+    s_out[0] = s;
+    if (diag) {
+      diag[0] = fmax(diag[0], 1.0 - k / a);
+      if (r < mn) diag[1] = fmin(diag[1], (S[r - 1] - S[r]) / S[0]);
+      diag[2] = fmax(diag[2], fabs(log10(s)));
+    }
+  }
+}
+
+__global__ void scale_rows_kernel(cplx* __restrict__ dst, const cplx* __restrict__ src, int rows, int cols,
+                                  const double* __restrict__ S, const double* __restrict__ s) {
+  const int64_t n = (int64_t)rows * cols;
+  const double f = s ? s[0] : 1.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = cscale(src[i], f * S[i / cols]);
+}
+
+__global__ void conjT_scale_kernel(cplx* __restrict__ dst, const cplx* __restrict__ uh, int r, int m,
+                                   const double* __restrict__ S, const double* __restrict__ s) {
+  const int64_t n = (int64_t)r * m;
+  const double f = s ? s[0] : 1.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int a = (int)(i / r), j = (int)(i % r);
+    cplx v = cconj(uh[(int64_t)j * m + a]);
+    if (S) v = cscale(v, f * S[j]);
+    dst[i] = v;
+  }
+}
+
+__global__ void tri_kernel(cplx* __restrict__ dst, const cplx* __restrict__ buf, int rows, int cols, int64_t lda,
+                           int upper) {
+  const int64_t n = (int64_t)rows * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / cols), j = (int)(idx % cols);
+    cplx v = make_double2(0, 0);
+    if (upper) {
+      if (j >= i) v = buf[i + (int64_t)j * lda];
+    } else {
+      if (j <= i) v = buf[j + (int64_t)i * lda];
+    }
+    dst[idx] = v;
+  }
+}
+
+__global__ void dagger4_kernel(cplx* __restrict__ dst, const cplx* __restrict__ src, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n * 16) return;
+  const int64_t m = i / 16;
+  const int e = (int)(i % 16), a = e / 4, c = e % 4;
+  dst[i] = cconj(src[m * 16 + c * 4 + a]);
+}
+
+__global__ void finish_cost_kernel(double* scalars, const cplx* T11) {
+  const cplx T = T11[0];
+  scalars[0] = -(T.x * T.x + T.y * T.y);
+  scalars[1] = T.x;
+  scalars[2] = T.y;
+}
+}  // namespace
+
+void transpose(cudaStream_t st, cplx* dst, const cplx* src, int rows, int cols, bool conj) {
+  if ((int64_t)rows * cols == 0) return;
+  dim3 grid((cols + 31) / 32, (rows + 31) / 32), block(32, 8);
+  transpose_kernel<<<grid, block, 0, st>>>(dst, src, rows, cols, conj ? 1 : 0);
+  TN_CUDA(cudaGetLastError());
+}
+
+void svd_post(cudaStream_t st, const double* S, int mn, int r, double* s_out, double* diag) {
+  svd_post_kernel<<<1, 256, 0, st>>>(S, mn, r, s_out, diag);
+  TN_CUDA(cudaGetLastError());
+}
+
+void scale_rows_sv(cudaStream_t st, cplx* dst, const cplx* src, int rows, int cols, const double* S,
+                   const double* s) {
+  const int64_t n = (int64_t)rows * cols;
+  if (!n) return;
+  scale_rows_kernel<<<nblocks(n), TPB, 0, st>>>(dst, src, rows, cols, S, s);
+  TN_CUDA(cudaGetLastError());
+}
+
+void conjT_scale_cols(cudaStream_t st, cplx* dst, const cplx* uh, int r, int m, const double* S, const double* s) {
+  const int64_t n = (int64_t)r * m;
+  if (!n) return;
+  conjT_scale_kernel<<<nblocks(n), TPB, 0, st>>>(dst, uh, r, m, S, s);
+  TN_CUDA(cudaGetLastError());
+}
+
+void tri_extract(cudaStream_t st, cplx* dst, const cplx* buf, int rows, int cols, int64_t lda, bool upper) {
+  const int64_t n = (int64_t)rows * cols;
+  if (!n) return;
+  tri_kernel<<<nblocks(n), TPB, 0, st>>>(dst, buf, rows, cols, lda, upper ? 1 : 0);
+  TN_CUDA(cudaGetLastError());
+}
+
+void dagger4(cudaStream_t st, cplx* dst, const cplx* src, int64_t n) {
+  if (!n) return;
+  dagger4_kernel<<<(int)((n * 16 + 255) / 256), 256, 0, st>>>(dst, src, n);
+  TN_CUDA(cudaGetLastError());
+}
+
+void finish_cost(cudaStream_t st, double* scalars, const cplx* T11) {
+  finish_cost_kernel<<<1, 1, 0, st>>>(scalars, T11);
+  TN_CUDA(cudaGetLastError());
+}
+}  // namespace tn

@@ -1,0 +1,42 @@
+// Declarations of the small kernels (kernels.cu).
+#pragma once
+#include "common.cuh"
+
+namespace tn {
+// out[b] = alpha * gate[b] (x) I_in applied to the out legs of x[b] viewed as
+// [X][4][4][Y] (p = 2 out + in); accumulate adds to out.  In-place allowed.
+void apply_gate(cudaStream_t st, cplx* out, int64_t sout, const cplx* x, int64_t sx, const cplx* gate, int64_t sg,
+                int X, int Y, int batch, cplx alpha, bool accumulate);
+void axpby(cudaStream_t st, cplx* y, const cplx* x, cplx a, cplx b, int64_t n);   // y = a x + b y
+void scale_by(cudaStream_t st, cplx* y, const double* s, double pw, int64_t n);    // y *= s^pw (device s)
+// E[b] += alpha * sum conj(top[t,(o1 i1),(o2 i2),u]) z[b][t,(c1 i1),(c2 i2),u]
+void extract_env(cudaStream_t st, cplx* E, int64_t sE, const cplx* top, int64_t stop, const cplx* z, int64_t sz,
+                 int T, int U, int batch, cplx alpha);
+void project(cudaStream_t st, int K, int batch, const cplx* G, const cplx* in, cplx* out);
+void gradient_post(cudaStream_t st, int K, const cplx* G, const cplx* E, const double* scal, cplx* grad_f,
+                   cplx* grad_R);
+void hessian_post(cudaStream_t st, int K, int batch, const cplx* G, const cplx* E, const cplx* grad_f,
+                  const double* scal, const cplx* HT, const cplx* V, cplx* om, cplx* out);
+}  // namespace tn
+
+namespace tn {
+// dst[c][r] = (conj?) src[r][c]; src rows x cols row-major (ld = cols).
+void transpose(cudaStream_t st, cplx* dst, const cplx* src, int rows, int cols, bool conj);
+// Singular values S[0..mn) descending, keep r: s = ||S|| / ||S_r||.
+// Writes s to s_out[0]; diag[0] = max(diag[0], discarded weight),
+// diag[1] = min(diag[1], relative gap (S[r-1]-S[r])/S[0]), diag[2] = max(diag[2], |log10 s|).
+void svd_post(cudaStream_t st, const double* S, int mn, int r, double* s_out, double* diag);
+// dst[i][j] = s * S[i] * src[i][j]  (rows x cols), s from device (pw 1).
+void scale_rows_sv(cudaStream_t st, cplx* dst, const cplx* src, int rows, int cols, const double* S,
+                   const double* s);
+// dst[a][j] = conj(uh[j][a]) * (S ? s*S[j] : 1)  for uh (r x m) row-major -> dst (m x r).
+void conjT_scale_cols(cudaStream_t st, cplx* dst, const cplx* uh, int r, int m, const double* S, const double* s);
+// Row-major (rows x cols) from the upper triangle of a column-major buffer
+// (lda): dst[i][j] = (j >= i) ? buf[i + j*lda] : 0          (upper = true)
+// Lower variant for LQ: dst[i][j] = (j <= i) ? buf[j + i*lda] : 0 (rows x cols = b x kq).
+void tri_extract(cudaStream_t st, cplx* dst, const cplx* buf, int rows, int cols, int64_t lda, bool upper);
+// Vd[b][k] = V[b][k]^dag (4x4 each), n = batch*K matrices.
+void dagger4(cudaStream_t st, cplx* dst, const cplx* src, int64_t n);
+// scalars[0] = -|T|^2, [1..2] = T from a 1x1 complex env; keeps [3..] untouched.
+void finish_cost(cudaStream_t st, double* scalars, const cplx* T11);
+}  // namespace tn

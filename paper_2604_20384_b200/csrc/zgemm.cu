@@ -1,0 +1,221 @@
+// Batched complex128 GEMM on the FP64 tensor cores of sm_100a.
+//
+// tcgen05.mma has no f64 kind (ptxas rejects .kind::f64), so the FP64 tensor
+// path on B200 is the warp-level mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).  A
+// complex product is four real DMMAs on planar fragments:
+//   C_re += A_re B_re + (-A_im) B_im,   C_im += A_re B_im + A_im B_re.
+// Tiles: CTA 64x64 (complex) x BK=16, 4 warps in 2x2, warp tile 32x32 =
+// 4x4 DMMA tiles; operands staged global->shared with cp.async (16 B per
+// complex element, zero-filled outside the matrix), double-buffered; shared
+// strides padded so every fragment load (one LDS.128 = one complex) is
+// bank-conflict free.  op(A), op(B) in {N, T, C}; conjugation is folded into
+// the fragment sign.  Row-major everywhere; batch strides may be 0 (shared).
+#include "common.cuh"
+
+namespace tn {
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16, NT = 128;
+constexpr int LDN = BK + 4;    // [rows][BK] tiles: row stride = 20 complex (= 4 mod 8 slots)
+constexpr int LDT = BM + 2;    // [BK][cols] tiles: row stride = 66 complex (= 2 mod 8 slots)
+constexpr int TILE = BM * LDN; // 1280 >= BK * LDT = 1056
+constexpr int STAGE = 2 * TILE;
+constexpr int SMEM_BYTES = 2 * STAGE * (int)sizeof(cplx);
+
+struct Params {
+  int M, N, K;
+  cplx alpha, beta;
+  int has_beta;
+  const cplx* A;
+  const cplx* B;
+  cplx* C;
+  int64_t lda, ldb, ldc, sA, sB, sC;
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int sz = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <char OPA, char OPB>
+__global__ void __launch_bounds__(NT, 2) zgemm_kernel(Params p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx* smem = reinterpret_cast<cplx*>(smem_raw);
+  const int64_t bz = blockIdx.z;
+  const cplx* __restrict__ A = p.A + bz * p.sA;
+  const cplx* __restrict__ B = p.B + bz * p.sB;
+  cplx* __restrict__ C = p.C + bz * p.sC;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
+  const int g = lane >> 2, q = lane & 3;
+
+  auto load_stage = [&](int stage, int k0) {
+    cplx* sA = smem + stage * STAGE;
+    cplx* sB = sA + TILE;
+#pragma unroll
+    for (int j = 0; j < (BM * BK) / NT; ++j) {
+      const int e = tid + j * NT;
+      if (OPA == 'N') {
+        const int m = e / BK, k = e % BK, gm = m0 + m, gk = k0 + k;
+        const bool ok = gm < p.M && gk < p.K;
+        cp_async16(sA + m * LDN + k, ok ? (const void*)(A + (int64_t)gm * p.lda + gk) : (const void*)A, ok);
+      } else {
+        const int k = e / BM, m = e % BM, gm = m0 + m, gk = k0 + k;
+        const bool ok = gm < p.M && gk < p.K;
+        cp_async16(sA + k * LDT + m, ok ? (const void*)(A + (int64_t)gk * p.lda + gm) : (const void*)A, ok);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < (BN * BK) / NT; ++j) {
+      const int e = tid + j * NT;
+      if (OPB == 'N') {
+        const int k = e / BN, n = e % BN, gn = n0 + n, gk = k0 + k;
+        const bool ok = gn < p.N && gk < p.K;
+        cp_async16(sB + k * LDT + n, ok ? (const void*)(B + (int64_t)gk * p.ldb + gn) : (const void*)B, ok);
+      } else {
+        const int n = e / BK, k = e % BK, gn = n0 + n, gk = k0 + k;
+        const bool ok = gn < p.N && gk < p.K;
+        cp_async16(sB + n * LDN + k, ok ? (const void*)(B + (int64_t)gn * p.ldb + gk) : (const void*)B, ok);
+      }
+    }
+  };
+
+  double acc_re[4][4][2], acc_im[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc_re[i][j][0] = acc_re[i][j][1] = acc_im[i][j][0] = acc_im[i][j][1] = 0.0;
+
+  const int nk = (p.K + BK - 1) / BK;
+  load_stage(0, 0);
+  cp_commit();
+  for (int kt = 0; kt < nk; ++kt) {
+    if (kt + 1 < nk) load_stage((kt + 1) & 1, (kt + 1) * BK);
+    cp_commit();
+    cp_wait<1>();
+    __syncthreads();
+    const cplx* sA = smem + (kt & 1) * STAGE;
+    const cplx* sB = sA + TILE;
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      double ar[4], ai[4], an[4], br[4], bi[4];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        const int row = wm * 32 + mi * 8 + g, col = kk * 4 + q;
+        const cplx a = (OPA == 'N') ? sA[row * LDN + col] : sA[col * LDT + row];
+        ar[mi] = a.x;
+        ai[mi] = (OPA == 'C') ? -a.y : a.y;
+        an[mi] = -ai[mi];
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const int krow = kk * 4 + q, ncol = wn * 32 + ni * 8 + g;
+        const cplx b = (OPB == 'N') ? sB[krow * LDT + ncol] : sB[ncol * LDN + krow];
+        br[ni] = b.x;
+        bi[ni] = (OPB == 'C') ? -b.y : b.y;
+      }
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+          dmma(acc_re[mi][ni], ar[mi], br[ni]);
+          dmma(acc_im[mi][ni], ar[mi], bi[ni]);
+          dmma(acc_re[mi][ni], an[mi], bi[ni]);
+          dmma(acc_im[mi][ni], ai[mi], br[ni]);
+        }
+    }
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    const int row = m0 + wm * 32 + mi * 8 + g;
+    if (row >= p.M) continue;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int col = n0 + wn * 32 + ni * 8 + 2 * q + j;
+        if (col < p.N) {
+          cplx v = cmul(p.alpha, make_double2(acc_re[mi][ni][j], acc_im[mi][ni][j]));
+          cplx* dst = C + (int64_t)row * p.ldc + col;
+          if (p.has_beta) v = cadd(v, cmul(p.beta, *dst));
+          *dst = v;
+        }
+      }
+    }
+  }
+}
+
+template <char OPA, char OPB>
+void launch(const Params& p, int batch, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    TN_CUDA(cudaFuncSetAttribute(zgemm_kernel<OPA, OPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    attr = true;
+  }
+  dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, batch);
+  zgemm_kernel<OPA, OPB><<<grid, NT, SMEM_BYTES, st>>>(p);
+  TN_CUDA(cudaGetLastError());
+}
+
+template <char OPA>
+void dispatch_b(char opb, const Params& p, int batch, cudaStream_t st) {
+  switch (opb) {
+    case 'N': launch<OPA, 'N'>(p, batch, st); break;
+    case 'T': launch<OPA, 'T'>(p, batch, st); break;
+    case 'C': launch<OPA, 'C'>(p, batch, st); break;
+    default: throw std::invalid_argument("opb");
+  }
+}
+
+}  // namespace
+
+void zgemm(cudaStream_t st, char opa, char opb, int M, int N, int K, cplx alpha, const cplx* A, int64_t lda,
+           int64_t sA, const cplx* B, int64_t ldb, int64_t sB, cplx beta, cplx* C, int64_t ldc, int64_t sC,
+           int batch) {
+  if (M <= 0 || N <= 0 || batch <= 0) return;
+  Params p;
+  p.alpha = alpha;
+  p.beta = beta;
+  p.has_beta = (beta.x != 0.0 || beta.y != 0.0);
+  p.A = A; p.B = B; p.C = C;
+  p.lda = lda; p.ldb = ldb; p.ldc = ldc; p.sA = sA; p.sB = sB; p.sC = sC;
+  p.M = M; p.N = N; p.K = K;
+  if (K <= 0) {  // C = beta C (alpha * empty product)
+    p.K = 0;
+  }
+  // Stack a batch with a shared B into one tall GEMM when rows are contiguous.
+  if (batch > 1 && sB == 0 && opa == 'N' && sA == (int64_t)M * lda && sC == (int64_t)M * ldc) {
+    p.M = M * batch;
+    batch = 1;
+  }
+  while (batch > 0) {  // grid.z <= 65535
+    const int b = batch < 65535 ? batch : 65535;
+    switch (opa) {
+      case 'N': dispatch_b<'N'>(opb, p, b, st); break;
+      case 'T': dispatch_b<'T'>(opb, p, b, st); break;
+      case 'C': dispatch_b<'C'>(opb, p, b, st); break;
+      default: throw std::invalid_argument("opa");
+    }
+    batch -= b;
+    p.A += (int64_t)b * p.sA;
+    p.B += (int64_t)b * p.sB;
+    p.C += (int64_t)b * p.sC;
+  }
+}
+
+}  // namespace tn

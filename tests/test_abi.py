@@ -1,0 +1,56 @@
+"""CPU-side checks of the boundary: the library loads, exports every symbol
+include/tn_hvp.h declares, and rejects bad arguments before any launch."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2604_20384_b200._native as N
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared():
+    src = open(os.path.join(ROOT, "include", "tn_hvp.h")).read()
+    return sorted(set(re.findall(r"\b(tn_[a-z_A-Z0-9]+)\s*\(", src)))
+
+
+def test_header_and_library_exports_match():
+    names = declared()
+    assert set(names) == set(N.EXPORTS)
+    lib = ctypes.CDLL(N.LIB_PATH)
+    for nm in names:
+        assert hasattr(lib, nm), nm
+
+
+def test_num_gates():
+    assert [N.tn_hvp_num_gates(n, d) for n, d in [(6, 4), (16, 8), (32, 12), (50, 16), (128, 24)]] == \
+        [10, 60, 186, 392, 1524]
+    assert N.tn_hvp_num_gates(1, 4, 0) == -1
+
+
+def test_invalid_arguments_rejected_without_gpu():
+    cfg = N.Config(1, 4, 0, 8, 4, 0, 0)         # n < 2
+    with pytest.raises(N.TNError) as e:
+        N.tn_hvp_setup(cfg, [1, 1], 1, 0)
+    assert e.value.status == N.TN_EINVAL
+    cfg = N.Config(4, 4, 0, 8, 4, 0, 0)
+    with pytest.raises(N.TNError) as e:
+        N.tn_hvp_setup(cfg, [2, 1, 1, 1, 1], 1, 0)  # boundary bond != 1
+    assert e.value.status == N.TN_EINVAL
+    with pytest.raises(N.TNError) as e:
+        N.tn_zgemm("X", "N", 4, 4, 4, 1.0, 1, 4, 0, 1, 4, 0, 0.0, 1, 4, 0, 1, 0)
+    assert e.value.status == N.TN_EINVAL
+    with pytest.raises(N.TNError) as e:
+        N.tn_riemannian_project(-1, 1, 1, 1, 1, 0)
+    assert e.value.status == N.TN_EINVAL
+
+
+def test_product_path_has_no_oracle_import():
+    pkg = os.path.join(ROOT, "paper_2604_20384_b200")
+    for dp, _, fs in os.walk(pkg):
+        for f in fs:
+            if f.endswith(".py"):
+                src = open(os.path.join(dp, f)).read()
+                assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", src, re.M), f
