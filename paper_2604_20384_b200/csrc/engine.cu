@@ -17,6 +17,10 @@
 #include <cusolverDn.h>
 
 #include <algorithm>
+#include <atomic>
+#include <cstdlib>
+#include <exception>
+#include <thread>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -110,12 +114,23 @@ struct Engine {
   std::vector<double> h_s;                    // host copy of the frozen factors
   cplx* ref = nullptr;                        // reference MPO copy (device)
   std::vector<size_t> ref_off;
-  // solver
-  cusolverDnHandle_t solver = nullptr;
-  gesvdjInfo_t svdj = nullptr;
-  int lwork_svd = 0, lwork_geqrf = 0, lwork_ungqr = 0;
+  // solvers: one per concurrent primal sweep (bottom on the caller's stream,
+  // top on an internal stream driven by a second host thread)
+  struct Solver {
+    cusolverDnHandle_t h = nullptr;
+    cusolverDnParams_t prm = nullptr;
+    gesvdjInfo_t svdj = nullptr;
+    std::vector<char> host_ws;
+  };
+  Solver sol[2];
+  int svd_method = 1;  // 0 gesvdj, 1 Xgesvdp (default), 2 Xgesvd
+  size_t svd_dws = 0, svd_hws = 0;
+  int lwork_geqrf = 0, lwork_ungqr = 0;
+  cudaStream_t st2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool primal_valid = false;
-  double work_primal = 0, work_apply = 0, work_counter = 0;
+  double work_primal = 0, work_apply = 0;
+  std::atomic<double> work_counter{0.0};
   std::string err;
   int device = 0;
 
@@ -128,7 +143,7 @@ struct Engine {
   void mm(cudaStream_t st, char oa, char ob, int M, int N, int Kd, cplx a, const cplx* A, int64_t lda, int64_t sA,
           const cplx* B, int64_t ldb, int64_t sB, cplx b, cplx* C, int64_t ldc, int64_t sC, int batch) {
     if (M <= 0 || N <= 0 || batch <= 0) return;
-    work_counter += (double)M * N * std::max(Kd, 0) * batch;
+    work_counter.fetch_add((double)M * N * std::max(Kd, 0) * batch, std::memory_order_relaxed);
     zgemm(st, oa, ob, M, N, Kd, a, A, lda, sA, B, ldb, sB, b, C, ldc, sC, batch);
   }
   // C(MxN) = a A(MxK) B(KxN) + b C
@@ -328,39 +343,66 @@ struct Engine {
     TN_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t thr = UINT64_MAX;
     TN_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-    // solver
-    TN_SOLVER(cusolverDnCreate(&solver));
-    TN_SOLVER(cusolverDnCreateGesvdjInfo(&svdj));
-    TN_SOLVER(cusolverDnXgesvdjSetTolerance(svdj, 1e-15));
-    TN_SOLVER(cusolverDnXgesvdjSetMaxSweeps(svdj, 100));
-    TN_SOLVER(cusolverDnSetStream(solver, st));
-    int maxM = 1;
+    if (const char* m = std::getenv("TN_SVD")) {
+      const std::string v(m);
+      svd_method = v == "gesvdj" ? 0 : v == "gesvd" ? 2 : 1;
+    }
+    TN_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+    TN_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    TN_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    for (Solver& so : sol) {
+      TN_SOLVER(cusolverDnCreate(&so.h));
+      TN_SOLVER(cusolverDnCreateParams(&so.prm));
+      TN_SOLVER(cusolverDnCreateGesvdjInfo(&so.svdj));
+      TN_SOLVER(cusolverDnXgesvdjSetTolerance(so.svdj, 1e-15));
+      TN_SOLVER(cusolverDnXgesvdjSetMaxSweeps(so.svdj, 100));
+    }
+    Solver& so = sol[0];
+    TN_SOLVER(cusolverDnSetStream(so.h, st));
     for (SidePlan* sp : {&bot, &top})
       for (auto& ls : sp->steps)
         for (Step& s : ls) {
           if (s.type == PAIR) {
-            int lw = 0;
-            TN_SOLVER(cusolverDnZgesvdj_bufferSize(solver, CUSOLVER_EIG_MODE_VECTOR, 1, 4 * s.br, 4 * s.bl, nullptr,
-                                                   4 * s.br, nullptr, nullptr, 4 * s.br, nullptr, 4 * s.bl, &lw,
-                                                   svdj));
-            lwork_svd = std::max(lwork_svd, lw);
+            const int mr = std::max(4 * s.bl, 4 * s.br), nc_ = std::min(4 * s.bl, 4 * s.br);
+            size_t dws = 0, hws = 0;
+            if (svd_method == 0) {
+              int lw = 0;
+              TN_SOLVER(cusolverDnZgesvdj_bufferSize(so.h, CUSOLVER_EIG_MODE_VECTOR, 1, mr, nc_, nullptr, mr, nullptr,
+                                                     nullptr, mr, nullptr, nc_, &lw, so.svdj));
+              dws = (size_t)lw * sizeof(cplx);
+            } else if (svd_method == 1) {
+              TN_SOLVER(cusolverDnXgesvdp_bufferSize(so.h, so.prm, CUSOLVER_EIG_MODE_VECTOR, 1, mr, nc_, CUDA_C_64F,
+                                                     nullptr, mr, CUDA_R_64F, nullptr, CUDA_C_64F, nullptr, mr,
+                                                     CUDA_C_64F, nullptr, nc_, CUDA_C_64F, &dws, &hws));
+            } else {
+              TN_SOLVER(cusolverDnXgesvd_bufferSize(so.h, so.prm, 'S', 'S', mr, nc_, CUDA_C_64F, nullptr, mr,
+                                                    CUDA_R_64F, nullptr, CUDA_C_64F, nullptr, mr, CUDA_C_64F, nullptr,
+                                                    nc_, CUDA_C_64F, &dws, &hws));
+            }
+            svd_dws = std::max(svd_dws, dws);
+            svd_hws = std::max(svd_hws, hws);
           } else {
             const int mr = s.type == MOVE_R ? 4 * s.b : 4 * s.bp;
-            const int nc = s.type == MOVE_R ? s.bp : s.b;
+            const int nc_ = s.type == MOVE_R ? s.bp : s.b;
             int lw = 0;
-            TN_SOLVER(cusolverDnZgeqrf_bufferSize(solver, mr, nc, nullptr, mr, &lw));
+            TN_SOLVER(cusolverDnZgeqrf_bufferSize(so.h, mr, nc_, nullptr, mr, &lw));
             lwork_geqrf = std::max(lwork_geqrf, lw);
-            TN_SOLVER(cusolverDnZungqr_bufferSize(solver, mr, s.kq, s.kq, nullptr, mr, nullptr, &lw));
+            TN_SOLVER(cusolverDnZungqr_bufferSize(so.h, mr, s.kq, s.kq, nullptr, mr, nullptr, &lw));
             lwork_ungqr = std::max(lwork_ungqr, lw);
-            maxM = std::max(maxM, mr);
           }
         }
-    (void)maxM;
+    for (Solver& x : sol) x.host_ws.assign(svd_hws + 64, 0);
   }
 
   ~Engine() {
-    if (svdj) cusolverDnDestroyGesvdjInfo(svdj);
-    if (solver) cusolverDnDestroy(solver);
+    for (Solver& so : sol) {
+      if (so.svdj) cusolverDnDestroyGesvdjInfo(so.svdj);
+      if (so.prm) cusolverDnDestroyParams(so.prm);
+      if (so.h) cusolverDnDestroy(so.h);
+    }
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (st2) cudaStreamDestroy(st2);
     if (arena) cudaFree(arena);
     if (ref) cudaFree(ref);
   }
@@ -371,40 +413,85 @@ struct Engine {
     std::vector<int> b;  // bonds
   };
 
-  void qr_right(cudaStream_t st, Pool& pool, const cplx* P, int rows, int cols, int kq, cplx* Q, cplx* R, int* info) {
+  void qr_right(cudaStream_t st, Solver& so, Pool& pool, const cplx* P, int rows, int cols, int kq, cplx* Q, cplx* R, int* info) {
     // P row-major rows x cols -> Q (rows x kq) row-major, R (kq x cols) row-major
     cplx* cm = pool.c((int64_t)rows * cols);
     transpose(st, cm, P, rows, cols, false);  // column-major rows x cols
     cplx* tau = pool.c(std::min(rows, cols));
     cplx* work = pool.c(std::max(lwork_geqrf, lwork_ungqr));
-    TN_SOLVER(cusolverDnSetStream(solver, st));
-    TN_SOLVER(cusolverDnZgeqrf(solver, rows, cols, (cuDoubleComplex*)cm, rows, (cuDoubleComplex*)tau,
+    TN_SOLVER(cusolverDnSetStream(so.h, st));
+    TN_SOLVER(cusolverDnZgeqrf(so.h, rows, cols, (cuDoubleComplex*)cm, rows, (cuDoubleComplex*)tau,
                                (cuDoubleComplex*)work, lwork_geqrf, info));
     tri_extract(st, R, cm, kq, cols, rows, true);
-    TN_SOLVER(cusolverDnZungqr(solver, rows, kq, kq, (cuDoubleComplex*)cm, rows, (cuDoubleComplex*)tau,
+    TN_SOLVER(cusolverDnZungqr(so.h, rows, kq, kq, (cuDoubleComplex*)cm, rows, (cuDoubleComplex*)tau,
                                (cuDoubleComplex*)work, lwork_ungqr, info));
     transpose(st, Q, cm, kq, rows, false);  // cm is (kq x rows) row-major -> Q rows x kq
   }
 
-  void lq_left(cudaStream_t st, Pool& pool, const cplx* P, int rows, int cols, int kq, cplx* Q, cplx* L, int* info) {
+  void lq_left(cudaStream_t st, Solver& so, Pool& pool, const cplx* P, int rows, int cols, int kq, cplx* Q, cplx* L, int* info) {
     // P row-major rows x cols = L (rows x kq) Q (kq x cols), Q row-orthonormal
     cplx* cm = pool.c((int64_t)rows * cols);
     TN_CUDA(cudaMemcpyAsync(cm, P, (size_t)rows * cols * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
     cplx* tau = pool.c(std::min(rows, cols));
     cplx* work = pool.c(std::max(lwork_geqrf, lwork_ungqr));
-    TN_SOLVER(cusolverDnSetStream(solver, st));
+    TN_SOLVER(cusolverDnSetStream(so.h, st));
     // column-major view: cols x rows matrix P^T
-    TN_SOLVER(cusolverDnZgeqrf(solver, cols, rows, (cuDoubleComplex*)cm, cols, (cuDoubleComplex*)tau,
+    TN_SOLVER(cusolverDnZgeqrf(so.h, cols, rows, (cuDoubleComplex*)cm, cols, (cuDoubleComplex*)tau,
                                (cuDoubleComplex*)work, lwork_geqrf, info));
     tri_extract(st, L, cm, rows, kq, cols, false);
-    TN_SOLVER(cusolverDnZungqr(solver, cols, kq, kq, (cuDoubleComplex*)cm, cols, (cuDoubleComplex*)tau,
+    TN_SOLVER(cusolverDnZungqr(so.h, cols, kq, kq, (cuDoubleComplex*)cm, cols, (cuDoubleComplex*)tau,
                                (cuDoubleComplex*)work, lwork_ungqr, info));
     TN_CUDA(cudaMemcpyAsync(Q, cm, (size_t)kq * cols * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
   }
 
+  // Truncated SVD of a row-major (R x Cc) matrix A (destroyed): S (min(R,Cc)),
+  // uh = U_r^H (r x R row-major), vh = W_r^H (r x Cc row-major).
+  void svd_rowmajor(cudaStream_t st, Solver& so, Pool& pool, cplx* A, int R, int Cc, int r, double* S, cplx* uh,
+                    cplx* vh, int* info) {
+    const bool tr = Cc >= R;  // column-major view of A is A^T (Cc x R): use it directly when Cc >= R
+    cplx* M = A;
+    int m = Cc, nn_ = R;
+    if (!tr) {
+      M = pool.c((int64_t)R * Cc);
+      transpose(st, M, A, R, Cc, false);  // column-major R x Cc = A
+      m = R;
+      nn_ = Cc;
+    }
+    const int mn = nn_;
+    cplx* Up = pool.c((int64_t)m * mn);
+    cplx* Vp = pool.c((int64_t)nn_ * mn);
+    void* dws = pool.raw(svd_dws + 64);
+    TN_SOLVER(cusolverDnSetStream(so.h, st));
+    if (svd_method == 0) {
+      TN_SOLVER(cusolverDnZgesvdj(so.h, CUSOLVER_EIG_MODE_VECTOR, 1, m, nn_, (cuDoubleComplex*)M, m, S,
+                                  (cuDoubleComplex*)Up, m, (cuDoubleComplex*)Vp, nn_, (cuDoubleComplex*)dws,
+                                  (int)(svd_dws / sizeof(cplx)), info, so.svdj));
+    } else if (svd_method == 1) {
+      double herr = 0;
+      TN_SOLVER(cusolverDnXgesvdp(so.h, so.prm, CUSOLVER_EIG_MODE_VECTOR, 1, m, nn_, CUDA_C_64F, M, m, CUDA_R_64F, S,
+                                  CUDA_C_64F, Up, m, CUDA_C_64F, Vp, nn_, CUDA_C_64F, dws, svd_dws,
+                                  so.host_ws.data(), svd_hws, info, &herr));
+    } else {
+      // Xgesvd returns V^H (mn x nn_, ldvt = mn) in Vp
+      TN_SOLVER(cusolverDnXgesvd(so.h, so.prm, 'S', 'S', m, nn_, CUDA_C_64F, M, m, CUDA_R_64F, S, CUDA_C_64F, Up, m,
+                                 CUDA_C_64F, Vp, mn, CUDA_C_64F, dws, svd_dws, so.host_ws.data(), svd_hws, info));
+      cplx* V = pool.c((int64_t)nn_ * mn);
+      transpose(st, V, Vp, mn, nn_, true);  // V (col-major nn_ x mn) = (V^H)^H
+      Vp = V;
+    }
+    // column-major M = Up S Vp^H
+    if (tr) {  // M = A^T  ->  A = conj(Vp) S Up^T:  U_A^H = Vp^T, W_A^H = Up^T  (row-major views)
+      TN_CUDA(cudaMemcpyAsync(uh, Vp, (size_t)r * R * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+      TN_CUDA(cudaMemcpyAsync(vh, Up, (size_t)r * Cc * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+    } else {   // M = A  ->  U_A^H = conj(Up^T), W_A^H = conj(Vp^T)
+      conj_copy(st, uh, Up, (int64_t)r * R);
+      conj_copy(st, vh, Vp, (int64_t)r * Cc);
+    }
+  }
+
   // Runs one side's primal sweep.  store: write snapshots / replay data to the arena.
   // Returns the final MPS (pool-owned) -- the top side's T_0.
-  Mps primal_side(cudaStream_t st, Pool& pool, bool is_top, bool store, int* info, double* diag) {
+  Mps primal_side(cudaStream_t st, Solver& so, Pool& pool, bool is_top, bool store, int* info, double* diag) {
     SidePlan& sp = is_top ? top : bot;
     const cplx* G = is_top ? at(o_gdag) : at(o_gates);
     Mps P;
@@ -421,7 +508,6 @@ struct Engine {
         TN_CUDA(cudaMemcpyAsync(P.a[s], id, sizeof(id), cudaMemcpyHostToDevice, st));
       }
     }
-    cplx* sv_buf = nullptr;
     for (size_t li = 0; li < sp.steps.size(); ++li) {
       if (store) snapshot(st, P, sp.o_snap[li]);
       for (const Step& s : sp.steps[li]) {
@@ -429,7 +515,7 @@ struct Engine {
           const int c = s.site;
           cplx* Q = store ? at(s.o_q) : pool.c((int64_t)4 * s.b * s.kq);
           cplx* R = pool.c((int64_t)s.kq * s.bp);
-          qr_right(st, pool, P.a[c], 4 * s.b, s.bp, s.kq, Q, R, info);
+          qr_right(st, so, pool, P.a[c], 4 * s.b, s.bp, s.kq, Q, R, info);
           cplx* nc_ = pool.c((int64_t)4 * s.b * s.kq);
           TN_CUDA(cudaMemcpyAsync(nc_, Q, (size_t)4 * s.b * s.kq * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
           cplx* nx = pool.c((int64_t)s.kq * 4 * s.nb2);
@@ -441,7 +527,7 @@ struct Engine {
           const int c = s.site;
           cplx* Q = store ? at(s.o_q) : pool.c((int64_t)s.kq * 4 * s.bp);
           cplx* L = pool.c((int64_t)s.b * s.kq);
-          lq_left(st, pool, P.a[c], s.b, 4 * s.bp, s.kq, Q, L, info);
+          lq_left(st, so, pool, P.a[c], s.b, 4 * s.bp, s.kq, Q, L, info);
           cplx* nc_ = pool.c((int64_t)s.kq * 4 * s.bp);
           TN_CUDA(cudaMemcpyAsync(nc_, Q, (size_t)s.kq * 4 * s.bp * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
           cplx* nx = pool.c((int64_t)s.nb2 * 4 * s.kq);
@@ -456,21 +542,10 @@ struct Engine {
           nn(st, 4 * s.bl, 4 * s.br, s.m, P.a[i], 0, P.a[i + 1], 0, theta, 0, 1);
           cplx* A = pool.c(nth);
           apply_gate(st, A, 0, theta, 0, G + (int64_t)s.k * 16, 0, s.bl, s.br, 1, ONE, false);
-          // SVD of A (row-major 4bl x 4br) through its column-major view A^T (4br x 4bl):
-          // A^T = U' S V'^H  ->  A = conj(V') S U'^T, so Uh := U_r^H = V'^T (row-major r x 4bl view
-          // of V') and Vh := W_r^H = U'^T (row-major r x 4br view of U').
           double* S = store ? at<double>(s.o_S) : (double*)pool.raw((size_t)s.mn * sizeof(double));
-          cplx* Up = pool.c((int64_t)4 * s.br * s.mn);
-          cplx* Vp = pool.c((int64_t)4 * s.bl * s.mn);
-          if (!sv_buf) sv_buf = pool.c(std::max(lwork_svd, 1));
-          TN_SOLVER(cusolverDnSetStream(solver, st));
-          TN_SOLVER(cusolverDnZgesvdj(solver, CUSOLVER_EIG_MODE_VECTOR, 1, 4 * s.br, 4 * s.bl, (cuDoubleComplex*)A,
-                                      4 * s.br, S, (cuDoubleComplex*)Up, 4 * s.br, (cuDoubleComplex*)Vp, 4 * s.bl,
-                                      (cuDoubleComplex*)sv_buf, lwork_svd, info + 1, svdj));
           cplx* uh = store ? at(s.o_uh) : pool.c((int64_t)s.r * 4 * s.bl);
           cplx* vh = store ? at(s.o_vh) : pool.c((int64_t)s.r * 4 * s.br);
-          TN_CUDA(cudaMemcpyAsync(uh, Vp, (size_t)s.r * 4 * s.bl * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-          TN_CUDA(cudaMemcpyAsync(vh, Up, (size_t)s.r * 4 * s.br * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+          svd_rowmajor(st, so, pool, A, 4 * s.bl, 4 * s.br, s.r, S, uh, vh, info + 1);
           double* sc = store ? at<double>(s.o_s) : (double*)pool.raw(sizeof(double));
           svd_post(st, S, s.mn, s.r, sc, diag);
           cplx* ni = pool.c((int64_t)4 * s.bl * s.r);
@@ -540,17 +615,42 @@ struct Engine {
   void environments(cudaStream_t st, const cplx* gates, double* scalars, cplx* grad_R) {
     TN_CUDA(cudaSetDevice(device));
     primal_valid = false;
-    const double wc0 = work_counter;
+    const double wc0 = work_counter.load();
     Pool pool(st);
     TN_CUDA(cudaMemcpyAsync(at(o_gates), gates, (size_t)K * 16 * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
     dagger4(st, at(o_gdag), at(o_gates), K);
-    const int n_info = 2;
+    // info[0..1]: bottom (qr, svd); info[2..3]: top.  diag: bottom [0..2], top [8..10]
+    const int n_info = 4;
     int* info = (int*)pool.raw(n_info * sizeof(int));
     TN_CUDA(cudaMemsetAsync(info, 0, n_info * sizeof(int), st));
-    double hdiag[8] = {0, 1.0, 0, 0, 0, 0, 0, 0};
-    TN_CUDA(cudaMemcpyAsync(at<double>(o_diag), hdiag, sizeof(hdiag), cudaMemcpyHostToDevice, st));
-    primal_side(st, pool, false, true, info, at<double>(o_diag));
-    primal_side(st, pool, true, true, info, at<double>(o_diag));
+    double* dg = (double*)pool.raw(16 * sizeof(double));
+    double hdiag[16] = {0, 1.0, 0, 0, 0, 0, 0, 0, 0, 1.0, 0, 0, 0, 0, 0, 0};
+    TN_CUDA(cudaMemcpyAsync(dg, hdiag, sizeof(hdiag), cudaMemcpyHostToDevice, st));
+    // fork: the top sweep runs on st2 from a second host thread (cuSOLVER's
+    // Xgesvdp returns to the host per call, so two threads keep both in flight)
+    TN_CUDA(cudaEventRecord(ev_fork, st));
+    TN_CUDA(cudaStreamWaitEvent(st2, ev_fork, 0));
+    std::exception_ptr top_err;
+    std::thread th([&] {
+      try {
+        TN_CUDA(cudaSetDevice(device));
+        Pool pool2(st2);
+        primal_side(st2, sol[1], pool2, true, true, info + 2, dg + 8);
+      } catch (...) {
+        top_err = std::current_exception();
+      }
+    });
+    try {
+      primal_side(st, sol[0], pool, false, true, info, dg);
+    } catch (...) {
+      th.join();
+      throw;
+    }
+    th.join();
+    if (top_err) std::rethrow_exception(top_err);
+    TN_CUDA(cudaEventRecord(ev_join, st2));
+    TN_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
+    combine_diag(st, at<double>(o_diag), dg);
     // T = <<T_0|B_0>>  (Alg. 1)
     cplx* T11 = overlap(st, pool, snap_ptrs(top, D), top.snap[D].p, snap_ptrs(bot, 0), bot.snap[0].p);
     finish_cost(st, at<double>(o_scal), T11);
@@ -568,16 +668,16 @@ struct Engine {
     TN_CUDA(cudaMemcpyAsync(sc, at<double>(o_scal), 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
     TN_CUDA(cudaMemcpyAsync(sc + 3, at<double>(o_diag), 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
     TN_CUDA(cudaStreamSynchronize(st));
-    if (hinfo[0] != 0 || hinfo[1] != 0)
-      throw NumericError("cuSOLVER info nonzero (qr " + std::to_string(hinfo[0]) + ", svd " +
-                         std::to_string(hinfo[1]) + ")");
+    for (int j = 0; j < n_info; ++j)
+      if (hinfo[j] != 0)
+        throw NumericError("cuSOLVER info nonzero (slot " + std::to_string(j) + ": " + std::to_string(hinfo[j]) + ")");
     for (int j = 0; j < 6; ++j)
       if (!std::isfinite(sc[j])) throw NumericError("non-finite primal scalar");
     sc[6] = sc[7] = 0;
     TN_CUDA(cudaMemcpyAsync(scalars, sc, 8 * sizeof(double), cudaMemcpyHostToDevice, st));
     TN_CUDA(cudaMemcpyAsync(at<double>(o_scal), sc, 8 * sizeof(double), cudaMemcpyHostToDevice, st));
     TN_CUDA(cudaStreamSynchronize(st));
-    work_primal = work_counter - wc0;
+    work_primal = work_counter.load() - wc0;
     primal_valid = true;
   }
 
@@ -653,7 +753,7 @@ struct Engine {
     TN_CUDA(cudaMemcpyAsync(at(o_gdag), Gd, (size_t)K * 16 * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
     int* info = (int*)pool.raw(2 * sizeof(int));
     TN_CUDA(cudaMemsetAsync(info, 0, 2 * sizeof(int), st));
-    Mps T0 = primal_side(st, pool, true, false, info, nullptr);
+    Mps T0 = primal_side(st, sol[0], pool, true, false, info, nullptr);
     TN_CUDA(cudaMemcpyAsync(at(o_gdag), saved, (size_t)K * 16 * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
     std::vector<const cplx*> tp(T0.a.begin(), T0.a.end());
     std::vector<int> ones(n + 1, 1);
@@ -1132,7 +1232,7 @@ struct Engine {
   void apply(cudaStream_t st, int batch, const cplx* dirs, cplx* hess, cplx* aux) {
     TN_CUDA(cudaSetDevice(device));
     if (!primal_valid) throw StateError("tn_hvp_apply before tn_hvp_environments");
-    const double wc0 = work_counter;
+    const double wc0 = work_counter.load();
     const int64_t KK = (int64_t)K * 16;
     for (int b0 = 0; b0 < batch; b0 += cfg.max_batch) {
       const int nb = std::min(cfg.max_batch, batch - b0);
@@ -1170,7 +1270,7 @@ struct Engine {
                                 cudaMemcpyDeviceToDevice, st));
       }
     }
-    work_apply = (work_counter - wc0) / std::max(batch, 1);
+    work_apply = (work_counter.load() - wc0) / std::max(batch, 1);
   }
 };
 

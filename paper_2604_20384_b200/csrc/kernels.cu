@@ -414,6 +414,17 @@ __global__ void dagger4_kernel(cplx* __restrict__ dst, const cplx* __restrict__ 
   dst[i] = cconj(src[m * 16 + c * 4 + a]);
 }
 
+__global__ void combine_diag_kernel(double* out, const double* d) {
+  out[0] = fmax(d[0], d[8]);
+  out[1] = fmin(d[1], d[9]);
+  out[2] = fmax(d[2], d[10]);
+}
+
+__global__ void conj_copy_kernel(cplx* __restrict__ dst, const cplx* __restrict__ src, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = cconj(src[i]);
+}
+
 __global__ void finish_cost_kernel(double* scalars, const cplx* T11) {
   const cplx T = T11[0];
   scalars[0] = -(T.x * T.x + T.y * T.y);
@@ -459,6 +470,17 @@ void tri_extract(cudaStream_t st, cplx* dst, const cplx* buf, int rows, int cols
 void dagger4(cudaStream_t st, cplx* dst, const cplx* src, int64_t n) {
   if (!n) return;
   dagger4_kernel<<<(int)((n * 16 + 255) / 256), 256, 0, st>>>(dst, src, n);
+  TN_CUDA(cudaGetLastError());
+}
+
+void combine_diag(cudaStream_t st, double* out, const double* d) {
+  combine_diag_kernel<<<1, 1, 0, st>>>(out, d);
+  TN_CUDA(cudaGetLastError());
+}
+
+void conj_copy(cudaStream_t st, cplx* dst, const cplx* src, int64_t n) {
+  if (!n) return;
+  conj_copy_kernel<<<nblocks(n), TPB, 0, st>>>(dst, src, n);
   TN_CUDA(cudaGetLastError());
 }
 

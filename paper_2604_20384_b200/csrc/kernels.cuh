@@ -37,6 +37,10 @@ void conjT_scale_cols(cudaStream_t st, cplx* dst, const cplx* uh, int r, int m, 
 void tri_extract(cudaStream_t st, cplx* dst, const cplx* buf, int rows, int cols, int64_t lda, bool upper);
 // Vd[b][k] = V[b][k]^dag (4x4 each), n = batch*K matrices.
 void dagger4(cudaStream_t st, cplx* dst, const cplx* src, int64_t n);
+// out[0..2] = (max, min, max) of the two sides' diagnostics d[0..2], d[8..10]
+void combine_diag(cudaStream_t st, double* out, const double* d);
+// dst = conj(src), n elements
+void conj_copy(cudaStream_t st, cplx* dst, const cplx* src, int64_t n);
 // scalars[0] = -|T|^2, [1..2] = T from a 1x1 complex env; keeps [3..] untouched.
 void finish_cost(cudaStream_t st, double* scalars, const cplx* T11);
 }  // namespace tn
