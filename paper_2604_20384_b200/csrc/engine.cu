@@ -75,6 +75,20 @@ struct SidePlan {
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+cplx* dnew(int64_t n, cudaStream_t st) {
+  void* p = nullptr;
+  TN_CUDA(cudaMallocAsync(&p, (size_t)std::max<int64_t>(n, 1) * sizeof(cplx), st));
+  return (cplx*)p;
+}
+void ddel(cplx*& p, cudaStream_t st) {
+  if (p) cudaFreeAsync(p, st);
+  p = nullptr;
+}
+void dset(cplx*& slot, cplx* nw, cudaStream_t st) {
+  ddel(slot, st);
+  slot = nw;
+}
+
 struct Pool {  // stream-ordered transient device buffers
   cudaStream_t st;
   std::vector<void*> ptrs;
@@ -381,6 +395,11 @@ struct Engine {
             }
             svd_dws = std::max(svd_dws, dws);
             svd_hws = std::max(svd_hws, hws);
+            int lw = 0;  // LQ of Y (r x 4br): geqrf on the column-major (4br x r) view
+            TN_SOLVER(cusolverDnZgeqrf_bufferSize(so.h, 4 * s.br, s.r, nullptr, 4 * s.br, &lw));
+            lwork_geqrf = std::max(lwork_geqrf, lw);
+            TN_SOLVER(cusolverDnZungqr_bufferSize(so.h, 4 * s.br, s.r, s.r, nullptr, 4 * s.br, nullptr, &lw));
+            lwork_ungqr = std::max(lwork_ungqr, lw);
           } else {
             const int mr = s.type == MOVE_R ? 4 * s.b : 4 * s.bp;
             const int nc_ = s.type == MOVE_R ? s.bp : s.b;
@@ -444,10 +463,10 @@ struct Engine {
     TN_CUDA(cudaMemcpyAsync(Q, cm, (size_t)kq * cols * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
   }
 
-  // Truncated SVD of a row-major (R x Cc) matrix A (destroyed): S (min(R,Cc)),
-  // uh = U_r^H (r x R row-major), vh = W_r^H (r x Cc row-major).
-  void svd_rowmajor(cudaStream_t st, Solver& so, Pool& pool, cplx* A, int R, int Cc, int r, double* S, cplx* uh,
-                    cplx* vh, int* info) {
+  // SVD of a row-major (R x Cc) matrix A (destroyed): singular values S (mn =
+  // min(R, Cc), descending) and the full left basis uhf = U^H (mn x R row-major).
+  void svd_rowmajor(cudaStream_t st, Solver& so, Pool& pool, cplx* A, int R, int Cc, double* S, cplx* uhf,
+                    int* info) {
     const bool tr = Cc >= R;  // column-major view of A is A^T (Cc x R): use it directly when Cc >= R
     cplx* M = A;
     int m = Cc, nn_ = R;
@@ -476,17 +495,40 @@ struct Engine {
       TN_SOLVER(cusolverDnXgesvd(so.h, so.prm, 'S', 'S', m, nn_, CUDA_C_64F, M, m, CUDA_R_64F, S, CUDA_C_64F, Up, m,
                                  CUDA_C_64F, Vp, mn, CUDA_C_64F, dws, svd_dws, so.host_ws.data(), svd_hws, info));
       cplx* V = pool.c((int64_t)nn_ * mn);
-      transpose(st, V, Vp, mn, nn_, true);  // V (col-major nn_ x mn) = (V^H)^H
+      transpose(st, V, Vp, nn_, mn, true);
       Vp = V;
     }
     // column-major M = Up S Vp^H
-    if (tr) {  // M = A^T  ->  A = conj(Vp) S Up^T:  U_A^H = Vp^T, W_A^H = Up^T  (row-major views)
-      TN_CUDA(cudaMemcpyAsync(uh, Vp, (size_t)r * R * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-      TN_CUDA(cudaMemcpyAsync(vh, Up, (size_t)r * Cc * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-    } else {   // M = A  ->  U_A^H = conj(Up^T), W_A^H = conj(Vp^T)
-      conj_copy(st, uh, Up, (int64_t)r * R);
-      conj_copy(st, vh, Vp, (int64_t)r * Cc);
+    if (tr)  // M = A^T -> A = conj(Vp) S Up^T: U_A^H = Vp^T (row-major view of Vp)
+      TN_CUDA(cudaMemcpyAsync(uhf, Vp, (size_t)mn * R * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+    else     // M = A -> U_A^H = conj(Up)^T
+      conj_copy(st, uhf, Up, (int64_t)mn * R);
+  }
+
+  // Kept left subspace refinement (SVD-method independent, relative accuracy):
+  // with B = U^H A, make the kept rows orthogonal to the discarded rows by the
+  // first-order rotation c_ij = (B_i B_j^H) / (s_j^2 - s_i^2) (one-sided Jacobi
+  // across the cut), twice, then Loewdin re-orthonormalisation of the kept rows.
+  void refine_kept(cudaStream_t st, Pool& pool, cplx* uhf, const double* S, const cplx* A, int R, int Cc, int mn,
+                   int r) {
+    const int nd = mn - r;
+    if (nd <= 0) return;
+    cplx* B = pool.c((int64_t)mn * Cc);
+    cplx* Md = pool.c((int64_t)nd * r);
+    cplx* Cm = pool.c((int64_t)nd * r);
+    cplx* old = pool.c((int64_t)r * R);
+    for (int it = 0; it < 2; ++it) {
+      nn(st, mn, Cc, R, uhf, 0, A, 0, B, 0, 1);
+      nc(st, nd, r, Cc, B + (int64_t)r * Cc, 0, B, 0, Md, 0, 1);
+      kept_rotation(st, Cm, Md, S, nd, r);
+      TN_CUDA(cudaMemcpyAsync(old, uhf, (size_t)r * R * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+      cn(st, r, R, nd, Cm, 0, uhf + (int64_t)r * R, 0, uhf, 0, 1, ONE, ONE);      // kept += C^H disc
+      nn(st, nd, R, r, Cm, 0, old, 0, uhf + (int64_t)r * R, 0, 1, MONE, ONE);    // disc -= C kept_old
     }
+    cplx* F = pool.c((int64_t)r * r);
+    nc(st, r, r, R, uhf, 0, uhf, 0, F, 0, 1);
+    TN_CUDA(cudaMemcpyAsync(old, uhf, (size_t)r * R * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+    nn(st, r, R, r, F, 0, old, 0, uhf, 0, 1, {-0.5, 0.0}, {1.5, 0.0});
   }
 
   // Runs one side's primal sweep.  store: write snapshots / replay data to the arena.
@@ -545,16 +587,28 @@ struct Engine {
           double* S = store ? at<double>(s.o_S) : (double*)pool.raw((size_t)s.mn * sizeof(double));
           cplx* uh = store ? at(s.o_uh) : pool.c((int64_t)s.r * 4 * s.bl);
           cplx* vh = store ? at(s.o_vh) : pool.c((int64_t)s.r * 4 * s.br);
-          svd_rowmajor(st, so, pool, A, 4 * s.bl, 4 * s.br, s.r, S, uh, vh, info + 1);
+          cplx* Acp = pool.c(nth);
+          TN_CUDA(cudaMemcpyAsync(Acp, A, nth * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+          cplx* uhf = pool.c((int64_t)s.mn * 4 * s.bl);
+          svd_rowmajor(st, so, pool, Acp, 4 * s.bl, 4 * s.br, S, uhf, info + 1);
           double* sc = store ? at<double>(s.o_s) : (double*)pool.raw(sizeof(double));
           svd_post(st, S, s.mn, s.r, sc, diag);
+          refine_kept(st, pool, uhf, S, A, 4 * s.bl, 4 * s.br, s.mn, s.r);
+          TN_CUDA(cudaMemcpyAsync(uh, uhf, (size_t)s.r * 4 * s.bl * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+          // Y = U_r^H A (= S_r W_r^H up to a kept-space rotation); LQ gives W_r^H
+          cplx* Y = pool.c((int64_t)s.r * 4 * s.br);
+          nn(st, s.r, 4 * s.br, 4 * s.bl, uh, 0, A, 0, Y, 0, 1);
+          cplx* Lq = pool.c((int64_t)s.r * s.r);
+          lq_left(st, so, pool, Y, s.r, 4 * s.br, s.r, vh, Lq, info);
           cplx* ni = pool.c((int64_t)4 * s.bl * s.r);
           cplx* nj = pool.c((int64_t)s.r * 4 * s.br);
-          if (s.lr) {
+          if (s.lr) {  // (U_r, s U_r^H A), centre -> i+1
             conjT_scale_cols(st, ni, uh, s.r, 4 * s.bl, nullptr, nullptr);
-            scale_rows_sv(st, nj, vh, s.r, 4 * s.br, S, sc);
-          } else {
-            conjT_scale_cols(st, ni, uh, s.r, 4 * s.bl, S, sc);
+            TN_CUDA(cudaMemcpyAsync(nj, Y, (size_t)s.r * 4 * s.br * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+            scale_by(st, nj, sc, 1.0, (int64_t)s.r * 4 * s.br);
+          } else {     // (s U_r L, W_r^H), centre -> i
+            cn(st, 4 * s.bl, s.r, s.r, uh, 0, Lq, 0, ni, 0, 1);
+            scale_by(st, ni, sc, 1.0, (int64_t)4 * s.bl * s.r);
             TN_CUDA(cudaMemcpyAsync(nj, vh, (size_t)s.r * 4 * s.br * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
           }
           P.a[i] = ni;
@@ -782,15 +836,15 @@ struct Engine {
 
   int64_t bsize(const Bonds& b, int s) const { return (int64_t)b.ab[s] * 4 * b.aa[s + 1]; }
 
-  void tangent_init(cudaStream_t st, Pool& pool, Tangent& t, const SidePlan& sp, bool is_top, int nb) {
+  void tangent_init(cudaStream_t st, Tangent& t, const SidePlan& sp, bool is_top, int nb) {
     t.bd = sp.init;
     t.Ab.assign(n, nullptr);
     t.Aa.assign(n, nullptr);
     t.B.assign(n, nullptr);
     for (int s = 0; s < n; ++s) {
       const int64_t e = (int64_t)t.bd.p[s] * 4 * t.bd.p[s + 1];
-      t.Ab[s] = pool.c(e);
-      t.Aa[s] = pool.c(e);
+      t.Ab[s] = dnew(e, st);
+      t.Aa[s] = dnew(e, st);
       const cplx* src = is_top ? ref + ref_off[s] : nullptr;
       if (is_top) {
         TN_CUDA(cudaMemcpyAsync(t.Ab[s], src, e * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
@@ -801,36 +855,43 @@ struct Engine {
         TN_CUDA(cudaMemcpyAsync(t.Ab[s], id, sizeof(id), cudaMemcpyHostToDevice, st));
         TN_CUDA(cudaMemcpyAsync(t.Aa[s], id, sizeof(id), cudaMemcpyHostToDevice, st));
       }
-      t.B[s] = pool.c(e * nb);
+      t.B[s] = dnew(e * nb, st);
       TN_CUDA(cudaMemsetAsync(t.B[s], 0, (size_t)e * nb * sizeof(cplx), st));
     }
   }
 
+  template <class T>
+  void release(T& t, cudaStream_t st) {
+    for (auto* v : {&t.Ab, &t.Aa, &t.B})
+      for (cplx*& p : *v) ddel(p, st);
+  }
+
   // One replayed step on a batch of tangents.  M: gate array (G or G^dag),
   // VM: per-direction gate variations [nb][K][16] (V or V^dag).
-  void tangent_step(cudaStream_t st, Pool& pool, Tangent& t, const Step& s, const cplx* M, const cplx* VM, int nb) {
+  void tangent_step(cudaStream_t st, Tangent& t, const Step& s, const cplx* M, const cplx* VM, int nb) {
     const int64_t KK = (int64_t)K * 16;
+    Pool pool(st);  // step temporaries
     if (s.type == MOVE_R) {
       const int c = s.site, b = s.b, kq = s.kq;
       const int ab1 = s.ab1, ab2 = s.ab2, aa1 = s.aa1, aa2 = s.aa2;
       const cplx* Q = at(s.o_q);                        // (4b x kq)
       cplx* X = pool.c((int64_t)kq * ab1);              // Q^H Ab_c
       cn(st, kq, ab1, 4 * b, Q, 0, t.Ab[c], 0, X, 0, 1);
-      cplx* nAbc = pool.c((int64_t)4 * b * kq);
+      cplx* nAbc = dnew((int64_t)4 * b * kq, st);
       TN_CUDA(cudaMemcpyAsync(nAbc, Q, (size_t)4 * b * kq * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-      cplx* nAb1 = pool.c((int64_t)kq * 4 * ab2);
+      cplx* nAb1 = dnew((int64_t)kq * 4 * ab2, st);
       nn(st, kq, 4 * ab2, ab1, X, 0, t.Ab[c + 1], 0, nAb1, 0, 1);
       // blocks: B_c (b,4,aa1), B_{c+1} (ab1,4,aa2)
       const int64_t sc0 = (int64_t)4 * b * aa1, sc1o = (int64_t)ab1 * 4 * aa2, sc1n = (int64_t)kq * 4 * aa2;
       cplx* Y = pool.c((int64_t)kq * aa1 * nb);
       cn(st, kq, aa1, 4 * b, Q, 0, t.B[c], sc0, Y, (int64_t)kq * aa1, nb);
       nn(st, 4 * b, aa1, kq, Q, 0, Y, (int64_t)kq * aa1, t.B[c], sc0, nb, MONE, ONE);
-      cplx* nB1 = pool.c(sc1n * nb);
+      cplx* nB1 = dnew(sc1n * nb, st);
       nn(st, kq, 4 * aa2, ab1, X, 0, t.B[c + 1], sc1o, nB1, sc1n, nb);
       nn(st, kq, 4 * aa2, aa1, Y, (int64_t)kq * aa1, t.Aa[c + 1], 0, nB1, sc1n, nb, ONE, ONE);
-      t.Ab[c] = nAbc;
-      t.Ab[c + 1] = nAb1;
-      t.B[c + 1] = nB1;
+      dset(t.Ab[c], nAbc, st);
+      dset(t.Ab[c + 1], nAb1, st);
+      dset(t.B[c + 1], nB1, st);
       t.bd.p[c + 1] = kq;
       t.bd.ab[c + 1] = kq;
     } else if (s.type == MOVE_L) {
@@ -839,21 +900,21 @@ struct Engine {
       const cplx* Q = at(s.o_q);                        // (kq x 4bp)
       cplx* X = pool.c((int64_t)aa0 * kq);              // Aa_c Q^H
       nc(st, aa0, kq, 4 * bp, t.Aa[c], 0, Q, 0, X, 0, 1);
-      cplx* nAac = pool.c((int64_t)kq * 4 * bp);
+      cplx* nAac = dnew((int64_t)kq * 4 * bp, st);
       TN_CUDA(cudaMemcpyAsync(nAac, Q, (size_t)kq * 4 * bp * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-      cplx* nAam = pool.c((int64_t)aam * 4 * kq);
+      cplx* nAam = dnew((int64_t)aam * 4 * kq, st);
       nn(st, aam * 4, kq, aa0, t.Aa[c - 1], 0, X, 0, nAam, 0, 1);
       // blocks: B_c (ab0,4,bp), B_{c-1} (abm,4,aa0)
       const int64_t sc0 = (int64_t)ab0 * 4 * bp, sm_o = (int64_t)abm * 4 * aa0, sm_n = (int64_t)abm * 4 * kq;
       cplx* Y = pool.c((int64_t)ab0 * kq * nb);
       nc(st, ab0, kq, 4 * bp, t.B[c], sc0, Q, 0, Y, (int64_t)ab0 * kq, nb);
       nn(st, ab0, 4 * bp, kq, Y, (int64_t)ab0 * kq, Q, 0, t.B[c], sc0, nb, MONE, ONE);
-      cplx* nBm = pool.c(sm_n * nb);
+      cplx* nBm = dnew(sm_n * nb, st);
       nn(st, abm * 4, kq, aa0, t.B[c - 1], sm_o, X, 0, nBm, sm_n, nb);
       nn(st, abm * 4, kq, ab0, t.Ab[c - 1], 0, Y, (int64_t)ab0 * kq, nBm, sm_n, nb, ONE, ONE);
-      t.Aa[c] = nAac;
-      t.Aa[c - 1] = nAam;
-      t.B[c - 1] = nBm;
+      dset(t.Aa[c], nAac, st);
+      dset(t.Aa[c - 1], nAam, st);
+      dset(t.B[c - 1], nBm, st);
       t.bd.p[c] = kq;
       t.bd.aa[c] = kq;
     } else {
@@ -877,8 +938,8 @@ struct Engine {
       nn(st, r, 4 * br, 4 * bl, uh, 0, Dt, nD, UD, sUD, nb);  // U^H D (uh is U^H, r x 4bl)
       cplx* Z = pool.c(sZ * nb);
       nc(st, 4 * bl, r, 4 * br, Dt, nD, vh, 0, Z, sZ, nb);  // D W = D vh^H
-      cplx* nBi = pool.c(sZ * nb);
-      cplx* nBj = pool.c(sUD * nb);
+      cplx* nBi = dnew(sZ * nb, st);
+      cplx* nBj = dnew(sUD * nb, st);
       if (s.lr) {
         // B_{i+1} = s U^H D ; B_i = s (D W - U (U^H D W))
         cplx* UDW = pool.c(sRR * nb);
@@ -898,23 +959,23 @@ struct Engine {
       cplx* aa2t = pool.c((int64_t)16 * aa0 * br);
       nn(st, 4 * aa0, 4 * br, aa1, t.Aa[i], 0, t.Aa[i + 1], 0, aa2t, 0, 1);
       apply_gate(st, aa2t, 0, aa2t, 0, Mk, 0, aa0, br, 1, ONE, false);
-      cplx* nAai = pool.c((int64_t)4 * aa0 * r);
+      cplx* nAai = dnew((int64_t)4 * aa0 * r, st);
       nc(st, 4 * aa0, r, 4 * br, aa2t, 0, vh, 0, nAai, 0, 1, csc);
-      cplx* nAaj = pool.c((int64_t)r * 4 * br);
+      cplx* nAaj = dnew((int64_t)r * 4 * br, st);
       TN_CUDA(cudaMemcpyAsync(nAaj, vh, (size_t)r * 4 * br * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
       cplx* ab2t = pool.c((int64_t)16 * bl * ab2);
       nn(st, 4 * bl, 4 * ab2, ab1, t.Ab[i], 0, t.Ab[i + 1], 0, ab2t, 0, 1);
       apply_gate(st, ab2t, 0, ab2t, 0, Mk, 0, bl, ab2, 1, ONE, false);
-      cplx* nAbj = pool.c((int64_t)r * 4 * ab2);
+      cplx* nAbj = dnew((int64_t)r * 4 * ab2, st);
       nn(st, r, 4 * ab2, 4 * bl, uh, 0, ab2t, 0, nAbj, 0, 1, csc);
-      cplx* nAbi = pool.c((int64_t)4 * bl * r);
+      cplx* nAbi = dnew((int64_t)4 * bl * r, st);
       conjT_scale_cols(st, nAbi, uh, r, 4 * bl, nullptr, nullptr);
-      t.Aa[i] = nAai;
-      t.Aa[i + 1] = nAaj;
-      t.Ab[i] = nAbi;
-      t.Ab[i + 1] = nAbj;
-      t.B[i] = nBi;
-      t.B[i + 1] = nBj;
+      dset(t.Aa[i], nAai, st);
+      dset(t.Aa[i + 1], nAaj, st);
+      dset(t.Ab[i], nAbi, st);
+      dset(t.Ab[i + 1], nAbj, st);
+      dset(t.B[i], nBi, st);
+      dset(t.B[i + 1], nBj, st);
       t.bd.p[i + 1] = r;
       t.bd.ab[i + 1] = r;
       t.bd.aa[i + 1] = r;
@@ -926,7 +987,7 @@ struct Engine {
     Bonds bd;
   };
 
-  TanSnap take_snapshot(cudaStream_t st, Pool& pool, const Tangent& t, int nb) {
+  TanSnap take_snapshot(cudaStream_t st, const Tangent& t, int nb) {
     TanSnap sn;
     sn.bd = t.bd;
     sn.Ab.resize(n);
@@ -936,9 +997,9 @@ struct Engine {
       const int64_t eb = (int64_t)t.bd.ab[s] * 4 * t.bd.ab[s + 1];
       const int64_t ea = (int64_t)t.bd.aa[s] * 4 * t.bd.aa[s + 1];
       const int64_t e = bsize(t.bd, s) * nb;
-      sn.Ab[s] = pool.c(eb);
-      sn.Aa[s] = pool.c(ea);
-      sn.B[s] = pool.c(e);
+      sn.Ab[s] = dnew(eb, st);
+      sn.Aa[s] = dnew(ea, st);
+      sn.B[s] = dnew(e, st);
       TN_CUDA(cudaMemcpyAsync(sn.Ab[s], t.Ab[s], eb * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
       TN_CUDA(cudaMemcpyAsync(sn.Aa[s], t.Aa[s], ea * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
       TN_CUDA(cudaMemcpyAsync(sn.B[s], t.B[s], e * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
@@ -1001,8 +1062,9 @@ struct Engine {
   }
 
   // H_T contributions of layer ell (all three channels) for nb directions.
-  void layer_hvp(cudaStream_t st, Pool& pool, int ell, const TanSnap& DBs, const Tangent& DT, const cplx* V,
-                 cplx* HT, int nb, bool skipB, bool skipT) {
+  void layer_hvp(cudaStream_t st, int ell, const TanSnap& DBs, const Tangent& DT, const cplx* V, cplx* HT, int nb,
+                 bool skipB, bool skipT) {
+    Pool pool(st);  // layer-lifetime buffers
     const auto tpv = snap_ptrs(top, D - ell);
     const auto bpv = snap_ptrs(bot, ell - 1);
     const auto& tb = top.snap[D - ell].p;
@@ -1100,24 +1162,25 @@ struct Engine {
       const int w = k < 0 ? 4 : 16, e = k < 0 ? s + 1 : s + 2;
       Blk& q = bk[s];
       const cplx* R0e = at(o_R[ell][e]);
+      Pool rp(st);  // block temporaries
       // V channel: dRV[s] = (BB dRV[e] + [V] BB R0[e]) TTg^H   (V replaces G: top ungated)
       {
         const int64_t sY = (int64_t)bb[s] * w * tb[e];
-        cplx* Y = pool.c(sY * nb);
+        cplx* Y = rp.c(sY * nb);
         nn(st, w * bb[s], tb[e], bb[e], q.BB, 0, dRV[e], (int64_t)bb[e] * tb[e], Y, sY, nb);
         dRV[s] = pool.c((int64_t)bb[s] * tb[s] * nb);
         nc(st, bb[s], tb[s], w * tb[e], Y, sY, q.TTg, 0, dRV[s], (int64_t)bb[s] * tb[s], nb);
         if (k >= 0) {
-          cplx* Y0 = pool.c(sY);
+          cplx* Y0 = rp.c(sY);
           nn(st, w * bb[s], tb[e], bb[e], q.BB, 0, R0e, 0, Y0, 0, 1);
-          cplx* YV = pool.c(sY * nb);
+          cplx* YV = rp.c(sY * nb);
           apply_gate(st, YV, sY, Y0, 0, Vd + (int64_t)k * 16, KK, bb[s], tb[e], nb, ONE, false);
           nc(st, bb[s], tb[s], w * tb[e], YV, sY, q.TT, 0, dRV[s], (int64_t)bb[s] * tb[s], nb, ONE, ONE);
         }
       }
       if (!skipB) {  // dRB[s] = (BAbB dRB[e] + BBd RBa[e]) TTg^H
         const int64_t sY = (int64_t)xb[s] * w * tb[e];
-        cplx* Y = pool.c(sY * nb);
+        cplx* Y = rp.c(sY * nb);
         nn(st, w * xb[s], tb[e], xb[e], q.BAbB, 0, dRB[e], (int64_t)xb[e] * tb[e], Y, sY, nb);
         nn(st, w * xb[s], tb[e], ya[e], q.BBd, (int64_t)w * xb[s] * ya[e], RBa[e], 0, Y, sY, nb, ONE, ONE);
         dRB[s] = pool.c((int64_t)xb[s] * tb[s] * nb);
@@ -1125,40 +1188,46 @@ struct Engine {
       }
       if (!skipT) {  // dRT[s] = (BB dRT[e]) TAbG^H + (BB RTa[e]) TBdG^H
         const int64_t sY = (int64_t)bb[s] * w * ub[e];
-        cplx* Y = pool.c(sY * nb);
+        cplx* Y = rp.c(sY * nb);
         nn(st, w * bb[s], ub[e], bb[e], q.BB, 0, dRT[e], (int64_t)bb[e] * ub[e], Y, sY, nb);
         dRT[s] = pool.c((int64_t)bb[s] * ub[s] * nb);
         nc(st, bb[s], ub[s], w * ub[e], Y, sY, q.TAbG, 0, dRT[s], (int64_t)bb[s] * ub[s], nb);
         const int64_t sY2 = (int64_t)bb[s] * w * va[e];
-        cplx* Y2 = pool.c(sY2);
+        cplx* Y2 = rp.c(sY2);
         nn(st, w * bb[s], va[e], bb[e], q.BB, 0, RTa[e], 0, Y2, 0, 1);
         nc(st, bb[s], ub[s], w * va[e], Y2, 0, q.TBdG, (int64_t)w * ub[s] * va[e], dRT[s], (int64_t)bb[s] * ub[s],
            nb, ONE, ONE);
       }
     }
     // ---------------- left sweep with extraction
-    cplx* dLV = zero1(1);
-    cplx* dLB = skipB ? nullptr : zero1(1);
-    cplx* dLT = skipT ? nullptr : zero1(1);
+    auto zero_owned = [&](int64_t e) {
+      cplx* p = dnew(e * nb, st);
+      TN_CUDA(cudaMemsetAsync(p, 0, (size_t)e * nb * sizeof(cplx), st));
+      return p;
+    };
+    cplx* dLV = zero_owned(1);
+    cplx* dLB = skipB ? nullptr : zero_owned(1);
+    cplx* dLT = skipT ? nullptr : zero_owned(1);
     for (auto [s, k] : blks) {
       const int w = k < 0 ? 4 : 16, e = k < 0 ? s + 1 : s + 2;
       Blk& q = bk[s];
+      Pool bpool(st);  // block temporaries
       const cplx* L0s = at(o_L[ell][s]);
       const cplx* R0e = at(o_R[ell][e]);
       // Y tensors (open gate, bottom side), per direction, top-index rows: (t x w x b')
       const int64_t sYV = (int64_t)tb[s] * w * bb[e];
-      cplx* YV = pool.c(sYV * nb);  // dLV BB
+      cplx* YV = bpool.c(sYV * nb);  // dLV BB
       nn(st, tb[s], w * bb[e], bb[s], dLV, (int64_t)tb[s] * bb[s], q.BB, 0, YV, sYV, nb);
       cplx* Y0 = nullptr;  // L0 BB (shared)
       if (k >= 0) {
-        Y0 = pool.c(sYV);
+        Y0 = bpool.c(sYV);
         nn(st, tb[s], w * bb[e], bb[s], L0s, 0, q.BB, 0, Y0, 0, 1);
       }
       cplx* YB = nullptr;
       int64_t sYB = 0;
       if (!skipB) {  // dLB BAaB + LBb BBd : (t x w x ya')
         sYB = (int64_t)tb[s] * w * ya[e];
-        YB = pool.c(sYB * nb);
+        YB = bpool.c(sYB * nb);
         nn(st, tb[s], w * ya[e], ya[s], dLB, (int64_t)tb[s] * ya[s], q.BAaB, 0, YB, sYB, nb);
         nn(st, tb[s], w * ya[e], xb[s], LBb[s], 0, q.BBd, (int64_t)w * xb[s] * ya[e], YB, sYB, nb, ONE, ONE);
       }
@@ -1167,20 +1236,20 @@ struct Engine {
       int64_t sYT = 0;
       if (!skipT) {  // dLT BB : (va x w x b') ; LTb BB (shared) : (ub x w x b')
         sYT = (int64_t)va[s] * w * bb[e];
-        YT = pool.c(sYT * nb);
+        YT = bpool.c(sYT * nb);
         nn(st, va[s], w * bb[e], bb[s], dLT, (int64_t)va[s] * bb[s], q.BB, 0, YT, sYT, nb);
-        YT0 = pool.c((int64_t)ub[s] * w * bb[e]);
+        YT0 = bpool.c((int64_t)ub[s] * w * bb[e]);
         nn(st, ub[s], w * bb[e], bb[s], LTb[s], 0, q.BB, 0, YT0, 0, 1);
       }
       if (k >= 0) {
         // ---- extraction: top TT
         const int64_t sZ = (int64_t)16 * tb[s] * tb[e];
-        cplx* Z = pool.c(sZ * nb);
+        cplx* Z = bpool.c(sZ * nb);
         nn(st, 16 * tb[s], tb[e], bb[e], YV, sYV, R0e, 0, Z, sZ, nb);
         nn(st, 16 * tb[s], tb[e], bb[e], Y0, 0, dRV[e], (int64_t)bb[e] * tb[e], Z, sZ, nb, ONE, ONE);
         if (!skipB) {
           nn(st, 16 * tb[s], tb[e], ya[e], YB, sYB, RBa[e], 0, Z, sZ, nb, ONE, ONE);
-          cplx* LBA = pool.c((int64_t)16 * tb[s] * xb[e]);
+          cplx* LBA = bpool.c((int64_t)16 * tb[s] * xb[e]);
           nn(st, tb[s], 16 * xb[e], xb[s], LBb[s], 0, q.BAbB, 0, LBA, 0, 1);
           nn(st, 16 * tb[s], tb[e], xb[e], LBA, 0, dRB[e], (int64_t)xb[e] * tb[e], Z, sZ, nb, ONE, ONE);
         }
@@ -1188,45 +1257,48 @@ struct Engine {
         if (!skipT) {
           // top TAaB with (dLT BB) RTa
           const int64_t sZ2 = (int64_t)16 * va[s] * va[e];
-          cplx* Z2 = pool.c(sZ2 * nb);
+          cplx* Z2 = bpool.c(sZ2 * nb);
           nn(st, 16 * va[s], va[e], bb[e], YT, sYT, RTa[e], 0, Z2, sZ2, nb);
           extract_env(st, HT + (int64_t)k * 16, KK, q.TAaB, 0, Z2, sZ2, va[s], va[e], nb, ONE);
           // per-dir top TBd with shared (LTb BB) RTa
           const int64_t sZ3 = (int64_t)16 * ub[s] * va[e];
-          cplx* Z3 = pool.c(sZ3);
+          cplx* Z3 = bpool.c(sZ3);
           nn(st, 16 * ub[s], va[e], bb[e], YT0, 0, RTa[e], 0, Z3, 0, 1);
           extract_env(st, HT + (int64_t)k * 16, KK, q.TBd, sZ3, Z3, 0, ub[s], va[e], nb, ONE);
           // top TAbB with (LTb BB) dRT
           const int64_t sZ4 = (int64_t)16 * ub[s] * ub[e];
-          cplx* Z4 = pool.c(sZ4 * nb);
+          cplx* Z4 = bpool.c(sZ4 * nb);
           nn(st, 16 * ub[s], ub[e], bb[e], YT0, 0, dRT[e], (int64_t)bb[e] * ub[e], Z4, sZ4, nb);
           extract_env(st, HT + (int64_t)k * 16, KK, q.TAbB, 0, Z4, sZ4, ub[s], ub[e], nb, ONE);
         }
       }
       // ---- left updates
       {  // dLV' = TT^H (G YV + V Y0)  ==  TTg^H YV + TT^H (V Y0)
-        cplx* nL = pool.c((int64_t)tb[e] * bb[e] * nb);
+        cplx* nL = dnew((int64_t)tb[e] * bb[e] * nb, st);
         cn(st, tb[e], bb[e], w * tb[s], q.TTg, 0, YV, sYV, nL, (int64_t)tb[e] * bb[e], nb);
         if (k >= 0) {
-          cplx* YVV = pool.c(sYV * nb);
+          cplx* YVV = bpool.c(sYV * nb);
           apply_gate(st, YVV, sYV, Y0, 0, Vd + (int64_t)k * 16, KK, tb[s], bb[e], nb, ONE, false);
           cn(st, tb[e], bb[e], w * tb[s], q.TT, 0, YVV, sYV, nL, (int64_t)tb[e] * bb[e], nb, ONE, ONE);
         }
-        dLV = nL;
+        dset(dLV, nL, st);
       }
       if (!skipB) {
-        cplx* nL = pool.c((int64_t)tb[e] * ya[e] * nb);
+        cplx* nL = dnew((int64_t)tb[e] * ya[e] * nb, st);
         cn(st, tb[e], ya[e], w * tb[s], q.TTg, 0, YB, sYB, nL, (int64_t)tb[e] * ya[e], nb);
-        dLB = nL;
+        dset(dLB, nL, st);
       }
       if (!skipT) {
-        cplx* nL = pool.c((int64_t)va[e] * bb[e] * nb);
+        cplx* nL = dnew((int64_t)va[e] * bb[e] * nb, st);
         cn(st, va[e], bb[e], w * va[s], q.TAaG, 0, YT, sYT, nL, (int64_t)va[e] * bb[e], nb);
         cn(st, va[e], bb[e], w * ub[s], q.TBdG, (int64_t)w * ub[s] * va[e], YT0, 0, nL, (int64_t)va[e] * bb[e], nb,
            ONE, ONE);
-        dLT = nL;
+        dset(dLT, nL, st);
       }
     }
+    ddel(dLV, st);
+    ddel(dLB, st);
+    ddel(dLT, st);
   }
 
   void apply(cudaStream_t st, int batch, const cplx* dirs, cplx* hess, cplx* aux) {
@@ -1246,20 +1318,23 @@ struct Engine {
       std::vector<TanSnap> DB(D);
       {
         Tangent t;
-        tangent_init(st, pool, t, bot, false, nb);
+        tangent_init(st, t, bot, false, nb);
         for (size_t li = 0; li < bot.steps.size(); ++li) {
-          DB[li] = take_snapshot(st, pool, t, nb);
-          for (const Step& s : bot.steps[li]) tangent_step(st, pool, t, s, at(o_gates), V, nb);
+          DB[li] = take_snapshot(st, t, nb);
+          for (const Step& s : bot.steps[li]) tangent_step(st, t, s, at(o_gates), V, nb);
         }
+        release(t, st);
       }
       // backward (top) tangent on the fly + layer HVP extraction
       Tangent t;
-      tangent_init(st, pool, t, top, true, nb);
+      tangent_init(st, t, top, true, nb);
       for (size_t li = 0; li < top.steps.size(); ++li) {
         const int ell = top.ell[li];
-        layer_hvp(st, pool, ell, DB[ell - 1], t, V, HT, nb, ell == 1, li == 0);
-        for (const Step& s : top.steps[li]) tangent_step(st, pool, t, s, at(o_gdag), Vd, nb);
+        layer_hvp(st, ell, DB[ell - 1], t, V, HT, nb, ell == 1, li == 0);
+        release(DB[ell - 1], st);
+        for (const Step& s : top.steps[li]) tangent_step(st, t, s, at(o_gdag), Vd, nb);
       }
+      release(t, st);
       cplx* om = pool.c(nb);
       hessian_post(st, K, nb, at(o_gates), at(o_E), at(o_gradf), at<double>(o_scal), HT, V, om,
                    hess + (int64_t)b0 * KK);

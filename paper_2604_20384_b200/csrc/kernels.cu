@@ -420,6 +420,17 @@ __global__ void combine_diag_kernel(double* out, const double* d) {
   out[2] = fmax(d[2], d[10]);
 }
 
+__global__ void kept_rotation_kernel(cplx* __restrict__ Cm, const cplx* __restrict__ M, const double* __restrict__ S,
+                                     int nd, int r) {
+  const int64_t n = (int64_t)nd * r;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / r), j = (int)(idx % r);
+    const double sj = S[j], si = S[r + i];
+    const double den = (sj - si) * (sj + si);
+    Cm[idx] = (den > 1e-300) ? cscale(M[idx], 1.0 / den) : make_double2(0.0, 0.0);
+  }
+}
+
 __global__ void conj_copy_kernel(cplx* __restrict__ dst, const cplx* __restrict__ src, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = cconj(src[i]);
@@ -475,6 +486,13 @@ void dagger4(cudaStream_t st, cplx* dst, const cplx* src, int64_t n) {
 
 void combine_diag(cudaStream_t st, double* out, const double* d) {
   combine_diag_kernel<<<1, 1, 0, st>>>(out, d);
+  TN_CUDA(cudaGetLastError());
+}
+
+void kept_rotation(cudaStream_t st, cplx* Cm, const cplx* M, const double* S, int nd, int r) {
+  const int64_t n = (int64_t)nd * r;
+  if (!n) return;
+  kept_rotation_kernel<<<nblocks(n), TPB, 0, st>>>(Cm, M, S, nd, r);
   TN_CUDA(cudaGetLastError());
 }
 

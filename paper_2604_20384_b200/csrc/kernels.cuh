@@ -39,6 +39,10 @@ void tri_extract(cudaStream_t st, cplx* dst, const cplx* buf, int rows, int cols
 void dagger4(cudaStream_t st, cplx* dst, const cplx* src, int64_t n);
 // out[0..2] = (max, min, max) of the two sides' diagnostics d[0..2], d[8..10]
 void combine_diag(cudaStream_t st, double* out, const double* d);
+// C[i][j] = M[i][j] / (S[j]^2 - S[r+i]^2) for i < nd (discarded), j < r (kept);
+// the first-order rotation that makes the kept rows of B = U^H A orthogonal to
+// the discarded ones (one-sided Jacobi step across the cut).
+void kept_rotation(cudaStream_t st, cplx* Cm, const cplx* M, const double* S, int nd, int r);
 // dst = conj(src), n elements
 void conj_copy(cudaStream_t st, cplx* dst, const cplx* src, int64_t n);
 // scalars[0] = -|T|^2, [1..2] = T from a 1x1 complex env; keeps [3..] untouched.
