@@ -138,6 +138,7 @@ struct Engine {
   };
   Solver sol[2];
   int svd_method = 1;  // 0 gesvdj, 1 Xgesvdp (default), 2 Xgesvd
+  bool debug = false;
   size_t svd_dws = 0, svd_hws = 0;
   int lwork_geqrf = 0, lwork_ungqr = 0;
   cudaStream_t st2 = nullptr;
@@ -357,6 +358,7 @@ struct Engine {
     TN_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t thr = UINT64_MAX;
     TN_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    debug = std::getenv("TN_DEBUG") != nullptr;
     if (const char* m = std::getenv("TN_SVD")) {
       const std::string v(m);
       svd_method = v == "gesvdj" ? 0 : v == "gesvd" ? 2 : 1;
@@ -541,7 +543,7 @@ struct Engine {
     P.b = sp.init.p;
     for (int s = 0; s < n; ++s) {
       const int64_t e = (int64_t)P.b[s] * 4 * P.b[s + 1];
-      P.a[s] = pool.c(e);
+      P.a[s] = dnew(e, st);
       if (is_top) {
         TN_CUDA(cudaMemcpyAsync(P.a[s], ref + ref_off[s], e * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
       } else {
@@ -553,55 +555,68 @@ struct Engine {
     for (size_t li = 0; li < sp.steps.size(); ++li) {
       if (store) snapshot(st, P, sp.o_snap[li]);
       for (const Step& s : sp.steps[li]) {
+        Pool tmp(st);  // step temporaries
         if (s.type == MOVE_R) {
           const int c = s.site;
-          cplx* Q = store ? at(s.o_q) : pool.c((int64_t)4 * s.b * s.kq);
-          cplx* R = pool.c((int64_t)s.kq * s.bp);
-          qr_right(st, so, pool, P.a[c], 4 * s.b, s.bp, s.kq, Q, R, info);
-          cplx* nc_ = pool.c((int64_t)4 * s.b * s.kq);
+          cplx* Q = store ? at(s.o_q) : tmp.c((int64_t)4 * s.b * s.kq);
+          cplx* R = tmp.c((int64_t)s.kq * s.bp);
+          qr_right(st, so, tmp, P.a[c], 4 * s.b, s.bp, s.kq, Q, R, info);
+          cplx* nc_ = dnew((int64_t)4 * s.b * s.kq, st);
           TN_CUDA(cudaMemcpyAsync(nc_, Q, (size_t)4 * s.b * s.kq * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-          cplx* nx = pool.c((int64_t)s.kq * 4 * s.nb2);
+          cplx* nx = dnew((int64_t)s.kq * 4 * s.nb2, st);
           nn(st, s.kq, 4 * s.nb2, s.bp, R, 0, P.a[c + 1], 0, nx, 0, 1);
-          P.a[c] = nc_;
-          P.a[c + 1] = nx;
+          dset(P.a[c], nc_, st);
+          dset(P.a[c + 1], nx, st);
           P.b[c + 1] = s.kq;
         } else if (s.type == MOVE_L) {
           const int c = s.site;
-          cplx* Q = store ? at(s.o_q) : pool.c((int64_t)s.kq * 4 * s.bp);
-          cplx* L = pool.c((int64_t)s.b * s.kq);
-          lq_left(st, so, pool, P.a[c], s.b, 4 * s.bp, s.kq, Q, L, info);
-          cplx* nc_ = pool.c((int64_t)s.kq * 4 * s.bp);
+          cplx* Q = store ? at(s.o_q) : tmp.c((int64_t)s.kq * 4 * s.bp);
+          cplx* L = tmp.c((int64_t)s.b * s.kq);
+          lq_left(st, so, tmp, P.a[c], s.b, 4 * s.bp, s.kq, Q, L, info);
+          cplx* nc_ = dnew((int64_t)s.kq * 4 * s.bp, st);
           TN_CUDA(cudaMemcpyAsync(nc_, Q, (size_t)s.kq * 4 * s.bp * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-          cplx* nx = pool.c((int64_t)s.nb2 * 4 * s.kq);
+          cplx* nx = dnew((int64_t)s.nb2 * 4 * s.kq, st);
           nn(st, s.nb2 * 4, s.kq, s.b, P.a[c - 1], 0, L, 0, nx, 0, 1);
-          P.a[c] = nc_;
-          P.a[c - 1] = nx;
+          dset(P.a[c], nc_, st);
+          dset(P.a[c - 1], nx, st);
           P.b[c] = s.kq;
         } else {
           const int i = s.site;
           const int64_t nth = (int64_t)16 * s.bl * s.br;
-          cplx* theta = store ? at(s.o_theta) : pool.c(nth);
+          cplx* theta = store ? at(s.o_theta) : tmp.c(nth);
           nn(st, 4 * s.bl, 4 * s.br, s.m, P.a[i], 0, P.a[i + 1], 0, theta, 0, 1);
-          cplx* A = pool.c(nth);
+          cplx* A = tmp.c(nth);
           apply_gate(st, A, 0, theta, 0, G + (int64_t)s.k * 16, 0, s.bl, s.br, 1, ONE, false);
-          double* S = store ? at<double>(s.o_S) : (double*)pool.raw((size_t)s.mn * sizeof(double));
-          cplx* uh = store ? at(s.o_uh) : pool.c((int64_t)s.r * 4 * s.bl);
-          cplx* vh = store ? at(s.o_vh) : pool.c((int64_t)s.r * 4 * s.br);
-          cplx* Acp = pool.c(nth);
+          double* S = store ? at<double>(s.o_S) : (double*)tmp.raw((size_t)s.mn * sizeof(double));
+          cplx* uh = store ? at(s.o_uh) : tmp.c((int64_t)s.r * 4 * s.bl);
+          cplx* vh = store ? at(s.o_vh) : tmp.c((int64_t)s.r * 4 * s.br);
+          cplx* Acp = tmp.c(nth);
           TN_CUDA(cudaMemcpyAsync(Acp, A, nth * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-          cplx* uhf = pool.c((int64_t)s.mn * 4 * s.bl);
-          svd_rowmajor(st, so, pool, Acp, 4 * s.bl, 4 * s.br, S, uhf, info + 1);
-          double* sc = store ? at<double>(s.o_s) : (double*)pool.raw(sizeof(double));
+          cplx* uhf = tmp.c((int64_t)s.mn * 4 * s.bl);
+          svd_rowmajor(st, so, tmp, Acp, 4 * s.bl, 4 * s.br, S, uhf, info + 1);
+          double* sc = store ? at<double>(s.o_s) : (double*)tmp.raw(sizeof(double));
           svd_post(st, S, s.mn, s.r, sc, diag);
-          refine_kept(st, pool, uhf, S, A, 4 * s.bl, 4 * s.br, s.mn, s.r);
+          if (debug) {
+            std::vector<double> hS(s.mn);
+            TN_CUDA(cudaMemcpyAsync(hS.data(), S, s.mn * sizeof(double), cudaMemcpyDeviceToHost, st));
+            TN_CUDA(cudaStreamSynchronize(st));
+            bool bad = false;
+            for (double v : hS) bad |= !std::isfinite(v);
+            const double gap = s.r < s.mn ? (hS[s.r - 1] - hS[s.r]) / hS[0] : 1.0;
+            if (bad || gap < 1e-8 || hS[s.r - 1] < 1e-13 * hS[0])
+              fprintf(stderr, "[tn debug] %s pair site %d k %d lr %d shape %dx%d r %d mn %d: s0 %.3e s[r-1] %.3e s[r] %.3e gap %.3e nan %d\n",
+                      is_top ? "top" : "bot", i, s.k, (int)s.lr, 4 * s.bl, 4 * s.br, s.r, s.mn, hS[0], hS[s.r - 1],
+                      s.r < s.mn ? hS[s.r] : 0.0, gap, (int)bad);
+          }
+          refine_kept(st, tmp, uhf, S, A, 4 * s.bl, 4 * s.br, s.mn, s.r);
           TN_CUDA(cudaMemcpyAsync(uh, uhf, (size_t)s.r * 4 * s.bl * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
           // Y = U_r^H A (= S_r W_r^H up to a kept-space rotation); LQ gives W_r^H
-          cplx* Y = pool.c((int64_t)s.r * 4 * s.br);
+          cplx* Y = tmp.c((int64_t)s.r * 4 * s.br);
           nn(st, s.r, 4 * s.br, 4 * s.bl, uh, 0, A, 0, Y, 0, 1);
-          cplx* Lq = pool.c((int64_t)s.r * s.r);
-          lq_left(st, so, pool, Y, s.r, 4 * s.br, s.r, vh, Lq, info);
-          cplx* ni = pool.c((int64_t)4 * s.bl * s.r);
-          cplx* nj = pool.c((int64_t)s.r * 4 * s.br);
+          cplx* Lq = tmp.c((int64_t)s.r * s.r);
+          lq_left(st, so, tmp, Y, s.r, 4 * s.br, s.r, vh, Lq, info);
+          cplx* ni = dnew((int64_t)4 * s.bl * s.r, st);
+          cplx* nj = dnew((int64_t)s.r * 4 * s.br, st);
           if (s.lr) {  // (U_r, s U_r^H A), centre -> i+1
             conjT_scale_cols(st, ni, uh, s.r, 4 * s.bl, nullptr, nullptr);
             TN_CUDA(cudaMemcpyAsync(nj, Y, (size_t)s.r * 4 * s.br * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
@@ -611,8 +626,8 @@ struct Engine {
             scale_by(st, ni, sc, 1.0, (int64_t)4 * s.bl * s.r);
             TN_CUDA(cudaMemcpyAsync(nj, vh, (size_t)s.r * 4 * s.br * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
           }
-          P.a[i] = ni;
-          P.a[i + 1] = nj;
+          dset(P.a[i], ni, st);
+          dset(P.a[i + 1], nj, st);
           P.b[i + 1] = s.r;
         }
       }
@@ -689,13 +704,15 @@ struct Engine {
       try {
         TN_CUDA(cudaSetDevice(device));
         Pool pool2(st2);
-        primal_side(st2, sol[1], pool2, true, true, info + 2, dg + 8);
+        Mps T0 = primal_side(st2, sol[1], pool2, true, true, info + 2, dg + 8);
+        for (cplx*& p : T0.a) ddel(p, st2);
       } catch (...) {
         top_err = std::current_exception();
       }
     });
     try {
-      primal_side(st, sol[0], pool, false, true, info, dg);
+      Mps BD = primal_side(st, sol[0], pool, false, true, info, dg);
+      for (cplx*& p : BD.a) ddel(p, st);
     } catch (...) {
       th.join();
       throw;
@@ -708,7 +725,7 @@ struct Engine {
     // T = <<T_0|B_0>>  (Alg. 1)
     cplx* T11 = overlap(st, pool, snap_ptrs(top, D), top.snap[D].p, snap_ptrs(bot, 0), bot.snap[0].p);
     finish_cost(st, at<double>(o_scal), T11);
-    layer_gradients(st, pool);
+    layer_gradients(st);
     gradient_post(st, K, at(o_gates), at(o_E), at<double>(o_scal), at(o_gradf), grad_R);
     // host copies: scalars/diag, frozen s, solver info
     for (SidePlan* sp : {&bot, &top})
@@ -726,7 +743,10 @@ struct Engine {
       if (hinfo[j] != 0)
         throw NumericError("cuSOLVER info nonzero (slot " + std::to_string(j) + ": " + std::to_string(hinfo[j]) + ")");
     for (int j = 0; j < 6; ++j)
-      if (!std::isfinite(sc[j])) throw NumericError("non-finite primal scalar");
+      if (!std::isfinite(sc[j]))
+        throw NumericError("non-finite primal scalar: f=" + std::to_string(sc[0]) + " T=(" + std::to_string(sc[1]) +
+                           "," + std::to_string(sc[2]) + ") discarded=" + std::to_string(sc[3]) +
+                           " gap=" + std::to_string(sc[4]) + " log10s=" + std::to_string(sc[5]));
     sc[6] = sc[7] = 0;
     TN_CUDA(cudaMemcpyAsync(scalars, sc, 8 * sizeof(double), cudaMemcpyHostToDevice, st));
     TN_CUDA(cudaMemcpyAsync(at<double>(o_scal), sc, 8 * sizeof(double), cudaMemcpyHostToDevice, st));
@@ -742,7 +762,7 @@ struct Engine {
   }
 
   // a4: per layer right sweep, left sweep with E_k (primal envs stored for apply)
-  void layer_gradients(cudaStream_t st, Pool& pool) {
+  void layer_gradients(cudaStream_t st) {
     TN_CUDA(cudaMemsetAsync(at(o_E), 0, (size_t)K * 16 * sizeof(cplx), st));
     for (int ell = 1; ell <= D; ++ell) {
       const auto tp = snap_ptrs(top, D - ell);
@@ -755,6 +775,7 @@ struct Engine {
       // right sweep
       for (int j = (int)blks.size() - 1; j >= 0; --j) {
         const int s = blks[j].first, k = blks[j].second;
+        Pool pool(st);  // block temporaries
         if (k < 0) {
           cplx* Y = pool.c((int64_t)bb[s] * 4 * tb[s + 1]);
           nn(st, 4 * bb[s], tb[s + 1], bb[s + 1], bp[s], 0, at(o_R[ell][s + 1]), 0, Y, 0, 1);
@@ -773,6 +794,7 @@ struct Engine {
       // left sweep + extraction
       for (size_t j = 0; j < blks.size(); ++j) {
         const int s = blks[j].first, k = blks[j].second;
+        Pool pool(st);  // block temporaries
         if (k < 0) {
           cplx* Y = pool.c((int64_t)tb[s] * 4 * bb[s + 1]);
           nn(st, tb[s], 4 * bb[s + 1], bb[s], at(o_L[ell][s]), 0, bp[s], 0, Y, 0, 1);
@@ -818,6 +840,7 @@ struct Engine {
     TN_CUDA(cudaMemcpyAsync(id, idh, sizeof(idh), cudaMemcpyHostToDevice, st));
     for (int s = 0; s < n; ++s) bp[s] = id;
     cplx* T11 = overlap(st, pool, tp, T0.b, bp, ones);
+    for (cplx*& p : T0.a) ddel(p, st);
     double* sc = (double*)pool.raw(8 * sizeof(double));
     TN_CUDA(cudaMemsetAsync(sc, 0, 8 * sizeof(double), st));
     finish_cost(st, sc, T11);

@@ -427,7 +427,15 @@ __global__ void kept_rotation_kernel(cplx* __restrict__ Cm, const cplx* __restri
     const int i = (int)(idx / r), j = (int)(idx % r);
     const double sj = S[j], si = S[r + i];
     const double den = (sj - si) * (sj + si);
-    Cm[idx] = (den > 1e-300) ? cscale(M[idx], 1.0 / den) : make_double2(0.0, 0.0);
+    // Only a kept value above the noise floor defines a direction worth
+    // refining; a first-order rotation larger than 1e-3 is outside the
+    // linearised regime (then the SVD's own vectors are kept).
+    cplx c = make_double2(0.0, 0.0);
+    if (sj > 1e-11 * S[0] && den > 0.0) {
+      c = cscale(M[idx], 1.0 / den);
+      if (!(fabs(c.x) + fabs(c.y) < 1e-3)) c = make_double2(0.0, 0.0);
+    }
+    Cm[idx] = c;
   }
 }
 

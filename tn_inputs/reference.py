@@ -64,13 +64,25 @@ def tebd_out_legs(sites, layers, chi: int, tol: float = 1e-14):
             bl, br = sites[i].shape[0], sites[i + 1].shape[2]
             th = torch.einsum("apb,bqc->apqc", sites[i], sites[i + 1])
             th = _apply_out_gate(th, gt).reshape(bl * 4, 4 * br)
-            u, s, vh = torch.linalg.svd(th, full_matrices=False)
-            keep = int(min(chi, int((s > tol * s[0]).sum().item())))
-            keep = max(keep, 1)
-            nrm = torch.linalg.vector_norm(s)
-            sk = s[:keep] * (nrm / torch.linalg.vector_norm(s[:keep]))
-            sites[i] = u[:, :keep].reshape(bl, 4, keep)
-            sites[i + 1] = (sk[:, None].to(vh.dtype) * vh[:keep]).reshape(keep, 4, br)
+            nrm = torch.linalg.vector_norm(th)
+            if th.is_cuda:
+                # GPU input generation: split through the Gram matrix (eigh is
+                # ~15x faster than the GPU SVD at 1024^2); values below ~1e-7
+                # of the largest are resolved only roughly, which only changes
+                # WHICH reference MPO is generated, not its use downstream.
+                w, v = torch.linalg.eigh(th @ th.mH)
+                w, v = w.flip(0).clamp_min(0.0), v.flip(1)
+                keep = max(1, int(min(chi, int((w > (max(tol, 1e-7) ** 2) * w[0]).sum().item()))))
+                u = v[:, :keep]
+                right = u.mH @ th
+            else:
+                u, s, vh = torch.linalg.svd(th, full_matrices=False)
+                keep = max(1, int(min(chi, int((s > tol * s[0]).sum().item()))))
+                u = u[:, :keep]
+                right = s[:keep, None].to(vh.dtype) * vh[:keep]
+            right = right * (nrm / torch.linalg.vector_norm(right))
+            sites[i] = u.reshape(bl, 4, keep)
+            sites[i + 1] = right.reshape(keep, 4, br)
             c = i + 1
     while c > 0:
         _move_left(sites, c); c -= 1
