@@ -1,0 +1,301 @@
+"""Benchmark of the HVP hot path (BASELINE.json metric: HVPs/sec, complex128,
+and the fraction of the FP64 roofline) on 1..N B200s.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+A step is one pass of the whole hot path over one
+batch: tn_hvp_environments (primal sweeps, layer environments, f, grad_R) then
+tn_hvp_apply on the config's batch of tangent directions.  Multi-GPU: one
+process per GPU (torchrun), each rank runs the full per-GPU batch on its own
+directions with its own primal (weak scaling; the path has no exchange step
+inside the HVP).  value = directions of all ranks / max-over-ranks step time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from tn_inputs import configs as C  # noqa: E402
+
+METRIC = "HVPs/sec (complex128) and fraction of FP64/HBM roofline at 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=int(os.environ.get("TN_BENCH_CONFIG", 3)))
+    ap.add_argument("--batch", type=int, default=None, help="directions per GPU (default: the config's)")
+    ap.add_argument("--max-batch", type=int, default=None, help="internal sub-batch (memory)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------ helpers --
+class Clocks:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.rows = []
+        if self.proc is None:
+            return
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def summary(self):
+        if not getattr(self, "rows", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for r in self.rows for j in range(4) if r[2 + j].lower() == "active"})
+        loaded = [v for v in sm if v > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def fp64_peak():
+    """Measured DMMA peak (TF/s): live probe, else the committed measurement."""
+    exe = os.path.join(ROOT, "paper_2604_20384_b200", "bin", "fp64_peak")
+    try:
+        out = subprocess.run([exe], capture_output=True, text=True, timeout=60).stdout
+        d = json.loads(out)
+        return d["dmma_tflops"], "live bin/fp64_peak DMMA loop (MEASURED_PEAKS.json has no FP64 entry)"
+    except Exception:
+        with open(os.path.join(ROOT, "profiles", "r01_fp64_peak_probe.json")) as f:
+            d = json.load(f)
+        return d["loops"]["dmma_tflops"], "profiles/r01_fp64_peak_probe.json DMMA loop"
+
+
+def dist_init(n):
+    if n <= 1 and "WORLD_SIZE" not in os.environ:
+        return 0, 1, 0
+    import torch.distributed as dist
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------- oracle sample --
+def oracle_sample(cfg, ref_cpu, G):
+    """The CPU oracle (O3) as it stands on a bounded sample of the workload:
+    the first layer of the circuit against the full reference, 1 direction.
+    Rate extrapolated to the full depth assuming cost linear in D (stated)."""
+    from oracle import mpo as M
+    t0 = time.time()
+    K1 = C.num_gates(cfg.n, 1, cfg.first_offset)
+    V = C.tangent_directions(cfg.cid, G, 1)[:, :K1]
+    o = M.MPOOracle(cfg.n, 1, cfg.chi, G[:K1], ref_cpu, V, cfg.first_offset)
+    o.gradient_T()
+    o.hvp_T(0)
+    dt = time.time() - t0
+    hvps = 1.0 / cfg.depth / dt
+    return hvps, dt
+
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    ref = C.reference_mpo(cfg, device="cuda" if torch.cuda.is_available() else "cpu")
+    ref_cpu = [a.detach().resolve_conj().cpu().numpy() for a in ref]
+    G = C.haar_gates(cfg.cid, C.num_gates(cfg.n, cfg.depth, cfg.first_offset))
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        oracle_sample(cfg, ref_cpu, G)
+    rates, times = [], []
+    for _ in range(args.steps):
+        r, dt = oracle_sample(cfg, ref_cpu, G)
+        rates.append(r)
+        times.append(dt)
+    v = statistics.median(rates)
+    cores = torch.get_num_threads()
+    sample = (f"O3 numpy oracle, layer 1 of {cfg.depth} (its {C.num_gates(cfg.n, 1)} gates) vs the full reference, "
+              f"1 direction; HVPs/s extrapolated x1/{cfg.depth} assuming cost linear in depth")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "HVPs/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": cfg.name, "n": cfg.n, "depth": cfg.depth, "chi": cfg.chi},
+        "cpu_baseline": {"value": v, "unit": "HVPs/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": v, "unit": "HVPs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+# ----------------------------------------------------------------- ours --
+def main():
+    args = parse()
+    cfg = C.CONFIGS[args.config]
+    rank, world, local = dist_init(args.gpus)
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+    from paper_2604_20384_b200 import _native as N
+    from paper_2604_20384_b200.api import HVPEngine
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    B = args.batch or cfg.batch
+    mb = args.max_batch or {1: 1, 2: 16, 3: 64, 4: 16, 5: 1}[cfg.cid]
+    K = C.num_gates(cfg.n, cfg.depth, cfg.first_offset)
+    ref = C.reference_mpo(cfg, device=dev)
+    Gnp = C.haar_gates(cfg.cid, K)
+    Vnp = C.tangent_directions(cfg.cid, Gnp, B, offset=rank * B)   # each rank: its own directions
+    G = torch.tensor(Gnp, device=dev)
+    V = torch.tensor(Vnp, device=dev)
+    eng = HVPEngine(cfg.n, cfg.depth, cfg.chi, ref, cfg.first_offset, max_batch=mb)
+    out = torch.empty_like(V)
+
+    def step():
+        eng.environments(G)
+        eng.apply(V, out=out)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # instrumented (untimed) pass: GEMM kernel time and work of one step
+    N.tn_gemm_profile(1)
+    step()
+    torch.cuda.synchronize()
+    gemm_ms, gemm_cmac = N.tn_gemm_profile(0)
+    l0 = N.tn_hvp_launch_count()
+    step()
+    torch.cuda.synchronize()
+    launches = N.tn_hvp_launch_count() - l0
+    cmac_dir, cmac_primal = eng.work()
+
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        e0.record(st)
+        for _ in range(args.steps):
+            step()
+        e1.record(st)
+        torch.cuda.synchronize()
+    barrier(world)
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+    value = world * B / (ms / 1e3)
+
+    # end-to-end through the public API with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        Gh = torch.tensor(Gnp).pin_memory()
+        Vh = torch.tensor(Vnp).pin_memory()
+        Hh = torch.empty(Vh.shape, dtype=Vh.dtype).pin_memory()
+        Sh = torch.empty(8, dtype=torch.float64).pin_memory()
+        Gd, Vd = torch.empty_like(G), torch.empty_like(V)
+
+        def step_e2e():
+            Gd.copy_(Gh, non_blocking=True)
+            Vd.copy_(Vh, non_blocking=True)
+            sc, _ = eng.environments(Gd)
+            eng.apply(Vd, out=out)
+            Hh.copy_(out, non_blocking=True)
+            Sh.copy_(sc, non_blocking=True)
+
+        step_e2e()
+        torch.cuda.synchronize()
+        barrier(world)
+        e0.record(st)
+        for _ in range(args.steps):
+            step_e2e()
+        e1.record(st)
+        torch.cuda.synchronize()
+        barrier(world)
+        ms_e2e = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+        e2e = {"value": world * B / (ms_e2e / 1e3), "unit": "HVPs/s",
+               "h2d_bytes_per_step": int(Gh.numel() * 16 + Vh.numel() * 16),
+               "d2h_bytes_per_step": int(Hh.numel() * 16 + 8 * 8)}
+
+    peak, peak_src = fp64_peak()
+    achieved = 8 * gemm_cmac / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_c{cfg.cid}.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get("bytes_per_launch")
+    line = {
+        "metric": METRIC, "value": value, "unit": "HVPs/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": cfg.name, "n": cfg.n, "depth": cfg.depth, "chi": cfg.chi, "gates": K,
+                   "directions_per_gpu": B, "sub_batch": mb, "parallelism": f"weak x{world} (directions)",
+                   "l2": "working set (primal store, tangent caches: GBs) > 126 MB L2; no flush"},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "kernel": "zgemm_kernel (DMMA m8n8k4 f64)", "peak_source": peak_src,
+                     "gemm_share_of_step": gemm_ms / ms if ms else None,
+                     "flops_per_step": 8 * gemm_cmac, "apply_cmac_per_direction": cmac_dir,
+                     "primal_cmac": cmac_primal},
+        "clocks": clk.summary(),
+        "gpu_launches": int(launches),
+        "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ref_cpu = [a.detach().resolve_conj().cpu().numpy() for a in ref]
+        v, dt = oracle_sample(cfg, ref_cpu, Gnp)
+        line["cpu_baseline"] = {"value": v, "unit": "HVPs/s", "cores": torch.get_num_threads(), "kind": "oracle",
+                                "sample": f"O3 numpy oracle on layer 1 of {cfg.depth} (vs the full reference), "
+                                          f"1 direction, {dt:.1f} s; extrapolated x1/{cfg.depth}"}
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

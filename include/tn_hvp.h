@@ -126,6 +126,16 @@ tn_status tn_zgemm(char opa, char opb, int32_t M, int32_t N, int32_t K, const do
  * context runs), and the bytes of the dominant kernel class; for rooflines. */
 tn_status tn_hvp_work(tn_hvp_ctx* ctx, double* cmac_per_direction, double* cmac_primal);
 
+/* Number of kernels this library has launched since it was loaded (all
+ * contexts, all streams) -- the bench's gpu_launches evidence. */
+int64_t tn_hvp_launch_count(void);
+
+/* GEMM timing probe for the roofline: mode 1 = reset and start recording a
+ * CUDA-event pair around every DMMA GEMM launch; mode 0 = stop, synchronise
+ * the recorded events and return the summed kernel milliseconds and complex
+ * MACs (HOST outputs, may be NULL when mode = 1). */
+tn_status tn_gemm_profile(int32_t mode, double* ms, double* cmac);
+
 void tn_hvp_destroy(tn_hvp_ctx* ctx);
 
 /* Last error text of ctx (or of the calling thread when ctx is NULL). */

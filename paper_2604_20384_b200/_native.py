@@ -16,7 +16,7 @@ STATUS = {0: "TN_OK", 1: "TN_EINVAL", 2: "TN_ENOMEM", 3: "TN_ECUDA", 4: "TN_ENUM
 
 EXPORTS = ["tn_hvp_num_gates", "tn_hvp_setup", "tn_hvp_environments", "tn_hvp_apply", "tn_hvp_gradient_T",
            "tn_hvp_cost", "tn_hvp_primal_blob", "tn_hvp_primal_imported", "tn_riemannian_project", "tn_zgemm",
-           "tn_hvp_work", "tn_hvp_destroy", "tn_hvp_last_error"]
+           "tn_hvp_work", "tn_hvp_launch_count", "tn_gemm_profile", "tn_hvp_destroy", "tn_hvp_last_error"]
 
 
 class TNError(RuntimeError):
@@ -53,6 +53,10 @@ def lib():
         L.tn_zgemm.argtypes = [C.c_char, C.c_char, i32, i32, i32, C.POINTER(C.c_double), vp, i64, i64, vp, i64, i64,
                                C.POINTER(C.c_double), vp, i64, i64, i32, vp]
         L.tn_hvp_work.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.tn_hvp_launch_count.argtypes = []
+        L.tn_hvp_launch_count.restype = C.c_int64
+        L.tn_gemm_profile.argtypes = [i32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.tn_gemm_profile.restype = C.c_int
         L.tn_hvp_destroy.argtypes = [vp]
         L.tn_hvp_destroy.restype = None
         L.tn_hvp_last_error.argtypes = [vp]
@@ -125,6 +129,16 @@ def tn_zgemm(opa, opb, M, N, K, alpha, A, lda, sA, B, ldb, sB, beta, Cp, ldc, sC
 def tn_hvp_work(ctx):
     a, b = C.c_double(), C.c_double()
     check(lib().tn_hvp_work(ctx, C.byref(a), C.byref(b)), ctx)
+    return a.value, b.value
+
+
+def tn_hvp_launch_count():
+    return lib().tn_hvp_launch_count()
+
+
+def tn_gemm_profile(mode):
+    a, b = C.c_double(), C.c_double()
+    check(lib().tn_gemm_profile(mode, C.byref(a), C.byref(b)))
     return a.value, b.value
 
 

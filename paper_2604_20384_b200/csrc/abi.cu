@@ -135,6 +135,22 @@ tn_status tn_hvp_work(tn_hvp_ctx* ctx, double* per_dir, double* primal) {
   return guarded(ctx, [&] { tn::engine_work(ctx, per_dir, primal); });
 }
 
+int64_t tn_hvp_launch_count(void) { return tn::launch_count(); }
+
+tn_status tn_gemm_profile(int32_t mode, double* ms, double* cmac) {
+  if (mode != 0 && mode != 1) return fail(nullptr, TN_EINVAL, "tn_gemm_profile: mode must be 0 or 1");
+  return guarded(nullptr, [&] {
+    if (mode == 1) {
+      tn::gemm_profile_begin();
+    } else {
+      double a = 0, b = 0;
+      tn::gemm_profile_end(&a, &b);
+      if (ms) *ms = a;
+      if (cmac) *cmac = b;
+    }
+  });
+}
+
 void tn_hvp_destroy(tn_hvp_ctx* ctx) {
   if (ctx) tn::engine_destroy(ctx);
 }

@@ -36,6 +36,13 @@ __host__ __device__ inline cplx csub(cplx a, cplx b) { return make_double2(a.x -
 __host__ __device__ inline cplx cscale(cplx a, double s) { return make_double2(a.x * s, a.y * s); }
 __host__ __device__ inline cplx cconj(cplx a) { return make_double2(a.x, -a.y); }
 
+// Kernel-launch counter of this library (all wrappers bump it) and the
+// optional per-launch GEMM timing used by bench.py's roofline.
+void count_launch(int64_t n = 1);
+int64_t launch_count();
+void gemm_profile_begin();                      // enable + reset (host side)
+void gemm_profile_end(double* ms, double* cmac);  // sync, disable, read totals
+
 // Batched row-major complex GEMM on DMMA (zgemm.cu).
 // C[b] = alpha * op(A[b]) * op(B[b]) + beta * C[b]; op(A): M x K, op(B): K x N.
 // opa/opb in {'N','T','C'}; strides in elements, 0 = operand shared.

@@ -269,18 +269,21 @@ void apply_gate(cudaStream_t st, cplx* out, int64_t sout, const cplx* x, int64_t
   apply_gate_kernel<<<nblocks(total), TPB, 0, st>>>(out, sout, x, sx, gate, sg, X, Y, batch, alpha,
                                                     accumulate ? 1 : 0);
   TN_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 void axpby(cudaStream_t st, cplx* y, const cplx* x, cplx a, cplx b, int64_t n) {
   if (n == 0) return;
   axpby_kernel<<<nblocks(n), TPB, 0, st>>>(y, x, a, b, n);
   TN_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 void scale_by(cudaStream_t st, cplx* y, const double* s, double pw, int64_t n) {
   if (n == 0) return;
   scale_kernel<<<nblocks(n), TPB, 0, st>>>(y, s, pw, n);
   TN_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 void extract_env(cudaStream_t st, cplx* E, int64_t sE, const cplx* top, int64_t stop, const cplx* z, int64_t sz,
@@ -292,6 +295,7 @@ void extract_env(cudaStream_t st, cplx* E, int64_t sE, const cplx* top, int64_t 
   dim3 grid(bx, batch);
   extract_env_kernel<<<grid, TPB, 0, st>>>(E, sE, top, stop, z, sz, T, U, alpha);
   TN_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 void project(cudaStream_t st, int K, int batch, const cplx* G, const cplx* in, cplx* out) {
@@ -299,21 +303,25 @@ void project(cudaStream_t st, int K, int batch, const cplx* G, const cplx* in, c
   if (n == 0) return;
   project_kernel<<<(int)((n + 127) / 128), 128, 0, st>>>(K, batch, G, in, out);
   TN_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 void gradient_post(cudaStream_t st, int K, const cplx* G, const cplx* E, const double* scal, cplx* grad_f,
                    cplx* grad_R) {
   gradient_kernel<<<(K + 127) / 128, 128, 0, st>>>(K, G, E, scal, grad_f, grad_R);
   TN_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 void hessian_post(cudaStream_t st, int K, int batch, const cplx* G, const cplx* E, const cplx* grad_f,
                   const double* scal, const cplx* HT, const cplx* V, cplx* om, cplx* out) {
   omega_kernel<<<batch, TPB, 0, st>>>(K, E, V, om);
   TN_CUDA(cudaGetLastError());
+  count_launch();
   const int64_t n = (int64_t)K * batch;
   hessian_kernel<<<(int)((n + 63) / 64), 64, 0, st>>>(K, batch, G, E, grad_f, scal, HT, V, om, out);
   TN_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 }  // namespace tn
@@ -457,11 +465,13 @@ void transpose(cudaStream_t st, cplx* dst, const cplx* src, int rows, int cols, 
   dim3 grid((cols + 31) / 32, (rows + 31) / 32), block(32, 8);
   transpose_kernel<<<grid, block, 0, st>>>(dst, src, rows, cols, conj ? 1 : 0);
   TN_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 void svd_post(cudaStream_t st, const double* S, int mn, int r, double* s_out, double* diag) {
   svd_post_kernel<<<1, 256, 0, st>>>(S, mn, r, s_out, diag);
   TN_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 void scale_rows_sv(cudaStream_t st, cplx* dst, const cplx* src, int rows, int cols, const double* S,
@@ -470,6 +480,7 @@ void scale_rows_sv(cudaStream_t st, cplx* dst, const cplx* src, int rows, int co
   if (!n) return;
   scale_rows_kernel<<<nblocks(n), TPB, 0, st>>>(dst, src, rows, cols, S, s);
   TN_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 void conjT_scale_cols(cudaStream_t st, cplx* dst, const cplx* uh, int r, int m, const double* S, const double* s) {
@@ -477,6 +488,7 @@ void conjT_scale_cols(cudaStream_t st, cplx* dst, const cplx* uh, int r, int m, 
   if (!n) return;
   conjT_scale_kernel<<<nblocks(n), TPB, 0, st>>>(dst, uh, r, m, S, s);
   TN_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 void tri_extract(cudaStream_t st, cplx* dst, const cplx* buf, int rows, int cols, int64_t lda, bool upper) {
@@ -484,17 +496,20 @@ void tri_extract(cudaStream_t st, cplx* dst, const cplx* buf, int rows, int cols
   if (!n) return;
   tri_kernel<<<nblocks(n), TPB, 0, st>>>(dst, buf, rows, cols, lda, upper ? 1 : 0);
   TN_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 void dagger4(cudaStream_t st, cplx* dst, const cplx* src, int64_t n) {
   if (!n) return;
   dagger4_kernel<<<(int)((n * 16 + 255) / 256), 256, 0, st>>>(dst, src, n);
   TN_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 void combine_diag(cudaStream_t st, double* out, const double* d) {
   combine_diag_kernel<<<1, 1, 0, st>>>(out, d);
   TN_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 void kept_rotation(cudaStream_t st, cplx* Cm, const cplx* M, const double* S, int nd, int r) {
@@ -502,16 +517,19 @@ void kept_rotation(cudaStream_t st, cplx* Cm, const cplx* M, const double* S, in
   if (!n) return;
   kept_rotation_kernel<<<nblocks(n), TPB, 0, st>>>(Cm, M, S, nd, r);
   TN_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 void conj_copy(cudaStream_t st, cplx* dst, const cplx* src, int64_t n) {
   if (!n) return;
   conj_copy_kernel<<<nblocks(n), TPB, 0, st>>>(dst, src, n);
   TN_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 void finish_cost(cudaStream_t st, double* scalars, const cplx* T11) {
   finish_cost_kernel<<<1, 1, 0, st>>>(scalars, T11);
   TN_CUDA(cudaGetLastError());
+  count_launch();
 }
 }  // namespace tn

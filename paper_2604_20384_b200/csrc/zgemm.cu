@@ -10,11 +10,23 @@
 // strides padded so every fragment load (one LDS.128 = one complex) is
 // bank-conflict free.  op(A), op(B) in {N, T, C}; conjugation is folded into
 // the fragment sign.  Row-major everywhere; batch strides may be 0 (shared).
+#include <atomic>
+#include <mutex>
+#include <vector>
+
 #include "common.cuh"
 
 namespace tn {
 namespace {
 
+std::atomic<int64_t> g_launches{0};
+struct Prof {
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  std::vector<double> cm;
+};
+Prof g_prof;
+std::mutex g_prof_mu;
 constexpr int BM = 64, BN = 64, BK = 16, NT = 128;
 constexpr int LDN = BK + 4;    // [rows][BK] tiles: row stride = 20 complex (= 4 mod 8 slots)
 constexpr int LDT = BM + 2;    // [BK][cols] tiles: row stride = 66 complex (= 2 mod 8 slots)
@@ -168,8 +180,21 @@ void launch(const Params& p, int batch, cudaStream_t st) {
     attr = true;
   }
   dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, batch);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (g_prof.on) {
+    TN_CUDA(cudaEventCreate(&e0));
+    TN_CUDA(cudaEventCreate(&e1));
+    TN_CUDA(cudaEventRecord(e0, st));
+  }
   zgemm_kernel<OPA, OPB><<<grid, NT, SMEM_BYTES, st>>>(p);
   TN_CUDA(cudaGetLastError());
+  count_launch();
+  if (g_prof.on) {
+    TN_CUDA(cudaEventRecord(e1, st));
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof.ev.push_back({e0, e1});
+    g_prof.cm.push_back((double)p.M * p.N * p.K * batch);
+  }
 }
 
 template <char OPA>
@@ -182,7 +207,41 @@ void dispatch_b(char opb, const Params& p, int batch, cudaStream_t st) {
   }
 }
 
+
 }  // namespace
+
+void count_launch(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+int64_t launch_count() { return g_launches.load(); }
+
+void gemm_profile_begin() {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (auto& e : g_prof.ev) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  g_prof.ev.clear();
+  g_prof.cm.clear();
+  g_prof.on = true;
+}
+
+void gemm_profile_end(double* ms, double* cmac) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof.on = false;
+  double t = 0, c = 0;
+  for (size_t i = 0; i < g_prof.ev.size(); ++i) {
+    TN_CUDA(cudaEventSynchronize(g_prof.ev[i].second));
+    float m = 0;
+    TN_CUDA(cudaEventElapsedTime(&m, g_prof.ev[i].first, g_prof.ev[i].second));
+    t += m;
+    c += g_prof.cm[i];
+    cudaEventDestroy(g_prof.ev[i].first);
+    cudaEventDestroy(g_prof.ev[i].second);
+  }
+  g_prof.ev.clear();
+  g_prof.cm.clear();
+  *ms = t;
+  *cmac = c;
+}
 
 void zgemm(cudaStream_t st, char opa, char opb, int M, int N, int K, cplx alpha, const cplx* A, int64_t lda,
            int64_t sA, const cplx* B, int64_t ldb, int64_t sB, cplx beta, cplx* C, int64_t ldc, int64_t sC,
