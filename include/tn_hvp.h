@@ -114,6 +114,21 @@ tn_status tn_hvp_primal_imported(tn_hvp_ctx* ctx, const void* gates, void* strea
 tn_status tn_riemannian_project(int32_t K, int32_t batch, const void* gates, const void* in, void* out,
                                 void* stream);
 
+/* Retraction for the trust region: out_k = polar factor of (G_k + alpha xi_k)
+ * (unitary to machine precision).  DEVICE gates, xi, out
+ * [K][4][4]; returns TN_ENUMERIC if an iterate is singular (synchronises). */
+tn_status tn_retract(int32_t K, const void* gates, const void* xi, double alpha, void* out, void* stream);
+
+/* Tangent-vector algebra for tCG on U(4)^K (metric Re sum Tr(A^dag B), X15):
+ * out[b] = Re <A_b, B_b> over n complex entries each (DEVICE double[batch]);
+ * y = a x + b y over n complex entries (a, b complex, HOST double[2]). */
+tn_status tn_tangent_dot(int64_t n, int32_t batch, const void* A, const void* B, void* out, void* stream);
+tn_status tn_tangent_axpby(int64_t n, const double* a, const void* x, const double* b, void* y, void* stream);
+
+/* Copy the primal store to (into_ctx = 0) or from (into_ctx = 1) a caller
+ * DEVICE buffer of exactly tn_hvp_primal_blob's size (broadcast support). */
+tn_status tn_hvp_primal_copy(tn_hvp_ctx* ctx, void* buf, size_t bytes, int32_t into_ctx, void* stream);
+
 /* Building block exposed for tests: batched complex128 GEMM on the FP64
  * tensor cores (DMMA), C[b] = alpha op(A[b]) op(B[b]) + beta C[b], row-major,
  * op in {'N','T','C'}; op(A) is M x K.  Strides in elements (0 = shared).

@@ -16,7 +16,8 @@ STATUS = {0: "TN_OK", 1: "TN_EINVAL", 2: "TN_ENOMEM", 3: "TN_ECUDA", 4: "TN_ENUM
 
 EXPORTS = ["tn_hvp_num_gates", "tn_hvp_setup", "tn_hvp_environments", "tn_hvp_apply", "tn_hvp_gradient_T",
            "tn_hvp_cost", "tn_hvp_primal_blob", "tn_hvp_primal_imported", "tn_riemannian_project", "tn_zgemm",
-           "tn_hvp_work", "tn_hvp_launch_count", "tn_gemm_profile", "tn_hvp_destroy", "tn_hvp_last_error"]
+           "tn_hvp_work", "tn_retract", "tn_tangent_dot", "tn_tangent_axpby", "tn_hvp_primal_copy",
+           "tn_hvp_launch_count", "tn_gemm_profile", "tn_hvp_destroy", "tn_hvp_last_error"]
 
 
 class TNError(RuntimeError):
@@ -53,6 +54,12 @@ def lib():
         L.tn_zgemm.argtypes = [C.c_char, C.c_char, i32, i32, i32, C.POINTER(C.c_double), vp, i64, i64, vp, i64, i64,
                                C.POINTER(C.c_double), vp, i64, i64, i32, vp]
         L.tn_hvp_work.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.tn_retract.argtypes = [i32, vp, vp, C.c_double, vp, vp]
+        L.tn_tangent_dot.argtypes = [i64, i32, vp, vp, vp, vp]
+        L.tn_tangent_axpby.argtypes = [i64, C.POINTER(C.c_double), vp, C.POINTER(C.c_double), vp, vp]
+        L.tn_hvp_primal_copy.argtypes = [vp, vp, C.c_size_t, i32, vp]
+        for name in ("tn_retract", "tn_tangent_dot", "tn_tangent_axpby", "tn_hvp_primal_copy"):
+            getattr(L, name).restype = C.c_int
         L.tn_hvp_launch_count.argtypes = []
         L.tn_hvp_launch_count.restype = C.c_int64
         L.tn_gemm_profile.argtypes = [i32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
@@ -130,6 +137,26 @@ def tn_hvp_work(ctx):
     a, b = C.c_double(), C.c_double()
     check(lib().tn_hvp_work(ctx, C.byref(a), C.byref(b)), ctx)
     return a.value, b.value
+
+
+def tn_retract(K, gates_ptr, xi_ptr, alpha, out_ptr, stream):
+    check(lib().tn_retract(K, C.c_void_p(gates_ptr), C.c_void_p(xi_ptr), alpha, C.c_void_p(out_ptr),
+                           C.c_void_p(stream)))
+
+
+def tn_tangent_dot(n, batch, A_ptr, B_ptr, out_ptr, stream):
+    check(lib().tn_tangent_dot(n, batch, C.c_void_p(A_ptr), C.c_void_p(B_ptr), C.c_void_p(out_ptr),
+                               C.c_void_p(stream)))
+
+
+def tn_tangent_axpby(n, a, x_ptr, b, y_ptr, stream):
+    av = (C.c_double * 2)(complex(a).real, complex(a).imag)
+    bv = (C.c_double * 2)(complex(b).real, complex(b).imag)
+    check(lib().tn_tangent_axpby(n, av, C.c_void_p(x_ptr), bv, C.c_void_p(y_ptr), C.c_void_p(stream)))
+
+
+def tn_hvp_primal_copy(ctx, buf_ptr, nbytes, into_ctx, stream):
+    check(lib().tn_hvp_primal_copy(ctx, C.c_void_p(buf_ptr), nbytes, into_ctx, C.c_void_p(stream)), ctx)
 
 
 def tn_hvp_launch_count():

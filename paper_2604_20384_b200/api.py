@@ -118,3 +118,45 @@ def zgemm(A: torch.Tensor, B: torch.Tensor, opa="N", opb="N", alpha=1.0, beta=0.
     N.tn_zgemm(opa, opb, M, Nn, K, complex(alpha), A3.data_ptr(), A3.shape[2], sA, B3.data_ptr(), B3.shape[2], sB,
                complex(beta), C.data_ptr(), Nn, M * Nn, batch, _stream())
     return C
+
+
+def retract(gates: torch.Tensor, xi: torch.Tensor, alpha: float = 1.0) -> torch.Tensor:
+    """Polar retraction R_G(alpha xi) = polar(G + alpha xi), gate-wise."""
+    _require_cuda(gates, "gates")
+    _require_cuda(xi, "xi")
+    out = torch.empty_like(gates)
+    N.tn_retract(gates.shape[0], gates.data_ptr(), xi.data_ptr(), float(alpha), out.data_ptr(), _stream())
+    return out
+
+
+def tangent_dot(A: torch.Tensor, B: torch.Tensor) -> torch.Tensor:
+    """Re <A_b, B_b> for [batch, ...] tangent vectors -> float64 [batch] (device)."""
+    _require_cuda(A, "A")
+    _require_cuda(B, "B")
+    batch = A.shape[0] if A.dim() == 4 else 1
+    n = A.numel() // batch
+    out = torch.empty(batch, dtype=torch.float64, device=A.device)
+    N.tn_tangent_dot(n, batch, A.data_ptr(), B.data_ptr(), out.data_ptr(), _stream())
+    return out
+
+
+def axpby(a, x: torch.Tensor, b, y: torch.Tensor) -> torch.Tensor:
+    """y <- a x + b y in place (complex scalars a, b)."""
+    _require_cuda(x, "x")
+    _require_cuda(y, "y")
+    N.tn_tangent_axpby(x.numel(), a, x.data_ptr(), b, y.data_ptr(), _stream())
+    return y
+
+
+def primal_export(eng: "HVPEngine") -> torch.Tensor:
+    """Copy the context's primal store into a uint8 torch tensor (for a broadcast)."""
+    _, n = eng.primal_blob()
+    buf = torch.empty(n, dtype=torch.uint8, device=eng.device)
+    N.tn_hvp_primal_copy(eng.ctx, buf.data_ptr(), n, 0, _stream())
+    return buf
+
+
+def primal_import(eng: "HVPEngine", buf: torch.Tensor, gates: torch.Tensor):
+    """Fill the primal store from a buffer produced by primal_export (same shapes)."""
+    N.tn_hvp_primal_copy(eng.ctx, buf.data_ptr(), buf.numel(), 1, _stream())
+    eng.primal_imported(gates)

@@ -135,6 +135,51 @@ tn_status tn_hvp_work(tn_hvp_ctx* ctx, double* per_dir, double* primal) {
   return guarded(ctx, [&] { tn::engine_work(ctx, per_dir, primal); });
 }
 
+tn_status tn_retract(int32_t K, const void* gates, const void* xi, double alpha, void* out, void* stream) {
+  if (K < 0 || (K && (!gates || !xi || !out))) return fail(nullptr, TN_EINVAL, "tn_retract: bad argument");
+  return guarded(nullptr, [&] {
+    if (!K) return;
+    int* st = nullptr;
+    TN_CUDA(cudaMallocAsync((void**)&st, sizeof(int), (cudaStream_t)stream));
+    TN_CUDA(cudaMemsetAsync(st, 0, sizeof(int), (cudaStream_t)stream));
+    tn::retract((cudaStream_t)stream, K, (const tn::cplx*)gates, (const tn::cplx*)xi, alpha, (tn::cplx*)out, st);
+    int h = 0;
+    TN_CUDA(cudaMemcpyAsync(&h, st, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    TN_CUDA(cudaFreeAsync(st, (cudaStream_t)stream));
+    TN_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    if (h) throw tn::NumericError("tn_retract: singular iterate");
+  });
+}
+
+tn_status tn_tangent_dot(int64_t n, int32_t batch, const void* A, const void* B, void* out, void* stream) {
+  if (n < 0 || batch < 0 || (n && batch && (!A || !B || !out))) return fail(nullptr, TN_EINVAL, "tn_tangent_dot: bad argument");
+  return guarded(nullptr, [&] {
+    tn::tangent_dot((cudaStream_t)stream, n, batch, (const tn::cplx*)A, (const tn::cplx*)B, (double*)out);
+  });
+}
+
+tn_status tn_tangent_axpby(int64_t n, const double* a, const void* x, const double* b, void* y, void* stream) {
+  if (n < 0 || !a || !b || (n && (!x || !y))) return fail(nullptr, TN_EINVAL, "tn_tangent_axpby: bad argument");
+  return guarded(nullptr, [&] {
+    tn::axpby((cudaStream_t)stream, (tn::cplx*)y, (const tn::cplx*)x, make_double2(a[0], a[1]),
+              make_double2(b[0], b[1]), n);
+  });
+}
+
+tn_status tn_hvp_primal_copy(tn_hvp_ctx* ctx, void* buf, size_t bytes, int32_t into_ctx, void* stream) {
+  if (!ctx || !buf || (into_ctx != 0 && into_ctx != 1)) return fail(ctx, TN_EINVAL, "tn_hvp_primal_copy: bad argument");
+  return guarded(ctx, [&] {
+    void* p = nullptr;
+    size_t n = 0;
+    tn::engine_primal_blob(ctx, &p, &n);
+    if (bytes != n) throw std::invalid_argument("tn_hvp_primal_copy: size mismatch");
+    if (into_ctx)
+      TN_CUDA(cudaMemcpyAsync(p, buf, n, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    else
+      TN_CUDA(cudaMemcpyAsync(buf, p, n, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  });
+}
+
 int64_t tn_hvp_launch_count(void) { return tn::launch_count(); }
 
 tn_status tn_gemm_profile(int32_t mode, double* ms, double* cmac) {

@@ -452,6 +452,88 @@ __global__ void conj_copy_kernel(cplx* __restrict__ dst, const cplx* __restrict_
     dst[i] = cconj(src[i]);
 }
 
+// ---------------------------------------------------------- retraction --
+// 4x4 complex inverse by Gauss-Jordan with partial pivoting (in registers).
+__device__ bool inv4(const cplx* a, cplx* out) {
+  cplx m[4][8];
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 8; ++j) m[i][j] = j < 4 ? a[i * 4 + j] : make_double2(i == j - 4 ? 1.0 : 0.0, 0.0);
+  for (int c = 0; c < 4; ++c) {
+    int piv = c;
+    double best = hypot(m[c][c].x, m[c][c].y);
+    for (int r = c + 1; r < 4; ++r) {
+      const double v = hypot(m[r][c].x, m[r][c].y);
+      if (v > best) { best = v; piv = r; }
+    }
+    if (best == 0.0) return false;
+    if (piv != c)
+      for (int j = 0; j < 8; ++j) { const cplx t = m[c][j]; m[c][j] = m[piv][j]; m[piv][j] = t; }
+    const cplx d = m[c][c];
+    const double dn = d.x * d.x + d.y * d.y;
+    const cplx di = make_double2(d.x / dn, -d.y / dn);
+    for (int j = 0; j < 8; ++j) m[c][j] = cmul(m[c][j], di);
+    for (int r = 0; r < 4; ++r)
+      if (r != c) {
+        const cplx f = m[r][c];
+        for (int j = 0; j < 8; ++j) m[r][j] = csub(m[r][j], cmul(f, m[c][j]));
+      }
+  }
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) out[i * 4 + j] = m[i][j + 4];
+  return true;
+}
+
+// out_k = polar factor of (G_k + alpha xi_k): scaled Newton X <- (g X + X^{-H}/g)/2,
+// g = (||X^-1||_F / ||X||_F)^{1/2}, to machine precision (SPEC.md:475-483 retraction).
+__global__ void retract_kernel(int K, const cplx* __restrict__ G, const cplx* __restrict__ xi, double alpha,
+                               cplx* __restrict__ out, int* status) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  cplx x[16], xinv[16];
+  for (int e = 0; e < 16; ++e) x[e] = cadd(G[k * 16 + e], cscale(xi[k * 16 + e], alpha));
+  for (int it = 0; it < 60; ++it) {
+    if (!inv4(x, xinv)) { atomicExch(status, 1); break; }
+    double nx = 0, ni = 0;
+    for (int e = 0; e < 16; ++e) {
+      nx += x[e].x * x[e].x + x[e].y * x[e].y;
+      ni += xinv[e].x * xinv[e].x + xinv[e].y * xinv[e].y;
+    }
+    const double g = it < 8 ? sqrt(sqrt(ni / nx)) : 1.0;
+    double delta = 0;
+    cplx y[16];
+    for (int a = 0; a < 4; ++a)
+      for (int b = 0; b < 4; ++b) {
+        const cplx inh = cconj(xinv[b * 4 + a]);  // (X^{-1})^H
+        y[a * 4 + b] = cscale(cadd(cscale(x[a * 4 + b], g), cscale(inh, 1.0 / g)), 0.5);
+        const cplx d = csub(y[a * 4 + b], x[a * 4 + b]);
+        delta += d.x * d.x + d.y * d.y;
+      }
+    for (int e = 0; e < 16; ++e) x[e] = y[e];
+    if (it >= 8 && delta < 1e-30) break;
+  }
+  for (int e = 0; e < 16; ++e) out[k * 16 + e] = x[e];
+}
+
+// out[b] = Re sum_i conj(A[b,i]) B[b,i]   (metric Re Tr(A^dag B), X15)
+__global__ void tangent_dot_kernel(int64_t n, const cplx* __restrict__ A, const cplx* __restrict__ B,
+                                   double* __restrict__ out) {
+  const int b = blockIdx.x;
+  double acc = 0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const cplx a = A[b * n + i], c = B[b * n + i];
+    acc += a.x * c.x + a.y * c.y;
+  }
+  __shared__ double red[32];
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int j = 0; j < (int)(blockDim.x >> 5); ++j) t += red[j];
+    out[b] = t;
+  }
+}
+
 __global__ void finish_cost_kernel(double* scalars, const cplx* T11) {
   const cplx T = T11[0];
   scalars[0] = -(T.x * T.x + T.y * T.y);
@@ -523,6 +605,20 @@ void kept_rotation(cudaStream_t st, cplx* Cm, const cplx* M, const double* S, in
 void conj_copy(cudaStream_t st, cplx* dst, const cplx* src, int64_t n) {
   if (!n) return;
   conj_copy_kernel<<<nblocks(n), TPB, 0, st>>>(dst, src, n);
+  TN_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+void retract(cudaStream_t st, int K, const cplx* G, const cplx* xi, double alpha, cplx* out, int* status) {
+  if (!K) return;
+  retract_kernel<<<(K + 63) / 64, 64, 0, st>>>(K, G, xi, alpha, out, status);
+  TN_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+void tangent_dot(cudaStream_t st, int64_t n, int batch, const cplx* A, const cplx* B, double* out) {
+  if (!batch) return;
+  tangent_dot_kernel<<<batch, 256, 0, st>>>(n, A, B, out);
   TN_CUDA(cudaGetLastError());
   count_launch();
 }

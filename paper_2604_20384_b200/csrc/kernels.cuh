@@ -45,6 +45,10 @@ void combine_diag(cudaStream_t st, double* out, const double* d);
 void kept_rotation(cudaStream_t st, cplx* Cm, const cplx* M, const double* S, int nd, int r);
 // dst = conj(src), n elements
 void conj_copy(cudaStream_t st, cplx* dst, const cplx* src, int64_t n);
+// out_k = polar(G_k + alpha xi_k) (unitary retraction); status[0] = 1 on a singular iterate
+void retract(cudaStream_t st, int K, const cplx* G, const cplx* xi, double alpha, cplx* out, int* status);
+// out[b] = Re <A_b, B_b> over n complex entries per batch item
+void tangent_dot(cudaStream_t st, int64_t n, int batch, const cplx* A, const cplx* B, double* out);
 // scalars[0] = -|T|^2, [1..2] = T from a 1x1 complex env; keeps [3..] untouched.
 void finish_cost(cudaStream_t st, double* scalars, const cplx* T11);
 }  // namespace tn

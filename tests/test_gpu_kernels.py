@@ -49,3 +49,46 @@ def test_projection_kernel_matches_oracle():
     out = riemannian_project(torch.tensor(G, device=dev), torch.tensor(Z, device=dev)).cpu().numpy()
     ref = np.stack([cm.project(G, Z[b]) for b in range(3)])
     assert np.abs(out - ref).max() < 1e-15
+
+
+def test_retraction_is_the_polar_factor():
+    from paper_2604_20384_b200.api import retract
+    G = C.haar_gates(78, 7)
+    xi = 0.3 * _rand(G.shape, 9)
+    dev = torch.device("cuda")
+    out = retract(torch.tensor(G, device=dev), torch.tensor(xi, device=dev)).cpu().numpy()
+    for k in range(7):
+        u, _, vh = np.linalg.svd(G[k] + xi[k])
+        assert np.abs(out[k] - u @ vh).max() < 1e-13
+        assert np.abs(out[k].conj().T @ out[k] - np.eye(4)).max() < 1e-14
+
+
+def test_tangent_algebra():
+    from paper_2604_20384_b200.api import axpby, tangent_dot
+    dev = torch.device("cuda")
+    A, B = _rand((3, 5, 4, 4), 10), _rand((3, 5, 4, 4), 11)
+    d = tangent_dot(torch.tensor(A, device=dev), torch.tensor(B, device=dev)).cpu().numpy()
+    assert np.abs(d - np.real(np.sum(np.conj(A) * B, axis=(1, 2, 3)))).max() < 1e-12
+    y = torch.tensor(B, device=dev)
+    axpby(0.5 - 1j, torch.tensor(A, device=dev), 2.0, y)
+    assert np.abs(y.cpu().numpy() - ((0.5 - 1j) * A + 2.0 * B)).max() < 1e-14
+
+
+def test_primal_export_import_roundtrip():
+    from paper_2604_20384_b200.api import HVPEngine, primal_export, primal_import
+    from tn_inputs.reference import reference_mpo
+    cfg = C.small_case(79, 6, 4, 8, batch=2)
+    ref = reference_mpo(C.reference_layers(cfg), cfg.n, cfg.chi)
+    K = C.num_gates(cfg.n, cfg.depth)
+    G1, G2 = C.haar_gates(79, K), C.haar_gates(80, K)
+    V = C.tangent_directions(79, G1, 2)
+    dev = torch.device("cuda")
+    eng = HVPEngine(cfg.n, cfg.depth, cfg.chi, [a.to(dev) for a in ref], max_batch=2)
+    g1 = torch.tensor(G1, device=dev)
+    eng.environments(g1)
+    H1 = eng.apply(torch.tensor(V, device=dev)).cpu().numpy()
+    blob = primal_export(eng).clone()
+    eng.environments(torch.tensor(G2, device=dev))
+    primal_import(eng, blob, g1)
+    H2 = eng.apply(torch.tensor(V, device=dev)).cpu().numpy()
+    assert np.array_equal(H1, H2)

@@ -100,3 +100,25 @@ def test_chi_convergence_to_exact():
         errs.append(rel(o3.hvp_T(0), H))
     assert errs[0] > errs[1] > 1e-9
     assert errs[2] < 1e-12
+
+
+def test_insensitive_to_noise_floor_directions():
+    """Reading X10: with chi above the reference's numerical rank the cut falls
+    inside the ~1e-14 noise floor (kept directions there are arbitrary); the
+    outputs nevertheless move only at roundoff level under 1e-15 gate jitter."""
+    n, D, chi = 8, 4, 128
+    cfg = C.Config(3, "noise", n, D, chi, C.CONFIGS[3].model, 1.0, 20, 2, 1)
+    ref = reference_mpo(C.reference_layers(cfg), n, 1024)
+    refs = [a.numpy() for a in ref]
+    G = C.haar_gates(3, C.num_gates(n, D))
+    V = C.tangent_directions(3, G, 1)
+    rng = np.random.default_rng(5)
+    P = 1e-15 * (rng.standard_normal(G.shape) + 1j * rng.standard_normal(G.shape))
+    outs = []
+    for Gx in (G, G + P):
+        o = M.MPOOracle(n, D, chi, Gx, refs, V)
+        outs.append((o.T, o.gradient_T(), o.hvp_T(0), o.diag))
+    sig = [d["sigma"][d["r"] - 1] / d["sigma"][0] for d in outs[0][3]["top"]]
+    assert min(sig) < 1e-13                      # the cut really is in the noise floor
+    assert abs(outs[0][0] - outs[1][0]) < 1e-12 * abs(outs[0][0])
+    assert rel(outs[1][2], outs[0][2]) < 1e-12
