@@ -137,7 +137,8 @@ struct Engine {
     std::vector<char> host_ws;
   };
   Solver sol[2];
-  int svd_method = 1;  // 0 gesvdj, 1 Xgesvdp (default), 2 Xgesvd
+  int svd_method = 3;  // 0 gesvdj, 1 Xgesvdp, 2 Xgesvd, 3 Gram heevd (default)
+  int lwork_heevd = 0;
   bool debug = false;
   size_t svd_dws = 0, svd_hws = 0;
   int lwork_geqrf = 0, lwork_ungqr = 0;
@@ -361,7 +362,7 @@ struct Engine {
     debug = std::getenv("TN_DEBUG") != nullptr;
     if (const char* m = std::getenv("TN_SVD")) {
       const std::string v(m);
-      svd_method = v == "gesvdj" ? 0 : v == "gesvd" ? 2 : 1;
+      svd_method = v == "gesvdj" ? 0 : v == "gesvd" ? 2 : v == "gesvdp" ? 1 : 3;
     }
     TN_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
     TN_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
@@ -381,7 +382,14 @@ struct Engine {
           if (s.type == PAIR) {
             const int mr = std::max(4 * s.bl, 4 * s.br), nc_ = std::min(4 * s.bl, 4 * s.br);
             size_t dws = 0, hws = 0;
-            if (svd_method == 0) {
+            {
+              int lw = 0;
+              TN_SOLVER(cusolverDnZheevd_bufferSize(so.h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, 4 * s.bl,
+                                                    nullptr, 4 * s.bl, nullptr, &lw));
+              lwork_heevd = std::max(lwork_heevd, lw);
+            }
+            if (svd_method == 3) {
+            } else if (svd_method == 0) {
               int lw = 0;
               TN_SOLVER(cusolverDnZgesvdj_bufferSize(so.h, CUSOLVER_EIG_MODE_VECTOR, 1, mr, nc_, nullptr, mr, nullptr,
                                                      nullptr, mr, nullptr, nc_, &lw, so.svdj));
@@ -469,6 +477,18 @@ struct Engine {
   // min(R, Cc), descending) and the full left basis uhf = U^H (mn x R row-major).
   void svd_rowmajor(cudaStream_t st, Solver& so, Pool& pool, cplx* A, int R, int Cc, double* S, cplx* uhf,
                     int* info) {
+    if (svd_method == 3) {
+      // Gram split: G = A A^H (R x R), heevd -> all R left vectors (zeros beyond min(R, Cc))
+      cplx* Gm = pool.c((int64_t)R * R);
+      nc(st, R, R, Cc, A, 0, A, 0, Gm, 0, 1);
+      double* lam = (double*)pool.raw((size_t)R * sizeof(double));
+      cplx* work = pool.c(std::max(lwork_heevd, 1));
+      TN_SOLVER(cusolverDnSetStream(so.h, st));
+      TN_SOLVER(cusolverDnZheevd(so.h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, R, (cuDoubleComplex*)Gm, R,
+                                 lam, (cuDoubleComplex*)work, lwork_heevd, info));
+      eig_to_svd(st, uhf, S, Gm, lam, R);
+      return;
+    }
     const bool tr = Cc >= R;  // column-major view of A is A^T (Cc x R): use it directly when Cc >= R
     cplx* M = A;
     int m = Cc, nn_ = R;
@@ -512,25 +532,26 @@ struct Engine {
   // first-order rotation c_ij = (B_i B_j^H) / (s_j^2 - s_i^2) (one-sided Jacobi
   // across the cut), twice, then Loewdin re-orthonormalisation of the kept rows.
   void refine_kept(cudaStream_t st, Pool& pool, cplx* uhf, const double* S, const cplx* A, int R, int Cc, int mn,
-                   int r) {
+                   int r, int iters) {
     const int nd = mn - r;
     if (nd <= 0) return;
     cplx* B = pool.c((int64_t)mn * Cc);
     cplx* Md = pool.c((int64_t)nd * r);
     cplx* Cm = pool.c((int64_t)nd * r);
-    cplx* old = pool.c((int64_t)r * R);
-    for (int it = 0; it < 2; ++it) {
+    cplx* old = pool.c((int64_t)mn * R);
+    cplx* F = pool.c((int64_t)mn * mn);
+    for (int it = 0; it < iters; ++it) {
       nn(st, mn, Cc, R, uhf, 0, A, 0, B, 0, 1);
       nc(st, nd, r, Cc, B + (int64_t)r * Cc, 0, B, 0, Md, 0, 1);
       kept_rotation(st, Cm, Md, S, nd, r);
       TN_CUDA(cudaMemcpyAsync(old, uhf, (size_t)r * R * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
       cn(st, r, R, nd, Cm, 0, uhf + (int64_t)r * R, 0, uhf, 0, 1, ONE, ONE);      // kept += C^H disc
       nn(st, nd, R, r, Cm, 0, old, 0, uhf + (int64_t)r * R, 0, 1, MONE, ONE);    // disc -= C kept_old
+      // Loewdin re-orthonormalisation of the whole basis: U <- (3/2 - 1/2 U U^H) U
+      nc(st, mn, mn, R, uhf, 0, uhf, 0, F, 0, 1);
+      TN_CUDA(cudaMemcpyAsync(old, uhf, (size_t)mn * R * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+      nn(st, mn, R, mn, F, 0, old, 0, uhf, 0, 1, {-0.5, 0.0}, {1.5, 0.0});
     }
-    cplx* F = pool.c((int64_t)r * r);
-    nc(st, r, r, R, uhf, 0, uhf, 0, F, 0, 1);
-    TN_CUDA(cudaMemcpyAsync(old, uhf, (size_t)r * R * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-    nn(st, r, R, r, F, 0, old, 0, uhf, 0, 1, {-0.5, 0.0}, {1.5, 0.0});
   }
 
   // Runs one side's primal sweep.  store: write snapshots / replay data to the arena.
@@ -590,29 +611,25 @@ struct Engine {
           double* S = store ? at<double>(s.o_S) : (double*)tmp.raw((size_t)s.mn * sizeof(double));
           cplx* uh = store ? at(s.o_uh) : tmp.c((int64_t)s.r * 4 * s.bl);
           cplx* vh = store ? at(s.o_vh) : tmp.c((int64_t)s.r * 4 * s.br);
+          const int nbas = svd_method == 3 ? 4 * s.bl : s.mn;   // rows of the left basis
           cplx* Acp = tmp.c(nth);
           TN_CUDA(cudaMemcpyAsync(Acp, A, nth * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-          cplx* uhf = tmp.c((int64_t)s.mn * 4 * s.bl);
-          svd_rowmajor(st, so, tmp, Acp, 4 * s.bl, 4 * s.br, S, uhf, info + 1);
+          cplx* uhf = tmp.c((int64_t)nbas * 4 * s.bl);
+          double* Sf = (double*)tmp.raw((size_t)nbas * sizeof(double));
+          svd_rowmajor(st, so, tmp, Acp, 4 * s.bl, 4 * s.br, Sf, uhf, info + 1);
+          TN_CUDA(cudaMemcpyAsync(S, Sf, (size_t)s.mn * sizeof(double), cudaMemcpyDeviceToDevice, st));
           double* sc = store ? at<double>(s.o_s) : (double*)tmp.raw(sizeof(double));
-          svd_post(st, S, s.mn, s.r, sc, diag);
-          if (debug) {
-            std::vector<double> hS(s.mn);
-            TN_CUDA(cudaMemcpyAsync(hS.data(), S, s.mn * sizeof(double), cudaMemcpyDeviceToHost, st));
-            TN_CUDA(cudaStreamSynchronize(st));
-            bool bad = false;
-            for (double v : hS) bad |= !std::isfinite(v);
-            const double gap = s.r < s.mn ? (hS[s.r - 1] - hS[s.r]) / hS[0] : 1.0;
-            if (bad || gap < 1e-8 || hS[s.r - 1] < 1e-13 * hS[0])
-              fprintf(stderr, "[tn debug] %s pair site %d k %d lr %d shape %dx%d r %d mn %d: s0 %.3e s[r-1] %.3e s[r] %.3e gap %.3e nan %d\n",
-                      is_top ? "top" : "bot", i, s.k, (int)s.lr, 4 * s.bl, 4 * s.br, s.r, s.mn, hS[0], hS[s.r - 1],
-                      s.r < s.mn ? hS[s.r] : 0.0, gap, (int)bad);
-          }
-          refine_kept(st, tmp, uhf, S, A, 4 * s.bl, 4 * s.br, s.mn, s.r);
+          refine_kept(st, tmp, uhf, Sf, A, 4 * s.bl, 4 * s.br, nbas, s.r, svd_method == 3 ? 3 : 2);
           TN_CUDA(cudaMemcpyAsync(uh, uhf, (size_t)s.r * 4 * s.bl * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
           // Y = U_r^H A (= S_r W_r^H up to a kept-space rotation); LQ gives W_r^H
           cplx* Y = tmp.c((int64_t)s.r * 4 * s.br);
           nn(st, s.r, 4 * s.br, 4 * s.bl, uh, 0, A, 0, Y, 0, 1);
+          {  // frozen s = ||A|| / ||U_r^H A|| and diagnostics
+            double* nrm = (double*)tmp.raw(2 * sizeof(double));
+            tangent_dot(st, nth, 1, A, A, nrm);
+            tangent_dot(st, (int64_t)s.r * 4 * s.br, 1, Y, Y, nrm + 1);
+            s_from_norms(st, nrm, S, s.mn, s.r, sc, diag);
+          }
           cplx* Lq = tmp.c((int64_t)s.r * s.r);
           lq_left(st, so, tmp, Y, s.r, 4 * s.br, s.r, vh, Lq, info);
           cplx* ni = dnew((int64_t)4 * s.bl * s.r, st);

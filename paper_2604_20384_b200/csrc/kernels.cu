@@ -447,6 +447,33 @@ __global__ void kept_rotation_kernel(cplx* __restrict__ Cm, const cplx* __restri
   }
 }
 
+// Gram eigendecomposition -> left singular basis: heevd on the row-major Gram
+// G = A A^H (Hermitian, its column-major view is conj(G)) returns W with
+// conj(G) = W diag(lam) W^H ascending, so U = conj(W) and U^H rows are the
+// columns of W in descending order: uhf[j][a] = Wbuf[(R-1-j) R + a];
+// S[j] = sqrt(max(lam[R-1-j], 0)).
+__global__ void eig_to_svd_kernel(cplx* __restrict__ uhf, double* __restrict__ S, const cplx* __restrict__ W,
+                                  const double* __restrict__ lam, int R) {
+  const int64_t n = (int64_t)R * R;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(idx / R), a = (int)(idx % R);
+    uhf[idx] = W[(int64_t)(R - 1 - j) * R + a];
+    if (a == 0) S[j] = sqrt(fmax(lam[R - 1 - j], 0.0));
+  }
+}
+
+// s = sqrt(nA / nY) (frozen renormalisation) and diagnostics from the exact norms.
+__global__ void s_from_norms_kernel(const double* __restrict__ nrm, const double* __restrict__ S, int mn, int r,
+                                    double* s_out, double* diag) {
+  const double s = sqrt(nrm[0] / nrm[1]);
+  s_out[0] = s;
+  if (diag) {
+    diag[0] = fmax(diag[0], 1.0 - nrm[1] / nrm[0]);
+    if (r < mn) diag[1] = fmin(diag[1], (S[r - 1] - S[r]) / S[0]);
+    diag[2] = fmax(diag[2], fabs(log10(s)));
+  }
+}
+
 __global__ void conj_copy_kernel(cplx* __restrict__ dst, const cplx* __restrict__ src, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = cconj(src[i]);
@@ -598,6 +625,20 @@ void kept_rotation(cudaStream_t st, cplx* Cm, const cplx* M, const double* S, in
   const int64_t n = (int64_t)nd * r;
   if (!n) return;
   kept_rotation_kernel<<<nblocks(n), TPB, 0, st>>>(Cm, M, S, nd, r);
+  TN_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+void eig_to_svd(cudaStream_t st, cplx* uhf, double* S, const cplx* W, const double* lam, int R) {
+  const int64_t n = (int64_t)R * R;
+  if (!n) return;
+  eig_to_svd_kernel<<<nblocks(n), TPB, 0, st>>>(uhf, S, W, lam, R);
+  TN_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+void s_from_norms(cudaStream_t st, const double* nrm, const double* S, int mn, int r, double* s_out, double* diag) {
+  s_from_norms_kernel<<<1, 1, 0, st>>>(nrm, S, mn, r, s_out, diag);
   TN_CUDA(cudaGetLastError());
   count_launch();
 }

@@ -43,6 +43,10 @@ void combine_diag(cudaStream_t st, double* out, const double* d);
 // the first-order rotation that makes the kept rows of B = U^H A orthogonal to
 // the discarded ones (one-sided Jacobi step across the cut).
 void kept_rotation(cudaStream_t st, cplx* Cm, const cplx* M, const double* S, int nd, int r);
+// heevd output (column-major W, ascending lam) -> uhf = U^H rows (descending), S = sqrt(lam)
+void eig_to_svd(cudaStream_t st, cplx* uhf, double* S, const cplx* W, const double* lam, int R);
+// s = sqrt(nrm[0]/nrm[1]) into s_out; diag as in svd_post
+void s_from_norms(cudaStream_t st, const double* nrm, const double* S, int mn, int r, double* s_out, double* diag);
 // dst = conj(src), n elements
 void conj_copy(cudaStream_t st, cplx* dst, const cplx* src, int64_t n);
 // out_k = polar(G_k + alpha xi_k) (unitary retraction); status[0] = 1 on a singular iterate
