@@ -140,6 +140,7 @@ struct Engine {
   int svd_method = 3;  // 0 gesvdj, 1 Xgesvdp, 2 Xgesvd, 3 Gram heevd (default)
   int lwork_heevd = 0;
   bool debug = false;
+  std::atomic<int> n_fallback{0};
   size_t svd_dws = 0, svd_hws = 0;
   int lwork_geqrf = 0, lwork_ungqr = 0;
   cudaStream_t st2 = nullptr;
@@ -388,7 +389,13 @@ struct Engine {
                                                     nullptr, 4 * s.bl, nullptr, &lw));
               lwork_heevd = std::max(lwork_heevd, lw);
             }
-            if (svd_method == 3) {
+            {  // Jacobi workspace always (fallback of the Gram split)
+              int lw = 0;
+              TN_SOLVER(cusolverDnZgesvdj_bufferSize(so.h, CUSOLVER_EIG_MODE_VECTOR, 1, mr, nc_, nullptr, mr, nullptr,
+                                                     nullptr, mr, nullptr, nc_, &lw, so.svdj));
+              dws = std::max(dws, (size_t)lw * sizeof(cplx));
+            }
+            if (svd_method == 3 || svd_method == 0) {
             } else if (svd_method == 0) {
               int lw = 0;
               TN_SOLVER(cusolverDnZgesvdj_bufferSize(so.h, CUSOLVER_EIG_MODE_VECTOR, 1, mr, nc_, nullptr, mr, nullptr,
@@ -476,8 +483,8 @@ struct Engine {
   // SVD of a row-major (R x Cc) matrix A (destroyed): singular values S (mn =
   // min(R, Cc), descending) and the full left basis uhf = U^H (mn x R row-major).
   void svd_rowmajor(cudaStream_t st, Solver& so, Pool& pool, cplx* A, int R, int Cc, double* S, cplx* uhf,
-                    int* info) {
-    if (svd_method == 3) {
+                    int* info, int method) {
+    if (method == 3) {
       // Gram split: G = A A^H (R x R), heevd -> all R left vectors (zeros beyond min(R, Cc))
       cplx* Gm = pool.c((int64_t)R * R);
       nc(st, R, R, Cc, A, 0, A, 0, Gm, 0, 1);
@@ -503,11 +510,11 @@ struct Engine {
     cplx* Vp = pool.c((int64_t)nn_ * mn);
     void* dws = pool.raw(svd_dws + 64);
     TN_SOLVER(cusolverDnSetStream(so.h, st));
-    if (svd_method == 0) {
+    if (method == 0) {
       TN_SOLVER(cusolverDnZgesvdj(so.h, CUSOLVER_EIG_MODE_VECTOR, 1, m, nn_, (cuDoubleComplex*)M, m, S,
                                   (cuDoubleComplex*)Up, m, (cuDoubleComplex*)Vp, nn_, (cuDoubleComplex*)dws,
                                   (int)(svd_dws / sizeof(cplx)), info, so.svdj));
-    } else if (svd_method == 1) {
+    } else if (method == 1) {
       double herr = 0;
       TN_SOLVER(cusolverDnXgesvdp(so.h, so.prm, CUSOLVER_EIG_MODE_VECTOR, 1, m, nn_, CUDA_C_64F, M, m, CUDA_R_64F, S,
                                   CUDA_C_64F, Up, m, CUDA_C_64F, Vp, nn_, CUDA_C_64F, dws, svd_dws,
@@ -611,15 +618,33 @@ struct Engine {
           double* S = store ? at<double>(s.o_S) : (double*)tmp.raw((size_t)s.mn * sizeof(double));
           cplx* uh = store ? at(s.o_uh) : tmp.c((int64_t)s.r * 4 * s.bl);
           cplx* vh = store ? at(s.o_vh) : tmp.c((int64_t)s.r * 4 * s.br);
-          const int nbas = svd_method == 3 ? 4 * s.bl : s.mn;   // rows of the left basis
+          // Split: Gram heevd (fast) when the cut lies where it resolves the
+          // spectrum (smallest kept sigma >= 1e-6 sigma_1 and a boundary gap in
+          // sigma^2 >= 1e-12 sigma_1^2), else one-sided Jacobi (relative accuracy).
+          int method = svd_method;
+          int nbas = method == 3 ? 4 * s.bl : s.mn;
           cplx* Acp = tmp.c(nth);
           TN_CUDA(cudaMemcpyAsync(Acp, A, nth * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-          cplx* uhf = tmp.c((int64_t)nbas * 4 * s.bl);
-          double* Sf = (double*)tmp.raw((size_t)nbas * sizeof(double));
-          svd_rowmajor(st, so, tmp, Acp, 4 * s.bl, 4 * s.br, Sf, uhf, info + 1);
+          cplx* uhf = tmp.c((int64_t)4 * s.bl * 4 * s.bl);
+          double* Sf = (double*)tmp.raw((size_t)4 * s.bl * sizeof(double));
+          svd_rowmajor(st, so, tmp, Acp, 4 * s.bl, 4 * s.br, Sf, uhf, info + 1, method);
+          if (method == 3 && s.r < s.mn) {
+            double hs[2] = {0, 0}, h0 = 0;
+            TN_CUDA(cudaMemcpyAsync(&h0, Sf, sizeof(double), cudaMemcpyDeviceToHost, st));
+            TN_CUDA(cudaMemcpyAsync(hs, Sf + s.r - 1, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+            TN_CUDA(cudaStreamSynchronize(st));
+            const bool resolved = hs[0] >= 1e-6 * h0 && (hs[0] * hs[0] - hs[1] * hs[1]) >= 1e-12 * h0 * h0;
+            if (!resolved) {
+              method = 0;
+              nbas = s.mn;
+              TN_CUDA(cudaMemcpyAsync(Acp, A, nth * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+              svd_rowmajor(st, so, tmp, Acp, 4 * s.bl, 4 * s.br, Sf, uhf, info + 1, method);
+              ++n_fallback;
+            }
+          }
           TN_CUDA(cudaMemcpyAsync(S, Sf, (size_t)s.mn * sizeof(double), cudaMemcpyDeviceToDevice, st));
           double* sc = store ? at<double>(s.o_s) : (double*)tmp.raw(sizeof(double));
-          refine_kept(st, tmp, uhf, Sf, A, 4 * s.bl, 4 * s.br, nbas, s.r, svd_method == 3 ? 3 : 2);
+          refine_kept(st, tmp, uhf, Sf, A, 4 * s.bl, 4 * s.br, nbas, s.r, method == 3 ? 3 : 2);
           TN_CUDA(cudaMemcpyAsync(uh, uhf, (size_t)s.r * 4 * s.bl * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
           // Y = U_r^H A (= S_r W_r^H up to a kept-space rotation); LQ gives W_r^H
           cplx* Y = tmp.c((int64_t)s.r * 4 * s.br);
@@ -701,6 +726,7 @@ struct Engine {
   void environments(cudaStream_t st, const cplx* gates, double* scalars, cplx* grad_R) {
     TN_CUDA(cudaSetDevice(device));
     primal_valid = false;
+    n_fallback = 0;
     const double wc0 = work_counter.load();
     Pool pool(st);
     TN_CUDA(cudaMemcpyAsync(at(o_gates), gates, (size_t)K * 16 * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
@@ -764,7 +790,8 @@ struct Engine {
         throw NumericError("non-finite primal scalar: f=" + std::to_string(sc[0]) + " T=(" + std::to_string(sc[1]) +
                            "," + std::to_string(sc[2]) + ") discarded=" + std::to_string(sc[3]) +
                            " gap=" + std::to_string(sc[4]) + " log10s=" + std::to_string(sc[5]));
-    sc[6] = sc[7] = 0;
+    sc[6] = (double)n_fallback.load();
+    sc[7] = 0;
     TN_CUDA(cudaMemcpyAsync(scalars, sc, 8 * sizeof(double), cudaMemcpyHostToDevice, st));
     TN_CUDA(cudaMemcpyAsync(at<double>(o_scal), sc, 8 * sizeof(double), cudaMemcpyHostToDevice, st));
     TN_CUDA(cudaStreamSynchronize(st));
