@@ -628,7 +628,7 @@ struct Engine {
           cplx* uhf = tmp.c((int64_t)4 * s.bl * 4 * s.bl);
           double* Sf = (double*)tmp.raw((size_t)4 * s.bl * sizeof(double));
           svd_rowmajor(st, so, tmp, Acp, 4 * s.bl, 4 * s.br, Sf, uhf, info + 1, method);
-          if (method == 3 && s.r < s.mn) {
+          if (method == 3 && s.r < 4 * s.bl) {  // something (discarded or null) is excluded
             double hs[2] = {0, 0}, h0 = 0;
             TN_CUDA(cudaMemcpyAsync(&h0, Sf, sizeof(double), cudaMemcpyDeviceToHost, st));
             TN_CUDA(cudaMemcpyAsync(hs, Sf + s.r - 1, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
