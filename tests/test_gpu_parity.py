@@ -3,6 +3,8 @@
 Bar (BASELINE.json north_star): relative error <= 1e-10 in complex128 on the
 same seeded inputs (X18: rel = ||x_gpu - x_ref|| / ||x_ref|| per output; for
 Hess_R the max over directions)."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -83,3 +85,56 @@ def test_apply_is_linear_and_batch_independent():
     assert rel(g["HR"][2], a * g["HR"][0] + b * g["HR"][1]) < 1e-12
     g1 = gpu_outputs(cfg, ref, G, Vc[1:2])
     assert rel(g1["HR"][0], g["HR"][1]) < 1e-13
+
+
+def _layer_sites(cfg):
+    from oracle.common import layers
+    return layers(cfg.n, cfg.depth, cfg.first_offset)
+
+
+@pytest.mark.parametrize("cid", [3])
+def test_full_size_properties(cid):
+    """Properties that hold at any size, at the bench's full config and launch
+    configuration: per-layer Euler identity of E (X9), grad_R and Hess_R in the
+    tangent space, Hess_R real-linear in V, results independent of the
+    direction's position in the batch (bitwise)."""
+    cfg = C.CONFIGS[cid]
+    from paper_2604_20384_b200.api import HVPEngine, riemannian_project
+    from tn_inputs.reference import reference_mpo as _ref
+    dev = torch.device("cuda")
+    ref = C.reference_mpo(cfg, device=dev)
+    K = C.num_gates(cfg.n, cfg.depth)
+    G = C.haar_gates(cfg.cid, K)
+    V = C.tangent_directions(cfg.cid, G, cfg.batch)
+    eng = HVPEngine(cfg.n, cfg.depth, cfg.chi, ref, max_batch=cfg.batch)
+    Gt = torch.tensor(G, device=dev)
+    sc, gR = eng.environments(Gt)
+    E = eng.gradient_T().cpu().numpy()
+    for ly in _layer_sites(cfg):
+        vals = np.array([np.sum(G[k] * E[k]) for k, _ in ly])
+        assert np.abs(vals - vals[0]).max() <= 1e-12 * np.abs(vals[0])
+    assert rel(riemannian_project(Gt, gR).cpu().numpy(), gR.cpu().numpy()) < 1e-13
+    Vt = torch.tensor(V, device=dev)
+    H = eng.apply(Vt).cpu().numpy()
+    Hp = riemannian_project(Gt, torch.tensor(H, device=dev)).cpu().numpy()
+    assert rel(Hp, H) < 1e-13
+    comb = torch.tensor(np.stack([V[0] + 2.5 * V[1], V[1]]), device=dev)
+    Hc = eng.apply(comb).cpu().numpy()
+    assert rel(Hc[0], H[0] + 2.5 * H[1]) < 1e-11
+    assert np.array_equal(Hc[1], H[1])                  # same direction, other batch position
+    eng.close()
+
+
+@pytest.mark.skipif(os.environ.get("TN_FULL_PARITY") != "1", reason="~8 min of oracle CPU time; TN_FULL_PARITY=1")
+def test_parity_config3_sampled():
+    cfg = C.CONFIGS[3]
+    dev = torch.device("cuda")
+    ref = C.reference_mpo(cfg, device=dev)
+    K = C.num_gates(cfg.n, cfg.depth)
+    G = C.haar_gates(cfg.cid, K)
+    V = C.tangent_directions(cfg.cid, G, 1)
+    o = oracle_outputs(cfg, ref, G, V)
+    g = gpu_outputs(cfg, ref, G, V, max_batch=1)
+    assert abs(g["f"] - o["f"]) <= TOL * abs(o["f"])
+    assert rel(g["grad_R"], o["grad_R"]) < TOL
+    assert rel(g["HR"][0], o["HR"][0]) < TOL
