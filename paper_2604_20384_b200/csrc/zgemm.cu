@@ -11,6 +11,8 @@
 // bank-conflict free.  op(A), op(B) in {N, T, C}; conjugation is folded into
 // the fragment sign.  Row-major everywhere; batch strides may be 0 (shared).
 #include <atomic>
+#include <cstdlib>
+#include <string>
 #include <mutex>
 #include <vector>
 
@@ -172,11 +174,151 @@ __global__ void __launch_bounds__(NT, 2) zgemm_kernel(Params p) {
   }
 }
 
+
+// 3M (Gauss) variant: (a + ib)(c + id) = ac - bd + i[(a + b)(c + d) - ac - bd],
+// three real DMMAs per complex k-step: P1 += Ar Br, P2 += Ai Bi,
+// P3 += (Ar + Ai)(Br + Bi); C_re = P1 - P2, C_im = P3 - P1 - P2.  CTA 64x64,
+// 8 warps (4 x 2), warp tile 16 x 32 (2 x 4 DMMA tiles), NSTAGE-deep cp.async
+// pipeline, one CTA per SM (<= 255 registers).
+constexpr int NT3 = 256, NSTAGE3 = 4;
+constexpr int SMEM3_BYTES = NSTAGE3 * STAGE * (int)sizeof(cplx);
+
+template <char OPA, char OPB>
+__global__ void __launch_bounds__(NT3, 1) zgemm3m_kernel(Params p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx* smem = reinterpret_cast<cplx*>(smem_raw);
+  const int64_t bz = blockIdx.z;
+  const cplx* __restrict__ A = p.A + bz * p.sA;
+  const cplx* __restrict__ B = p.B + bz * p.sB;
+  cplx* __restrict__ C = p.C + bz * p.sC;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;  // 4 x 2 warps: warp rows of 16, columns of 32
+  const int g = lane >> 2, q = lane & 3;
+
+  auto load_stage = [&](int stage, int k0) {
+    cplx* sA = smem + stage * STAGE;
+    cplx* sB = sA + TILE;
+#pragma unroll
+    for (int j = 0; j < (BM * BK) / NT3; ++j) {
+      const int e = tid + j * NT3;
+      if (OPA == 'N') {
+        const int m = e / BK, k = e % BK, gm = m0 + m, gk = k0 + k;
+        const bool ok = gm < p.M && gk < p.K;
+        cp_async16(sA + m * LDN + k, ok ? (const void*)(A + (int64_t)gm * p.lda + gk) : (const void*)A, ok);
+      } else {
+        const int k = e / BM, m = e % BM, gm = m0 + m, gk = k0 + k;
+        const bool ok = gm < p.M && gk < p.K;
+        cp_async16(sA + k * LDT + m, ok ? (const void*)(A + (int64_t)gk * p.lda + gm) : (const void*)A, ok);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < (BN * BK) / NT3; ++j) {
+      const int e = tid + j * NT3;
+      if (OPB == 'N') {
+        const int k = e / BN, n = e % BN, gn = n0 + n, gk = k0 + k;
+        const bool ok = gn < p.N && gk < p.K;
+        cp_async16(sB + k * LDT + n, ok ? (const void*)(B + (int64_t)gk * p.ldb + gn) : (const void*)B, ok);
+      } else {
+        const int n = e / BK, k = e % BK, gn = n0 + n, gk = k0 + k;
+        const bool ok = gn < p.N && gk < p.K;
+        cp_async16(sB + n * LDN + k, ok ? (const void*)(B + (int64_t)gn * p.ldb + gk) : (const void*)B, ok);
+      }
+    }
+  };
+
+  double p1[2][4][2], p2[2][4][2], p3[2][4][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int t = 0; t < 2; ++t) p1[i][j][t] = p2[i][j][t] = p3[i][j][t] = 0.0;
+
+  const int nk = (p.K + BK - 1) / BK;
+#pragma unroll
+  for (int s = 0; s < NSTAGE3 - 1; ++s) {
+    if (s < nk) load_stage(s, s * BK);
+    cp_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_wait<NSTAGE3 - 2>();
+    __syncthreads();
+    {
+      const int nx = kt + NSTAGE3 - 1;
+      if (nx < nk) load_stage(nx % NSTAGE3, nx * BK);
+      cp_commit();
+    }
+    const cplx* sA = smem + (kt % NSTAGE3) * STAGE;
+    const cplx* sB = sA + TILE;
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      double ar[2], ai[2], as[2], br[4], bi[4], bs[4];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) {
+        const int row = wm * 16 + mi * 8 + g, col = kk * 4 + q;
+        const cplx a = (OPA == 'N') ? sA[row * LDN + col] : sA[col * LDT + row];
+        ar[mi] = a.x;
+        ai[mi] = (OPA == 'C') ? -a.y : a.y;
+        as[mi] = ar[mi] + ai[mi];
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const int krow = kk * 4 + q, ncol = wn * 32 + ni * 8 + g;
+        const cplx b = (OPB == 'N') ? sB[krow * LDT + ncol] : sB[ncol * LDN + krow];
+        br[ni] = b.x;
+        bi[ni] = (OPB == 'C') ? -b.y : b.y;
+        bs[ni] = br[ni] + bi[ni];
+      }
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+          dmma(p1[mi][ni], ar[mi], br[ni]);
+          dmma(p2[mi][ni], ai[mi], bi[ni]);
+          dmma(p3[mi][ni], as[mi], bs[ni]);
+        }
+    }
+  }
+  cp_wait<0>();
+
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi) {
+    const int row = m0 + wm * 16 + mi * 8 + g;
+    if (row >= p.M) continue;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int col = n0 + wn * 32 + ni * 8 + 2 * q + j;
+        if (col < p.N) {
+          const double re = p1[mi][ni][j] - p2[mi][ni][j];
+          const double im = p3[mi][ni][j] - p1[mi][ni][j] - p2[mi][ni][j];
+          cplx v = cmul(p.alpha, make_double2(re, im));
+          cplx* dst = C + (int64_t)row * p.ldc + col;
+          if (p.has_beta) v = cadd(v, cmul(p.beta, *dst));
+          *dst = v;
+        }
+      }
+    }
+  }
+}
+
+int g_variant = -1;  // 0 = 4M (4 warps, 2 stages), 1 = 3M (8 warps, 4 stages)
+int variant() {
+  if (g_variant < 0) {
+    const char* v = std::getenv("TN_GEMM");
+    g_variant = (v && std::string(v) == "4m") ? 0 : 1;
+  }
+  return g_variant;
+}
+
 template <char OPA, char OPB>
 void launch(const Params& p, int batch, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     TN_CUDA(cudaFuncSetAttribute(zgemm_kernel<OPA, OPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    TN_CUDA(cudaFuncSetAttribute(zgemm3m_kernel<OPA, OPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM3_BYTES));
     attr = true;
   }
   dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, batch);
@@ -186,7 +328,10 @@ void launch(const Params& p, int batch, cudaStream_t st) {
     TN_CUDA(cudaEventCreate(&e1));
     TN_CUDA(cudaEventRecord(e0, st));
   }
-  zgemm_kernel<OPA, OPB><<<grid, NT, SMEM_BYTES, st>>>(p);
+  if (variant() == 1)
+    zgemm3m_kernel<OPA, OPB><<<grid, NT3, SMEM3_BYTES, st>>>(p);
+  else
+    zgemm_kernel<OPA, OPB><<<grid, NT, SMEM_BYTES, st>>>(p);
   TN_CUDA(cudaGetLastError());
   count_launch();
   if (g_prof.on) {
