@@ -10,7 +10,9 @@
 // strides padded so every fragment load (one LDS.128 = one complex) is
 // bank-conflict free.  op(A), op(B) in {N, T, C}; conjugation is folded into
 // the fragment sign.  Row-major everywhere; batch strides may be 0 (shared).
+#include <array>
 #include <atomic>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 #include <mutex>
@@ -26,6 +28,7 @@ struct Prof {
   bool on = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
   std::vector<double> cm;
+  std::vector<std::array<int, 6>> shape;  // M, N, K, batch, opa, opb
 };
 Prof g_prof;
 std::mutex g_prof_mu;
@@ -339,6 +342,7 @@ void launch(const Params& p, int batch, cudaStream_t st) {
     std::lock_guard<std::mutex> lk(g_prof_mu);
     g_prof.ev.push_back({e0, e1});
     g_prof.cm.push_back((double)p.M * p.N * p.K * batch);
+    g_prof.shape.push_back({p.M, p.N, p.K, batch, (int)OPA, (int)OPB});
   }
 }
 
@@ -366,6 +370,7 @@ void gemm_profile_begin() {
   }
   g_prof.ev.clear();
   g_prof.cm.clear();
+  g_prof.shape.clear();
   g_prof.on = true;
 }
 
@@ -373,17 +378,25 @@ void gemm_profile_end(double* ms, double* cmac) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
   g_prof.on = false;
   double t = 0, c = 0;
+  FILE* log = nullptr;
+  if (const char* path = std::getenv("TN_GEMM_LOG")) log = std::fopen(path, "w");
   for (size_t i = 0; i < g_prof.ev.size(); ++i) {
     TN_CUDA(cudaEventSynchronize(g_prof.ev[i].second));
     float m = 0;
     TN_CUDA(cudaEventElapsedTime(&m, g_prof.ev[i].first, g_prof.ev[i].second));
     t += m;
     c += g_prof.cm[i];
+    if (log) {
+      const auto& sh = g_prof.shape[i];
+      std::fprintf(log, "%d %d %d %d %c %c %.6f\n", sh[0], sh[1], sh[2], sh[3], (char)sh[4], (char)sh[5], m);
+    }
     cudaEventDestroy(g_prof.ev[i].first);
     cudaEventDestroy(g_prof.ev[i].second);
   }
+  if (log) std::fclose(log);
   g_prof.ev.clear();
   g_prof.cm.clear();
+  g_prof.shape.clear();
   *ms = t;
   *cmac = c;
 }
