@@ -541,12 +541,11 @@ struct Engine {
   void refine_kept(cudaStream_t st, Pool& pool, cplx* uhf, const double* S, const cplx* A, int R, int Cc, int mn,
                    int r, int iters) {
     const int nd = mn - r;
-    if (nd <= 0) return;
+    if (nd <= 0 || iters <= 0) return;
     cplx* B = pool.c((int64_t)mn * Cc);
     cplx* Md = pool.c((int64_t)nd * r);
     cplx* Cm = pool.c((int64_t)nd * r);
     cplx* old = pool.c((int64_t)mn * R);
-    cplx* F = pool.c((int64_t)mn * mn);
     for (int it = 0; it < iters; ++it) {
       nn(st, mn, Cc, R, uhf, 0, A, 0, B, 0, 1);
       nc(st, nd, r, Cc, B + (int64_t)r * Cc, 0, B, 0, Md, 0, 1);
@@ -554,11 +553,12 @@ struct Engine {
       TN_CUDA(cudaMemcpyAsync(old, uhf, (size_t)r * R * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
       cn(st, r, R, nd, Cm, 0, uhf + (int64_t)r * R, 0, uhf, 0, 1, ONE, ONE);      // kept += C^H disc
       nn(st, nd, R, r, Cm, 0, old, 0, uhf + (int64_t)r * R, 0, 1, MONE, ONE);    // disc -= C kept_old
-      // Loewdin re-orthonormalisation of the whole basis: U <- (3/2 - 1/2 U U^H) U
-      nc(st, mn, mn, R, uhf, 0, uhf, 0, F, 0, 1);
-      TN_CUDA(cudaMemcpyAsync(old, uhf, (size_t)mn * R * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-      nn(st, mn, R, mn, F, 0, old, 0, uhf, 0, 1, {-0.5, 0.0}, {1.5, 0.0});
     }
+    // Loewdin re-orthonormalisation of the whole basis: U <- (3/2 - 1/2 U U^H) U
+    cplx* F = pool.c((int64_t)mn * mn);
+    nc(st, mn, mn, R, uhf, 0, uhf, 0, F, 0, 1);
+    TN_CUDA(cudaMemcpyAsync(old, uhf, (size_t)mn * R * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+    nn(st, mn, R, mn, F, 0, old, 0, uhf, 0, 1, {-0.5, 0.0}, {1.5, 0.0});
   }
 
   // Runs one side's primal sweep.  store: write snapshots / replay data to the arena.
@@ -628,23 +628,32 @@ struct Engine {
           cplx* uhf = tmp.c((int64_t)4 * s.bl * 4 * s.bl);
           double* Sf = (double*)tmp.raw((size_t)4 * s.bl * sizeof(double));
           svd_rowmajor(st, so, tmp, Acp, 4 * s.bl, 4 * s.br, Sf, uhf, info + 1, method);
+          int iters = method == 3 ? 0 : 2;
           if (method == 3 && s.r < 4 * s.bl) {  // something (discarded or null) is excluded
+            // kept/excluded mixing of the Gram basis ~ eps sigma_1^2 / (sigma_{r-1}^2 - sigma_r^2)
+            // (sigma_r = 0 for a null direction); first-order refinement converges
+            // quadratically from delta <~ 1e-2, else one-sided Jacobi.
             double hs[2] = {0, 0}, h0 = 0;
             TN_CUDA(cudaMemcpyAsync(&h0, Sf, sizeof(double), cudaMemcpyDeviceToHost, st));
             TN_CUDA(cudaMemcpyAsync(hs, Sf + s.r - 1, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
             TN_CUDA(cudaStreamSynchronize(st));
-            const bool resolved = hs[0] >= 1e-6 * h0 && (hs[0] * hs[0] - hs[1] * hs[1]) >= 1e-12 * h0 * h0;
-            if (!resolved) {
+            const double low = s.r < s.mn ? hs[1] : 0.0;
+            const double gap2 = (hs[0] * hs[0] - low * low) / (h0 * h0);
+            const double delta = gap2 > 0 ? 2.2e-16 / gap2 : 1.0;
+            if (delta > 1e-2) {
               method = 0;
               nbas = s.mn;
+              iters = 2;
               TN_CUDA(cudaMemcpyAsync(Acp, A, nth * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
               svd_rowmajor(st, so, tmp, Acp, 4 * s.bl, 4 * s.br, Sf, uhf, info + 1, method);
               ++n_fallback;
+            } else {
+              iters = delta < 1e-8 ? 1 : delta < 1e-4 ? 2 : 4;
             }
           }
           TN_CUDA(cudaMemcpyAsync(S, Sf, (size_t)s.mn * sizeof(double), cudaMemcpyDeviceToDevice, st));
           double* sc = store ? at<double>(s.o_s) : (double*)tmp.raw(sizeof(double));
-          refine_kept(st, tmp, uhf, Sf, A, 4 * s.bl, 4 * s.br, nbas, s.r, method == 3 ? 3 : 2);
+          refine_kept(st, tmp, uhf, Sf, A, 4 * s.bl, 4 * s.br, nbas, s.r, iters);
           TN_CUDA(cudaMemcpyAsync(uh, uhf, (size_t)s.r * 4 * s.bl * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
           // Y = U_r^H A (= S_r W_r^H up to a kept-space rotation); LQ gives W_r^H
           cplx* Y = tmp.c((int64_t)s.r * 4 * s.br);

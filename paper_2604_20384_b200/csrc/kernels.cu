@@ -436,12 +436,13 @@ __global__ void kept_rotation_kernel(cplx* __restrict__ Cm, const cplx* __restri
     const double sj = S[j], si = S[r + i];
     const double den = (sj - si) * (sj + si);
     // Only a kept value above the noise floor defines a direction worth
-    // refining; a first-order rotation larger than 1e-3 is outside the
-    // linearised regime (then the SVD's own vectors are kept).
+    // refining; a first-order rotation larger than 5e-2 is outside the
+    // linearised regime (then the SVD's own vectors are kept); the host
+    // only chooses this path when the expected mixing is <~ 1e-2.
     cplx c = make_double2(0.0, 0.0);
     if (sj > 1e-11 * S[0] && den > 0.0) {
       c = cscale(M[idx], 1.0 / den);
-      if (!(fabs(c.x) + fabs(c.y) < 1e-3)) c = make_double2(0.0, 0.0);
+      if (!(fabs(c.x) + fabs(c.y) < 5e-2)) c = make_double2(0.0, 0.0);
     }
     Cm[idx] = c;
   }
