@@ -68,8 +68,8 @@ __global__ void scale_kernel(cplx* __restrict__ y, const double* __restrict__ s,
 // Gate-environment extraction:
 // E[b][(o1 o2),(c1 c2)] += alpha * sum_{t,i1,i2,u} conj(top[t,o1 i1,o2 i2,u]) z[b][t,c1 i1,c2 i2,u]
 // top: [T][4][4][U] (shared, stride stop per batch, 0 allowed); z: [batch][T][4][4][U].
-__global__ void extract_env_kernel(cplx* __restrict__ E, int64_t sE, const cplx* __restrict__ top, int64_t stop,
-                                   const cplx* __restrict__ z, int64_t sz, int T, int U, cplx alpha) {
+__global__ void extract_env_kernel(double* __restrict__ part, const cplx* __restrict__ top, int64_t stop,
+                                   const cplx* __restrict__ z, int64_t sz, int T, int U) {
   const int b = blockIdx.y;
   const cplx* tp = top + b * stop;
   const cplx* zb = z + b * sz;
@@ -116,12 +116,22 @@ __global__ void extract_env_kernel(cplx* __restrict__ E, int64_t sE, const cplx*
     const int i = threadIdx.x >> 1, c = threadIdx.x & 1;
     double v = 0.0;
     for (int j = 0; j < TPB / 32; ++j) v += red[i][c][j];
-    // complex scale and accumulate with atomics (several blocks per batch entry)
-    const double other = __shfl_xor_sync(0xffffffffu, v, 1);
-    const double re = (c == 0) ? v : other, im = (c == 0) ? other : v;
-    const cplx s = cmul(alpha, make_double2(re, im));
-    atomicAdd(&reinterpret_cast<double*>(E + b * sE + i)[c], c == 0 ? s.x : s.y);
+    // block partial -> scratch[b][block][i][c]; summed in block order by extract_finish
+    part[(((int64_t)b * gridDim.x + blockIdx.x) * 16 + i) * 2 + c] = v;
   }
+}
+
+// E[b] += alpha * sum over blocks (fixed order: deterministic results)
+__global__ void extract_finish_kernel(cplx* __restrict__ E, int64_t sE, const double* __restrict__ part, int nblk,
+                                      cplx alpha) {
+  const int b = blockIdx.x, i = threadIdx.x;
+  if (i >= 16) return;
+  double re = 0, im = 0;
+  for (int j = 0; j < nblk; ++j) {
+    re += part[(((int64_t)b * nblk + j) * 16 + i) * 2];
+    im += part[(((int64_t)b * nblk + j) * 16 + i) * 2 + 1];
+  }
+  E[b * sE + i] = cadd(E[b * sE + i], cmul(alpha, make_double2(re, im)));
 }
 
 // P_G(Z) = 1/2 (Z - G Z^dag G), one thread per (batch, gate).
@@ -292,10 +302,16 @@ void extract_env(cudaStream_t st, cplx* E, int64_t sE, const cplx* top, int64_t 
   int bx = (int)((pairs + TPB * 8 - 1) / (TPB * 8));
   if (bx < 1) bx = 1;
   if (bx > 64) bx = 64;
+  double* part = nullptr;
+  TN_CUDA(cudaMallocAsync((void**)&part, sizeof(double) * 32 * bx * (size_t)batch, st));
   dim3 grid(bx, batch);
-  extract_env_kernel<<<grid, TPB, 0, st>>>(E, sE, top, stop, z, sz, T, U, alpha);
+  extract_env_kernel<<<grid, TPB, 0, st>>>(part, top, stop, z, sz, T, U);
   TN_CUDA(cudaGetLastError());
   count_launch();
+  extract_finish_kernel<<<batch, 32, 0, st>>>(E, sE, part, bx, alpha);
+  TN_CUDA(cudaGetLastError());
+  count_launch();
+  TN_CUDA(cudaFreeAsync(part, st));
 }
 
 void project(cudaStream_t st, int K, int batch, const cplx* G, const cplx* in, cplx* out) {
