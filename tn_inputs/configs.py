@@ -84,3 +84,21 @@ def small_case(cid: int, n: int, depth: int, chi: int, batch: int = 2, model: Mo
     m = model or Model("tfim", {"J": 1.0, "h": 0.9, "g": 0.4})
     return Config(cid, f"small-{cid}-n{n}-D{depth}-chi{chi}", n, depth, chi, m, t, steps, order, batch,
                   first_offset)
+
+
+def trotter_init_gates(cfg: Config, problem: int, steps: int | None = None, eps: float = 0.05) -> np.ndarray:
+    """Config-5 starting circuits: the 1st-order Trotter circuit
+    of the config's H with D/2 steps (one A and one B layer per step = the
+    brickwall layout), each gate multiplied by exp(-i eps H_s) with H_s a
+    seeded GUE 4x4 from stream (cfg, "init", problem*K + k)."""
+    from .models import bond_term, expm_herm
+    steps = steps or cfg.depth // 2
+    dt = cfg.t / steps
+    sites = brickwall_sites(cfg.n, cfg.depth, cfg.first_offset)
+    K = len(sites)
+    out = np.empty((K, 4, 4), dtype=np.complex128)
+    for k, s in enumerate(sites):
+        a = rng.complex_normal(rng.stream_key(cfg.cid, "init", problem * K + k), 16).reshape(4, 4)
+        hs = 0.5 * (a + a.conj().T)
+        out[k] = expm_herm(bond_term(cfg.model, cfg.n, s), dt) @ expm_herm(hs, eps)
+    return out
