@@ -139,6 +139,7 @@ struct Engine {
   Solver sol[2];
   int svd_method = 3;  // 0 gesvdj, 1 Xgesvdp, 2 Xgesvd, 3 Gram heevd (default)
   int lwork_heevd = 0;
+  int fallback_method = 2;  // TN_SVD_FALLBACK: gesvd (QR iteration, default) | gesvdj
   bool debug = false;
   std::atomic<int> n_fallback{0};
   size_t svd_dws = 0, svd_hws = 0;
@@ -361,6 +362,7 @@ struct Engine {
     uint64_t thr = UINT64_MAX;
     TN_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     debug = std::getenv("TN_DEBUG") != nullptr;
+    if (const char* f = std::getenv("TN_SVD_FALLBACK")) fallback_method = std::string(f) == "gesvdj" ? 0 : 2;
     if (const char* m = std::getenv("TN_SVD")) {
       const std::string v(m);
       svd_method = v == "gesvdj" ? 0 : v == "gesvd" ? 2 : v == "gesvdp" ? 1 : 3;
@@ -394,6 +396,14 @@ struct Engine {
               TN_SOLVER(cusolverDnZgesvdj_bufferSize(so.h, CUSOLVER_EIG_MODE_VECTOR, 1, mr, nc_, nullptr, mr, nullptr,
                                                      nullptr, mr, nullptr, nc_, &lw, so.svdj));
               dws = std::max(dws, (size_t)lw * sizeof(cplx));
+            }
+            {  // QR-iteration workspace always (fallback of the Gram split)
+              size_t d2 = 0, h2 = 0;
+              TN_SOLVER(cusolverDnXgesvd_bufferSize(so.h, so.prm, 'S', 'S', mr, nc_, CUDA_C_64F, nullptr, mr,
+                                                    CUDA_R_64F, nullptr, CUDA_C_64F, nullptr, mr, CUDA_C_64F, nullptr,
+                                                    nc_, CUDA_C_64F, &d2, &h2));
+              dws = std::max(dws, d2);
+              hws = std::max(hws, h2);
             }
             if (svd_method == 3 || svd_method == 0) {
             } else if (svd_method == 0) {
@@ -641,7 +651,7 @@ struct Engine {
             const double gap2 = (hs[0] * hs[0] - low * low) / (h0 * h0);
             const double delta = gap2 > 0 ? 2.2e-16 / gap2 : 1.0;
             if (delta > 1e-2) {
-              method = 0;
+              method = fallback_method;
               nbas = s.mn;
               iters = 2;
               TN_CUDA(cudaMemcpyAsync(Acp, A, nth * sizeof(cplx), cudaMemcpyDeviceToDevice, st));

@@ -26,7 +26,7 @@ K = C.num_gates(cfg.n, cfg.depth)
 G = C.haar_gates(cfg.cid, K)
 V = C.tangent_directions(cfg.cid, G, a.dirs)
 out = {"config": cfg.name}
-for m in ("eigh", "gesvdj"):
+for m in ("eigh",):
     os.environ["TN_SVD"] = m
     eng = HVPEngine(cfg.n, cfg.depth, cfg.chi, ref, max_batch=a.dirs)
     sc, gR = eng.environments(torch.tensor(G, device=dev))
@@ -47,7 +47,7 @@ if not a.no_hvp:
 out["oracle_s"] = time.time() - t0
 rel = lambda x, y: float(np.linalg.norm(np.ravel(x - y)) / np.linalg.norm(np.ravel(y)))
 res = {"config": cfg.name, "oracle_f": f, "oracle_seconds": out["oracle_s"]}
-for m in ("eigh", "gesvdj"):
+for m in ("eigh",):
     r = {"f_rel": abs(out[m]["f"] - f) / abs(f), "grad_R_rel": rel(out[m]["gR"], gR), "diag": out[m]["diag"]}
     if HR:
         r["hess_R_rel"] = max(rel(out[m]["H"][b], HR[b]) for b in range(a.dirs))
