@@ -141,7 +141,7 @@ struct Engine {
   int lwork_heevd = 0;
   int fallback_method = 2;  // TN_SVD_FALLBACK: gesvd (QR iteration, default) | gesvdj
   bool debug = false;
-  std::atomic<int> n_fallback{0};
+  std::atomic<int> n_fallback{0}, n_deflate{0};
   size_t svd_dws = 0, svd_hws = 0;
   int lwork_geqrf = 0, lwork_ungqr = 0;
   cudaStream_t st2 = nullptr;
@@ -571,6 +571,31 @@ struct Engine {
     nn(st, mn, R, mn, F, 0, old, 0, uhf, 0, 1, {-0.5, 0.0}, {1.5, 0.0});
   }
 
+  // Second Gram level for the low part of the spectrum: rows n_hi.. of uhf
+  // (already split from the high part by refine_kept) span a block whose
+  // singular values are small; A_lo = U_lo^H A, heevd of A_lo A_lo^H resolves
+  // them relative to their own scale.  Rotates those rows and rewrites S.
+  void deflate_low(cudaStream_t st, Solver& so, Pool& pool, cplx* uhf, double* S, const cplx* A, int R, int Cc,
+                   int n_hi, int* info) {
+    const int nl = R - n_hi;
+    if (nl <= 0) return;
+    cplx* lo = uhf + (int64_t)n_hi * R;
+    cplx* Alo = pool.c((int64_t)nl * Cc);
+    nn(st, nl, Cc, R, lo, 0, A, 0, Alo, 0, 1);
+    cplx* G2 = pool.c((int64_t)nl * nl);
+    nc(st, nl, nl, Cc, Alo, 0, Alo, 0, G2, 0, 1);
+    double* lam = (double*)pool.raw((size_t)nl * sizeof(double));
+    cplx* work = pool.c(std::max(lwork_heevd, 1));
+    TN_SOLVER(cusolverDnSetStream(so.h, st));
+    TN_SOLVER(cusolverDnZheevd(so.h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, nl, (cuDoubleComplex*)G2, nl,
+                               lam, (cuDoubleComplex*)work, lwork_heevd, info));
+    cplx* rot = pool.c((int64_t)nl * nl);
+    eig_to_svd(st, rot, S + n_hi, G2, lam, nl);
+    cplx* old = pool.c((int64_t)nl * R);
+    TN_CUDA(cudaMemcpyAsync(old, lo, (size_t)nl * R * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+    nn(st, nl, R, nl, rot, 0, old, 0, lo, 0, 1);
+  }
+
   // Runs one side's primal sweep.  store: write snapshots / replay data to the arena.
   // Returns the final MPS (pool-owned) -- the top side's T_0.
   Mps primal_side(cudaStream_t st, Solver& so, Pool& pool, bool is_top, bool store, int* info, double* diag) {
@@ -640,16 +665,32 @@ struct Engine {
           svd_rowmajor(st, so, tmp, Acp, 4 * s.bl, 4 * s.br, Sf, uhf, info + 1, method);
           int iters = method == 3 ? 0 : 2;
           if (method == 3 && s.r < 4 * s.bl) {  // something (discarded or null) is excluded
-            // kept/excluded mixing of the Gram basis ~ eps sigma_1^2 / (sigma_{r-1}^2 - sigma_r^2)
+            // kept/excluded mixing of a Gram basis ~ eps sigma_top^2 / (sigma_{r-1}^2 - sigma_r^2)
             // (sigma_r = 0 for a null direction); first-order refinement converges
-            // quadratically from delta <~ 1e-2, else one-sided Jacobi.
-            double hs[2] = {0, 0}, h0 = 0;
-            TN_CUDA(cudaMemcpyAsync(&h0, Sf, sizeof(double), cudaMemcpyDeviceToHost, st));
-            TN_CUDA(cudaMemcpyAsync(hs, Sf + s.r - 1, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+            // quadratically from delta <~ 1e-2.  Otherwise a second Gram level on the
+            // low block (resolves relative to its own scale), else QR-iteration SVD.
+            const int R = 4 * s.bl;
+            std::vector<double> hS(R);
+            TN_CUDA(cudaMemcpyAsync(hS.data(), Sf, R * sizeof(double), cudaMemcpyDeviceToHost, st));
             TN_CUDA(cudaStreamSynchronize(st));
-            const double low = s.r < s.mn ? hs[1] : 0.0;
-            const double gap2 = (hs[0] * hs[0] - low * low) / (h0 * h0);
-            const double delta = gap2 > 0 ? 2.2e-16 / gap2 : 1.0;
+            auto mixing = [&](double top) {
+              const double low = s.r < s.mn ? hS[s.r] : 0.0;
+              const double gap2 = (hS[s.r - 1] * hS[s.r - 1] - low * low) / (top * top);
+              return gap2 > 0 ? 2.2e-16 / gap2 : 1.0;
+            };
+            double delta = mixing(hS[0]);
+            if (delta > 1e-2) {
+              int n_hi = 0;
+              while (n_hi < R && hS[n_hi] >= 1e-4 * hS[0]) ++n_hi;
+              if (n_hi > 0 && n_hi < s.r) {
+                refine_kept(st, tmp, uhf, Sf, A, R, 4 * s.br, R, n_hi, 2);
+                deflate_low(st, so, tmp, uhf, Sf, A, R, 4 * s.br, n_hi, info + 1);
+                TN_CUDA(cudaMemcpyAsync(hS.data(), Sf, R * sizeof(double), cudaMemcpyDeviceToHost, st));
+                TN_CUDA(cudaStreamSynchronize(st));
+                delta = mixing(hS[n_hi]);
+                ++n_deflate;
+              }
+            }
             if (delta > 1e-2) {
               method = fallback_method;
               nbas = s.mn;
@@ -746,6 +787,7 @@ struct Engine {
     TN_CUDA(cudaSetDevice(device));
     primal_valid = false;
     n_fallback = 0;
+    n_deflate = 0;
     const double wc0 = work_counter.load();
     Pool pool(st);
     TN_CUDA(cudaMemcpyAsync(at(o_gates), gates, (size_t)K * 16 * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
@@ -810,7 +852,7 @@ struct Engine {
                            "," + std::to_string(sc[2]) + ") discarded=" + std::to_string(sc[3]) +
                            " gap=" + std::to_string(sc[4]) + " log10s=" + std::to_string(sc[5]));
     sc[6] = (double)n_fallback.load();
-    sc[7] = 0;
+    sc[7] = (double)n_deflate.load();
     TN_CUDA(cudaMemcpyAsync(scalars, sc, 8 * sizeof(double), cudaMemcpyHostToDevice, st));
     TN_CUDA(cudaMemcpyAsync(at<double>(o_scal), sc, 8 * sizeof(double), cudaMemcpyHostToDevice, st));
     TN_CUDA(cudaStreamSynchronize(st));

@@ -32,7 +32,7 @@ for m in ("eigh",):
     sc, gR = eng.environments(torch.tensor(G, device=dev))
     H = eng.apply(torch.tensor(V, device=dev))
     torch.cuda.synchronize()
-    out[m] = {"f": sc[0].item(), "gR": gR.cpu().numpy(), "H": H.cpu().numpy(), "diag": sc[3:7].tolist()}
+    out[m] = {"f": sc[0].item(), "gR": gR.cpu().numpy(), "H": H.cpu().numpy(), "diag": sc[3:8].tolist()}
     eng.close()
 t0 = time.time()
 o = M.MPOOracle(cfg.n, cfg.depth, cfg.chi, G, [x.detach().resolve_conj().cpu().numpy() for x in ref], V)
