@@ -77,7 +77,8 @@ tn_status tn_hvp_setup(const tn_hvp_config* cfg, const int32_t* ref_bonds, const
  * f and the Riemannian gradient.
  * gates: DEVICE [K][4][4].
  * scalars_out: DEVICE double[8] = {f, Re T, Im T, max discarded weight,
- *   min relative gap at a cut, max log10 |s|, 0, 0}.
+ *   min relative gap at a cut, max |log10 s|, #QR-iteration SVD fallbacks,
+ *   #second-level Gram deflations}.
  * grad_R_out: DEVICE [K][4][4] (may be NULL).
  * Synchronises the stream once at the end (SVD convergence flags). */
 tn_status tn_hvp_environments(tn_hvp_ctx* ctx, const void* gates, void* scalars_out, void* grad_R_out,
