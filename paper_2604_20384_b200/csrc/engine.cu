@@ -361,6 +361,12 @@ struct Engine {
     TN_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t thr = UINT64_MAX;
     TN_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    // no cross-stream reuse dependencies: the bottom and top sweeps run on two
+    // streams and must not be serialised through recycled pool blocks
+    int off = 0;
+    TN_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseFollowEventDependencies, &off));
+    TN_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowOpportunistic, &off));
+    TN_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &off));
     debug = std::getenv("TN_DEBUG") != nullptr;
     if (const char* f = std::getenv("TN_SVD_FALLBACK")) fallback_method = std::string(f) == "gesvdj" ? 0 : 2;
     if (const char* m = std::getenv("TN_SVD")) {
@@ -813,7 +819,15 @@ struct Engine {
     TN_CUDA(cudaEventRecord(ev_fork, st));
     TN_CUDA(cudaStreamWaitEvent(st2, ev_fork, 0));
     std::exception_ptr top_err;
+    const bool serial = std::getenv("TN_SERIAL_PRIMAL") != nullptr;
+    if (serial) {  // diagnostic: bottom then top on the caller's stream
+      Mps BD = primal_side(st, sol[0], pool, false, true, info, dg);
+      for (cplx*& p : BD.a) ddel(p, st);
+      Mps T0 = primal_side(st, sol[0], pool, true, true, info + 2, dg + 8);
+      for (cplx*& p : T0.a) ddel(p, st);
+    }
     std::thread th([&] {
+      if (serial) return;
       try {
         TN_CUDA(cudaSetDevice(device));
         Pool pool2(st2);
@@ -824,8 +838,10 @@ struct Engine {
       }
     });
     try {
-      Mps BD = primal_side(st, sol[0], pool, false, true, info, dg);
-      for (cplx*& p : BD.a) ddel(p, st);
+      if (!serial) {
+        Mps BD = primal_side(st, sol[0], pool, false, true, info, dg);
+        for (cplx*& p : BD.a) ddel(p, st);
+      }
     } catch (...) {
       th.join();
       throw;

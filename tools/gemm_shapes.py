@@ -40,6 +40,13 @@ for M_, N_, K_, b, oa, ob, t in rows:
     buck[key][2] += w
 for k, (n, t, w) in sorted(buck.items(), key=lambda x: -x[1][1])[:25]:
     print(f"{k:12s} n={n:6d} {t:9.2f} ms  {8*w/t/1e9 if t else 0:6.2f} TF/s")
+import math
+def ctas(M_, N_, b):
+    return math.ceil(int(M_) / 64) * math.ceil(int(N_) / 64) * int(b)
+small = [r for r in rows if ctas(r[0], r[1], r[3]) < 148]
+mid = [r for r in rows if 148 <= ctas(r[0], r[1], r[3]) < 592]
+print("grids < 148 CTAs: n=%d  %.1f ms;  148..591: n=%d  %.1f ms" % (len(small), sum(float(r[6]) for r in small),
+      len(mid), sum(float(r[6]) for r in mid)))
 slow = sorted(rows, key=lambda r: -float(r[6]))[:15]
 print("slowest launches (M N K batch op ms TF/s):")
 for M_, N_, K_, b, oa, ob, t in slow:
