@@ -1395,24 +1395,36 @@ struct Engine {
         nn(st, ub[s], w * bb[e], bb[s], LTb[s], 0, q.BB, 0, YT0, 0, 1);
       }
       if (k >= 0) {
-        // ---- extraction: top TT
-        const int64_t sZ = (int64_t)16 * tb[s] * tb[e];
-        cplx* Z = bpool.c(sZ * nb);
-        nn(st, 16 * tb[s], tb[e], bb[e], YV, sYV, R0e, 0, Z, sZ, nb);
-        nn(st, 16 * tb[s], tb[e], bb[e], Y0, 0, dRV[e], (int64_t)bb[e] * tb[e], Z, sZ, nb, ONE, ONE);
-        if (!skipB) {
-          nn(st, 16 * tb[s], tb[e], ya[e], YB, sYB, RBa[e], 0, Z, sZ, nb, ONE, ONE);
-          cplx* LBA = bpool.c((int64_t)16 * tb[s] * xb[e]);
-          nn(st, tb[s], 16 * xb[e], xb[s], LBb[s], 0, q.BAbB, 0, LBA, 0, 1);
-          nn(st, 16 * tb[s], tb[e], xb[e], LBA, 0, dRB[e], (int64_t)xb[e] * tb[e], Z, sZ, nb, ONE, ONE);
+        // ---- extraction.  Terms whose right environment R is shared across
+        // directions use Wt = Theta_top R^H (once per block) so that
+        // sum conj(top) (Y R) = sum conj(Wt) Y  -- no per-direction Y R product.
+        {
+          cplx* Wt = bpool.c((int64_t)16 * tb[s] * bb[e]);                 // TT R0^H
+          nc(st, 16 * tb[s], bb[e], tb[e], q.TT, 0, R0e, 0, Wt, 0, 1);
+          extract_env(st, HT + (int64_t)k * 16, KK, Wt, 0, YV, sYV, tb[s], bb[e], nb, ONE);
         }
-        extract_env(st, HT + (int64_t)k * 16, KK, q.TT, 0, Z, sZ, tb[s], tb[e], nb, ONE);
+        {  // per-direction right environments: Z = Y0 dRV (+ LBb BAbB dRB)
+          const int64_t sZ = (int64_t)16 * tb[s] * tb[e];
+          cplx* Z = bpool.c(sZ * nb);
+          nn(st, 16 * tb[s], tb[e], bb[e], Y0, 0, dRV[e], (int64_t)bb[e] * tb[e], Z, sZ, nb);
+          if (!skipB) {
+            cplx* LBA = bpool.c((int64_t)16 * tb[s] * xb[e]);
+            nn(st, tb[s], 16 * xb[e], xb[s], LBb[s], 0, q.BAbB, 0, LBA, 0, 1);
+            nn(st, 16 * tb[s], tb[e], xb[e], LBA, 0, dRB[e], (int64_t)xb[e] * tb[e], Z, sZ, nb, ONE, ONE);
+          }
+          extract_env(st, HT + (int64_t)k * 16, KK, q.TT, 0, Z, sZ, tb[s], tb[e], nb, ONE);
+        }
+        if (!skipB) {  // (dLB BAaB + LBb BBd) RBa  ->  Wt = TT RBa^H
+          cplx* Wt = bpool.c((int64_t)16 * tb[s] * ya[e]);
+          nc(st, 16 * tb[s], ya[e], tb[e], q.TT, 0, RBa[e], 0, Wt, 0, 1);
+          extract_env(st, HT + (int64_t)k * 16, KK, Wt, 0, YB, sYB, tb[s], ya[e], nb, ONE);
+        }
         if (!skipT) {
-          // top TAaB with (dLT BB) RTa
-          const int64_t sZ2 = (int64_t)16 * va[s] * va[e];
-          cplx* Z2 = bpool.c(sZ2 * nb);
-          nn(st, 16 * va[s], va[e], bb[e], YT, sYT, RTa[e], 0, Z2, sZ2, nb);
-          extract_env(st, HT + (int64_t)k * 16, KK, q.TAaB, 0, Z2, sZ2, va[s], va[e], nb, ONE);
+          {  // top TAaB with (dLT BB) RTa  ->  Wt = TAaB RTa^H
+            cplx* Wt = bpool.c((int64_t)16 * va[s] * bb[e]);
+            nc(st, 16 * va[s], bb[e], va[e], q.TAaB, 0, RTa[e], 0, Wt, 0, 1);
+            extract_env(st, HT + (int64_t)k * 16, KK, Wt, 0, YT, sYT, va[s], bb[e], nb, ONE);
+          }
           // per-dir top TBd with shared (LTb BB) RTa
           const int64_t sZ3 = (int64_t)16 * ub[s] * va[e];
           cplx* Z3 = bpool.c(sZ3);
