@@ -1253,6 +1253,7 @@ struct Engine {
     // block tensors cache (per block start site)
     struct Blk {
       cplx *TT = nullptr, *TTg = nullptr, *BB = nullptr;          // primal blocks (TTg gated with G^dag)
+      cplx* TTp = nullptr;                                          // TT with out legs split off
       cplx *BAaB = nullptr, *BAbB = nullptr, *BBd = nullptr;       // bottom chains + per-dir block
       cplx *TAaB = nullptr, *TAaG = nullptr, *TAbB = nullptr, *TAbG = nullptr, *TBd = nullptr, *TBdG = nullptr;
     };
@@ -1275,6 +1276,10 @@ struct Engine {
       };
       q.TT = mk2(tpv, tb);
       q.TTg = gated(q.TT, tb[s], tb[e]);
+      if (k >= 0) {
+        q.TTp = pool.c((int64_t)16 * tb[s] * tb[e]);
+        out_leg_split(st, q.TTp, q.TT, tb[s], tb[e]);
+      }
       q.BB = mk2(bpv, bb);
       if (!skipB) {
         q.BAaB = mk2(BAa, ya);
@@ -1323,12 +1328,16 @@ struct Engine {
         nn(st, w * bb[s], tb[e], bb[e], q.BB, 0, dRV[e], (int64_t)bb[e] * tb[e], Y, sY, nb);
         dRV[s] = pool.c((int64_t)bb[s] * tb[s] * nb);
         nc(st, bb[s], tb[s], w * tb[e], Y, sY, q.TTg, 0, dRV[s], (int64_t)bb[s] * tb[s], nb);
-        if (k >= 0) {
+        if (k >= 0) {  // (V Y0) TT^H = sum_ac V[a,c] Y0_c TT_a^H: 16 shared products, one K=16 GEMM
           cplx* Y0 = rp.c(sY);
           nn(st, w * bb[s], tb[e], bb[e], q.BB, 0, R0e, 0, Y0, 0, 1);
-          cplx* YV = rp.c(sY * nb);
-          apply_gate(st, YV, sY, Y0, 0, Vd + (int64_t)k * 16, KK, bb[s], tb[e], nb, ONE, false);
-          nc(st, bb[s], tb[s], w * tb[e], YV, sY, q.TT, 0, dRV[s], (int64_t)bb[s] * tb[s], nb, ONE, ONE);
+          cplx* Y0p = rp.c(sY);
+          out_leg_split(st, Y0p, Y0, bb[s], tb[e]);
+          const int64_t sq = (int64_t)bb[s] * tb[s], sy = (int64_t)bb[s] * 4 * tb[e], stt = (int64_t)tb[s] * 4 * tb[e];
+          cplx* Q = rp.c(16 * sq);
+          for (int a = 0; a < 4; ++a)  // Q[a*4+c] = Y0p[c] TTp[a]^H
+            nc(st, bb[s], tb[s], 4 * tb[e], Y0p, sy, q.TTp + a * stt, 0, Q + (int64_t)a * 4 * sq, sq, 4);
+          mm(st, 'N', 'N', nb, (int)sq, 16, ONE, Vd + (int64_t)k * 16, KK, 0, Q, sq, 0, ONE, dRV[s], sq, 0, 1);
         }
       }
       if (!skipB) {  // dRB[s] = (BAbB dRB[e] + BBd RBa[e]) TTg^H
@@ -1441,10 +1450,14 @@ struct Engine {
       {  // dLV' = TT^H (G YV + V Y0)  ==  TTg^H YV + TT^H (V Y0)
         cplx* nL = dnew((int64_t)tb[e] * bb[e] * nb, st);
         cn(st, tb[e], bb[e], w * tb[s], q.TTg, 0, YV, sYV, nL, (int64_t)tb[e] * bb[e], nb);
-        if (k >= 0) {
-          cplx* YVV = bpool.c(sYV * nb);
-          apply_gate(st, YVV, sYV, Y0, 0, Vd + (int64_t)k * 16, KK, tb[s], bb[e], nb, ONE, false);
-          cn(st, tb[e], bb[e], w * tb[s], q.TT, 0, YVV, sYV, nL, (int64_t)tb[e] * bb[e], nb, ONE, ONE);
+        if (k >= 0) {  // TT^H (V Y0) = sum_ac V[a,c] TT_a^H Y0_c: 16 shared products, one K=16 GEMM
+          cplx* Y0p = bpool.c(sYV);
+          out_leg_split(st, Y0p, Y0, tb[s], bb[e]);
+          const int64_t sp = (int64_t)tb[e] * bb[e], sy = (int64_t)tb[s] * 4 * bb[e], stt = (int64_t)tb[s] * 4 * tb[e];
+          cplx* Pm = bpool.c(16 * sp);
+          for (int a = 0; a < 4; ++a)  // P[a*4+c] = TTp[a]^H Y0p[c]
+            cn(st, tb[e], bb[e], 4 * tb[s], q.TTp + a * stt, 0, Y0p, sy, Pm + (int64_t)a * 4 * sp, sp, 4);
+          mm(st, 'N', 'N', nb, (int)sp, 16, ONE, Vd + (int64_t)k * 16, KK, 0, Pm, sp, 0, ONE, nL, sp, 0, 1);
         }
         dset(dLV, nL, st);
       }

@@ -491,6 +491,21 @@ __global__ void s_from_norms_kernel(const double* __restrict__ nrm, const double
   }
 }
 
+// dst[(o1 o2)][x][i1][i2][y] = src[x][(o1 i1)][(o2 i2)][y]  (split off the out legs)
+__global__ void out_leg_split_kernel(cplx* __restrict__ dst, const cplx* __restrict__ src, int X, int Y) {
+  const int64_t n = (int64_t)X * 16 * Y;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int y = (int)(idx % Y);
+    int64_t r = idx / Y;
+    const int i12 = (int)(r % 4);
+    r /= 4;
+    const int x = (int)(r % X);
+    const int a = (int)(r / X);
+    const int o1 = a >> 1, o2 = a & 1, i1 = i12 >> 1, i2 = i12 & 1;
+    dst[idx] = src[(((int64_t)x * 4 + (o1 * 2 + i1)) * 4 + (o2 * 2 + i2)) * Y + y];
+  }
+}
+
 __global__ void conj_copy_kernel(cplx* __restrict__ dst, const cplx* __restrict__ src, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = cconj(src[i]);
@@ -656,6 +671,14 @@ void eig_to_svd(cudaStream_t st, cplx* uhf, double* S, const cplx* W, const doub
 
 void s_from_norms(cudaStream_t st, const double* nrm, const double* S, int mn, int r, double* s_out, double* diag) {
   s_from_norms_kernel<<<1, 1, 0, st>>>(nrm, S, mn, r, s_out, diag);
+  TN_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+void out_leg_split(cudaStream_t st, cplx* dst, const cplx* src, int X, int Y) {
+  const int64_t n = (int64_t)X * 16 * Y;
+  if (!n) return;
+  out_leg_split_kernel<<<nblocks(n), TPB, 0, st>>>(dst, src, X, Y);
   TN_CUDA(cudaGetLastError());
   count_launch();
 }
