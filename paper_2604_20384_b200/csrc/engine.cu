@@ -1492,6 +1492,12 @@ struct Engine {
       dagger4(st, Vd, V, (int64_t)K * nb);
       cplx* HT = pool.c(KK * nb);
       TN_CUDA(cudaMemsetAsync(HT, 0, (size_t)KK * nb * sizeof(cplx), st));
+      const bool phases = std::getenv("TN_PHASES") != nullptr;
+      cudaEvent_t pe[4];
+      if (phases)
+        for (auto& e : pe) TN_CUDA(cudaEventCreate(&e));
+      float t_fwd = 0, t_bwd = 0, t_hvp = 0;
+      if (phases) TN_CUDA(cudaEventRecord(pe[0], st));
       // forward (bottom) tangent, cached per layer: DB_{ell-1}
       std::vector<TanSnap> DB(D);
       {
@@ -1503,16 +1509,42 @@ struct Engine {
         }
         release(t, st);
       }
+      if (phases) {
+        TN_CUDA(cudaEventRecord(pe[1], st));
+        TN_CUDA(cudaEventSynchronize(pe[1]));
+        TN_CUDA(cudaEventElapsedTime(&t_fwd, pe[0], pe[1]));
+      }
       // backward (top) tangent on the fly + layer HVP extraction
       Tangent t;
       tangent_init(st, t, top, true, nb);
       for (size_t li = 0; li < top.steps.size(); ++li) {
         const int ell = top.ell[li];
+        if (phases) TN_CUDA(cudaEventRecord(pe[2], st));
         layer_hvp(st, ell, DB[ell - 1], t, V, HT, nb, ell == 1, li == 0);
         release(DB[ell - 1], st);
+        if (phases) {
+          TN_CUDA(cudaEventRecord(pe[3], st));
+          TN_CUDA(cudaEventSynchronize(pe[3]));
+          float a = 0;
+          TN_CUDA(cudaEventElapsedTime(&a, pe[2], pe[3]));
+          t_hvp += a;
+          TN_CUDA(cudaEventRecord(pe[2], st));
+        }
         for (const Step& s : top.steps[li]) tangent_step(st, t, s, at(o_gdag), Vd, nb);
+        if (phases) {
+          TN_CUDA(cudaEventRecord(pe[3], st));
+          TN_CUDA(cudaEventSynchronize(pe[3]));
+          float a = 0;
+          TN_CUDA(cudaEventElapsedTime(&a, pe[2], pe[3]));
+          t_bwd += a;
+        }
       }
       release(t, st);
+      if (phases) {
+        fprintf(stderr, "[tn phases] sub-batch %d: forward tangent %.1f ms, backward tangent %.1f ms, layer HVP %.1f ms\n",
+                nb, t_fwd, t_bwd, t_hvp);
+        for (auto& e : pe) cudaEventDestroy(e);
+      }
       cplx* om = pool.c(nb);
       hessian_post(st, K, nb, at(o_gates), at(o_E), at(o_gradf), at<double>(o_scal), HT, V, om,
                    hess + (int64_t)b0 * KK);

@@ -10,6 +10,7 @@
 // strides padded so every fragment load (one LDS.128 = one complex) is
 // bank-conflict free.  op(A), op(B) in {N, T, C}; conjugation is folded into
 // the fragment sign.  Row-major everywhere; batch strides may be 0 (shared).
+#include <algorithm>
 #include <array>
 #include <atomic>
 #include <cstdio>
@@ -41,6 +42,8 @@ constexpr int SMEM_BYTES = 2 * STAGE * (int)sizeof(cplx);
 
 struct Params {
   int M, N, K;
+  int ksplit;          // > 1: blockIdx.z = batch * ksplit + split, partial sums to `part`
+  double* part;        // [batch][ksplit][M][N] complex partials (split-K only)
   cplx alpha, beta;
   int has_beta;
   const cplx* A;
@@ -190,13 +193,17 @@ template <char OPA, char OPB>
 __global__ void __launch_bounds__(NT3, 1) zgemm3m_kernel(Params p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cplx* smem = reinterpret_cast<cplx*>(smem_raw);
-  const int64_t bz = blockIdx.z;
+  const int ks = p.ksplit > 1 ? p.ksplit : 1;
+  const int64_t bz = blockIdx.z / ks;
+  const int split = blockIdx.z % ks;
   const cplx* __restrict__ A = p.A + bz * p.sA;
   const cplx* __restrict__ B = p.B + bz * p.sB;
   cplx* __restrict__ C = p.C + bz * p.sC;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 1, wn = warp & 1;  // 4 x 2 warps: warp rows of 16, columns of 32
+  const int nk_all = (p.K + BK - 1) / BK;
+  const int kt0 = (int)((int64_t)nk_all * split / ks), kt1 = (int)((int64_t)nk_all * (split + 1) / ks);
   const int g = lane >> 2, q = lane & 3;
 
   auto load_stage = [&](int stage, int k0) {
@@ -238,10 +245,10 @@ __global__ void __launch_bounds__(NT3, 1) zgemm3m_kernel(Params p) {
 #pragma unroll
       for (int t = 0; t < 2; ++t) p1[i][j][t] = p2[i][j][t] = p3[i][j][t] = 0.0;
 
-  const int nk = (p.K + BK - 1) / BK;
+  const int nk = kt1 - kt0;
 #pragma unroll
   for (int s = 0; s < NSTAGE3 - 1; ++s) {
-    if (s < nk) load_stage(s, s * BK);
+    if (s < nk) load_stage(s, (kt0 + s) * BK);
     cp_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
@@ -249,7 +256,7 @@ __global__ void __launch_bounds__(NT3, 1) zgemm3m_kernel(Params p) {
     __syncthreads();
     {
       const int nx = kt + NSTAGE3 - 1;
-      if (nx < nk) load_stage(nx % NSTAGE3, nx * BK);
+      if (nx < nk) load_stage(nx % NSTAGE3, (kt0 + nx) * BK);
       cp_commit();
     }
     const cplx* sA = smem + (kt % NSTAGE3) * STAGE;
@@ -297,13 +304,33 @@ __global__ void __launch_bounds__(NT3, 1) zgemm3m_kernel(Params p) {
         if (col < p.N) {
           const double re = p1[mi][ni][j] - p2[mi][ni][j];
           const double im = p3[mi][ni][j] - p1[mi][ni][j] - p2[mi][ni][j];
-          cplx v = cmul(p.alpha, make_double2(re, im));
-          cplx* dst = C + (int64_t)row * p.ldc + col;
-          if (p.has_beta) v = cadd(v, cmul(p.beta, *dst));
-          *dst = v;
+          if (ks > 1) {  // partial of this K slice (reduced in split order by zreduce_kernel)
+            reinterpret_cast<cplx*>(p.part)[((bz * ks + split) * (int64_t)p.M + row) * p.N + col] = make_double2(re, im);
+          } else {
+            cplx v = cmul(p.alpha, make_double2(re, im));
+            cplx* dst = C + (int64_t)row * p.ldc + col;
+            if (p.has_beta) v = cadd(v, cmul(p.beta, *dst));
+            *dst = v;
+          }
         }
       }
     }
+  }
+}
+
+// C = alpha * sum_split part + beta * C, splits summed in fixed order (deterministic)
+__global__ void zreduce_kernel(Params p, int batch) {
+  const int64_t mn = (int64_t)p.M * p.N, total = mn * batch;
+  const cplx* part = reinterpret_cast<const cplx*>(p.part);
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = idx / mn, e = idx % mn;
+    cplx acc = make_double2(0, 0);
+    for (int sp = 0; sp < p.ksplit; ++sp) acc = cadd(acc, part[(b * p.ksplit + sp) * mn + e]);
+    const int row = (int)(e / p.N), col = (int)(e % p.N);
+    cplx v = cmul(p.alpha, acc);
+    cplx* dst = p.C + b * p.sC + (int64_t)row * p.ldc + col;
+    if (p.has_beta) v = cadd(v, cmul(p.beta, *dst));
+    *dst = v;
   }
 }
 
@@ -325,6 +352,19 @@ void launch(const Params& p, int batch, cudaStream_t st) {
     attr = true;
   }
   dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, batch);
+  Params q = p;
+  q.ksplit = 1;
+  q.part = nullptr;
+  const int64_t ctas = (int64_t)grid.x * grid.y * batch;
+  const int nk = (p.K + BK - 1) / BK;
+  if (variant() == 1 && ctas < 148 && nk >= 16) {  // split K to fill the SMs (>= 8 k-tiles per split)
+    int ks = (int)std::min<int64_t>((296 + ctas - 1) / ctas, nk / 8);
+    if (ks > 1) {
+      q.ksplit = ks;
+      TN_CUDA(cudaMallocAsync((void**)&q.part, sizeof(cplx) * (size_t)ks * p.M * p.N * batch, st));
+      grid.z = batch * ks;
+    }
+  }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (g_prof.on) {
     TN_CUDA(cudaEventCreate(&e0));
@@ -332,11 +372,18 @@ void launch(const Params& p, int batch, cudaStream_t st) {
     TN_CUDA(cudaEventRecord(e0, st));
   }
   if (variant() == 1)
-    zgemm3m_kernel<OPA, OPB><<<grid, NT3, SMEM3_BYTES, st>>>(p);
+    zgemm3m_kernel<OPA, OPB><<<grid, NT3, SMEM3_BYTES, st>>>(q);
   else
     zgemm_kernel<OPA, OPB><<<grid, NT, SMEM_BYTES, st>>>(p);
   TN_CUDA(cudaGetLastError());
   count_launch();
+  if (q.ksplit > 1) {
+    const int64_t tot = (int64_t)p.M * p.N * batch;
+    zreduce_kernel<<<(int)std::min<int64_t>((tot + 255) / 256, 148 * 16), 256, 0, st>>>(q, batch);
+    TN_CUDA(cudaGetLastError());
+    count_launch();
+    TN_CUDA(cudaFreeAsync(q.part, st));
+  }
   if (g_prof.on) {
     TN_CUDA(cudaEventRecord(e1, st));
     std::lock_guard<std::mutex> lk(g_prof_mu);
@@ -406,6 +453,8 @@ void zgemm(cudaStream_t st, char opa, char opb, int M, int N, int K, cplx alpha,
            int batch) {
   if (M <= 0 || N <= 0 || batch <= 0) return;
   Params p;
+  p.ksplit = 1;
+  p.part = nullptr;
   p.alpha = alpha;
   p.beta = beta;
   p.has_beta = (beta.x != 0.0 || beta.y != 0.0);

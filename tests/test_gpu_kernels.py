@@ -15,7 +15,8 @@ def _rand(shape, seed):
 
 
 @pytest.mark.parametrize("opa,opb", [(a, b) for a in "NTC" for b in "NTC"])
-@pytest.mark.parametrize("M,N,K,batch", [(64, 64, 16, 1), (70, 33, 29, 3), (1, 1, 1, 2), (130, 257, 200, 2)])
+@pytest.mark.parametrize("M,N,K,batch", [(64, 64, 16, 1), (70, 33, 29, 3), (1, 1, 1, 2), (130, 257, 200, 2),
+                                         (64, 96, 1000, 1), (100, 64, 2050, 3)])  # last two: split-K
 def test_zgemm_ops_ragged(opa, opb, M, N, K, batch):
     from paper_2604_20384_b200.api import zgemm
     As = (batch, M, K) if opa == "N" else (batch, K, M)

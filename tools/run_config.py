@@ -43,5 +43,6 @@ out.update({"t_env_s": t1 - t0, "t_apply_s": t2 - t1, "batch": B, "f": sc[0].ite
 w_dir, w_pr = eng.work()
 out.update({"cmac_per_dir": w_dir, "cmac_primal": w_pr,
             "apply_tflops": 8 * w_dir * B / (t2 - t1) / 1e12, "hvp_per_s": B / (t2 - t1),
-            "step_hvp_per_s": B / (t2 - t0), "mem_gb": torch.cuda.max_memory_allocated() / 1e9})
+            "step_hvp_per_s": B / (t2 - t0), "mem_gb": torch.cuda.max_memory_allocated() / 1e9,
+            "device_used_gb": (torch.cuda.mem_get_info()[1] - torch.cuda.mem_get_info()[0]) / 1e9})
 print(json.dumps(out))
