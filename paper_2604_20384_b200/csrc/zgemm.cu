@@ -186,11 +186,10 @@ __global__ void __launch_bounds__(NT, 2) zgemm_kernel(Params p) {
 // P3 += (Ar + Ai)(Br + Bi); C_re = P1 - P2, C_im = P3 - P1 - P2.  CTA 64x64,
 // 8 warps (4 x 2), warp tile 16 x 32 (2 x 4 DMMA tiles), NSTAGE-deep cp.async
 // pipeline, one CTA per SM (<= 255 registers).
-constexpr int NT3 = 256, NSTAGE3 = 4;
-constexpr int SMEM3_BYTES = NSTAGE3 * STAGE * (int)sizeof(cplx);
+constexpr int NT3 = 256;
 
-template <char OPA, char OPB>
-__global__ void __launch_bounds__(NT3, 1) zgemm3m_kernel(Params p) {
+template <char OPA, char OPB, int NSTAGE3, int MINB>
+__global__ void __launch_bounds__(NT3, MINB) zgemm3m_kernel(Params p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cplx* smem = reinterpret_cast<cplx*>(smem_raw);
   const int ks = p.ksplit > 1 ? p.ksplit : 1;
@@ -334,21 +333,23 @@ __global__ void zreduce_kernel(Params p, int batch) {
   }
 }
 
-int g_variant = -1;  // 0 = 4M (4 warps, 2 stages), 1 = 3M (8 warps, 4 stages)
+int g_variant = -1;  // 0 = 4M (4 warps, 2 stages), 1 = 3M (8 warps, 4 stages, 1 CTA/SM), 2 = 3M (2 stages, 2 CTAs/SM)
 int variant() {
   if (g_variant < 0) {
     const char* v = std::getenv("TN_GEMM");
-    g_variant = (v && std::string(v) == "4m") ? 0 : 1;
+    g_variant = (v && std::string(v) == "4m") ? 0 : (v && std::string(v) == "3m2") ? 2 : 1;
   }
   return g_variant;
 }
+constexpr int SMEM3_4 = 4 * STAGE * (int)sizeof(cplx), SMEM3_2 = 2 * STAGE * (int)sizeof(cplx);
 
 template <char OPA, char OPB>
 void launch(const Params& p, int batch, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     TN_CUDA(cudaFuncSetAttribute(zgemm_kernel<OPA, OPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    TN_CUDA(cudaFuncSetAttribute(zgemm3m_kernel<OPA, OPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM3_BYTES));
+    TN_CUDA(cudaFuncSetAttribute(zgemm3m_kernel<OPA, OPB, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM3_4));
+    TN_CUDA(cudaFuncSetAttribute(zgemm3m_kernel<OPA, OPB, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM3_2));
     attr = true;
   }
   dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, batch);
@@ -357,7 +358,7 @@ void launch(const Params& p, int batch, cudaStream_t st) {
   q.part = nullptr;
   const int64_t ctas = (int64_t)grid.x * grid.y * batch;
   const int nk = (p.K + BK - 1) / BK;
-  if (variant() == 1 && ctas < 148 && nk >= 16) {  // split K to fill the SMs (>= 8 k-tiles per split)
+  if (variant() >= 1 && ctas < 148 && nk >= 16) {  // split K to fill the SMs (>= 8 k-tiles per split)
     int ks = (int)std::min<int64_t>((296 + ctas - 1) / ctas, nk / 8);
     if (ks > 1) {
       q.ksplit = ks;
@@ -372,7 +373,9 @@ void launch(const Params& p, int batch, cudaStream_t st) {
     TN_CUDA(cudaEventRecord(e0, st));
   }
   if (variant() == 1)
-    zgemm3m_kernel<OPA, OPB><<<grid, NT3, SMEM3_BYTES, st>>>(q);
+    zgemm3m_kernel<OPA, OPB, 4, 1><<<grid, NT3, SMEM3_4, st>>>(q);
+  else if (variant() == 2)
+    zgemm3m_kernel<OPA, OPB, 2, 2><<<grid, NT3, SMEM3_2, st>>>(q);
   else
     zgemm_kernel<OPA, OPB><<<grid, NT, SMEM_BYTES, st>>>(p);
   TN_CUDA(cudaGetLastError());
