@@ -333,11 +333,11 @@ __global__ void zreduce_kernel(Params p, int batch) {
   }
 }
 
-int g_variant = -1;  // 0 = 4M (4 warps, 2 stages), 1 = 3M (8 warps, 4 stages, 1 CTA/SM), 2 = 3M (2 stages, 2 CTAs/SM)
+int g_variant = -1;  // 0 = 4M (4 warps, 2 stages), 1 = 3M (8 warps, 4 stages, 1 CTA/SM), 2 = 3M (2 stages, 2 CTAs/SM, default)
 int variant() {
   if (g_variant < 0) {
     const char* v = std::getenv("TN_GEMM");
-    g_variant = (v && std::string(v) == "4m") ? 0 : (v && std::string(v) == "3m2") ? 2 : 1;
+    g_variant = (v && std::string(v) == "4m") ? 0 : (v && std::string(v) == "3m4") ? 1 : 2;
   }
   return g_variant;
 }
