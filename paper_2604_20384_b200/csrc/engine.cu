@@ -140,7 +140,6 @@ struct Engine {
   int svd_method = 3;  // 0 gesvdj, 1 Xgesvdp, 2 Xgesvd, 3 Gram heevd (default)
   int lwork_heevd = 0;
   int fallback_method = 2;  // TN_SVD_FALLBACK: gesvd (QR iteration, default) | gesvdj
-  bool debug = false;
   std::atomic<int> n_fallback{0}, n_deflate{0}, n_noise{0};
   size_t svd_dws = 0, svd_hws = 0;
   int lwork_geqrf = 0, lwork_ungqr = 0;
@@ -331,6 +330,13 @@ struct Engine {
     h_s.assign(s_index, 1.0);
   }
 
+  // Fresh device status word for one cuSOLVER call; fold it into `acc` afterwards.
+  int* call_info(Pool& pool, cudaStream_t st) {
+    int* p = (int*)pool.raw(sizeof(int));
+    TN_CUDA(cudaMemsetAsync(p, 0, sizeof(int), st));
+    return p;
+  }
+
   // ------------------------------------------------------------ setup --
   void setup(const tn_hvp_config& c, const int32_t* rb, const void* ref_mpo, cudaStream_t st) {
     cfg = c;
@@ -367,7 +373,6 @@ struct Engine {
     TN_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseFollowEventDependencies, &off));
     TN_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowOpportunistic, &off));
     TN_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &off));
-    debug = std::getenv("TN_DEBUG") != nullptr;
     if (const char* f = std::getenv("TN_SVD_FALLBACK")) fallback_method = std::string(f) == "gesvdj" ? 0 : 2;
     if (const char* m = std::getenv("TN_SVD")) {
       const std::string v(m);
@@ -472,11 +477,14 @@ struct Engine {
     cplx* tau = pool.c(std::min(rows, cols));
     cplx* work = pool.c(std::max(lwork_geqrf, lwork_ungqr));
     TN_SOLVER(cusolverDnSetStream(so.h, st));
+    int* ci = call_info(pool, st);
     TN_SOLVER(cusolverDnZgeqrf(so.h, rows, cols, (cuDoubleComplex*)cm, rows, (cuDoubleComplex*)tau,
-                               (cuDoubleComplex*)work, lwork_geqrf, info));
+                               (cuDoubleComplex*)work, lwork_geqrf, ci));
+    info_accum(st, info, ci);
     tri_extract(st, R, cm, kq, cols, rows, true);
     TN_SOLVER(cusolverDnZungqr(so.h, rows, kq, kq, (cuDoubleComplex*)cm, rows, (cuDoubleComplex*)tau,
-                               (cuDoubleComplex*)work, lwork_ungqr, info));
+                               (cuDoubleComplex*)work, lwork_ungqr, ci));
+    info_accum(st, info, ci);
     transpose(st, Q, cm, kq, rows, false);  // cm is (kq x rows) row-major -> Q rows x kq
   }
 
@@ -487,12 +495,15 @@ struct Engine {
     cplx* tau = pool.c(std::min(rows, cols));
     cplx* work = pool.c(std::max(lwork_geqrf, lwork_ungqr));
     TN_SOLVER(cusolverDnSetStream(so.h, st));
+    int* ci = call_info(pool, st);
     // column-major view: cols x rows matrix P^T
     TN_SOLVER(cusolverDnZgeqrf(so.h, cols, rows, (cuDoubleComplex*)cm, cols, (cuDoubleComplex*)tau,
-                               (cuDoubleComplex*)work, lwork_geqrf, info));
+                               (cuDoubleComplex*)work, lwork_geqrf, ci));
+    info_accum(st, info, ci);
     tri_extract(st, L, cm, rows, kq, cols, false);
     TN_SOLVER(cusolverDnZungqr(so.h, cols, kq, kq, (cuDoubleComplex*)cm, cols, (cuDoubleComplex*)tau,
-                               (cuDoubleComplex*)work, lwork_ungqr, info));
+                               (cuDoubleComplex*)work, lwork_ungqr, ci));
+    info_accum(st, info, ci);
     TN_CUDA(cudaMemcpyAsync(Q, cm, (size_t)kq * cols * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
   }
 
@@ -507,8 +518,10 @@ struct Engine {
       double* lam = (double*)pool.raw((size_t)R * sizeof(double));
       cplx* work = pool.c(std::max(lwork_heevd, 1));
       TN_SOLVER(cusolverDnSetStream(so.h, st));
+      int* ci = call_info(pool, st);
       TN_SOLVER(cusolverDnZheevd(so.h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, R, (cuDoubleComplex*)Gm, R,
-                                 lam, (cuDoubleComplex*)work, lwork_heevd, info));
+                                 lam, (cuDoubleComplex*)work, lwork_heevd, ci));
+      info_accum(st, info, ci);
       eig_to_svd(st, uhf, S, Gm, lam, R);
       return;
     }
@@ -526,23 +539,25 @@ struct Engine {
     cplx* Vp = pool.c((int64_t)nn_ * mn);
     void* dws = pool.raw(svd_dws + 64);
     TN_SOLVER(cusolverDnSetStream(so.h, st));
+    int* ci = call_info(pool, st);
     if (method == 0) {
       TN_SOLVER(cusolverDnZgesvdj(so.h, CUSOLVER_EIG_MODE_VECTOR, 1, m, nn_, (cuDoubleComplex*)M, m, S,
                                   (cuDoubleComplex*)Up, m, (cuDoubleComplex*)Vp, nn_, (cuDoubleComplex*)dws,
-                                  (int)(svd_dws / sizeof(cplx)), info, so.svdj));
+                                  (int)(svd_dws / sizeof(cplx)), ci, so.svdj));
     } else if (method == 1) {
       double herr = 0;
       TN_SOLVER(cusolverDnXgesvdp(so.h, so.prm, CUSOLVER_EIG_MODE_VECTOR, 1, m, nn_, CUDA_C_64F, M, m, CUDA_R_64F, S,
                                   CUDA_C_64F, Up, m, CUDA_C_64F, Vp, nn_, CUDA_C_64F, dws, svd_dws,
-                                  so.host_ws.data(), svd_hws, info, &herr));
+                                  so.host_ws.data(), svd_hws, ci, &herr));
     } else {
       // Xgesvd returns V^H (mn x nn_, ldvt = mn) in Vp
       TN_SOLVER(cusolverDnXgesvd(so.h, so.prm, 'S', 'S', m, nn_, CUDA_C_64F, M, m, CUDA_R_64F, S, CUDA_C_64F, Up, m,
-                                 CUDA_C_64F, Vp, mn, CUDA_C_64F, dws, svd_dws, so.host_ws.data(), svd_hws, info));
+                                 CUDA_C_64F, Vp, mn, CUDA_C_64F, dws, svd_dws, so.host_ws.data(), svd_hws, ci));
       cplx* V = pool.c((int64_t)nn_ * mn);
       transpose(st, V, Vp, nn_, mn, true);
       Vp = V;
     }
+    info_accum(st, info, ci);
     // column-major M = Up S Vp^H
     if (tr)  // M = A^T -> A = conj(Vp) S Up^T: U_A^H = Vp^T (row-major view of Vp)
       TN_CUDA(cudaMemcpyAsync(uhf, Vp, (size_t)mn * R * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
@@ -593,8 +608,10 @@ struct Engine {
     double* lam = (double*)pool.raw((size_t)nl * sizeof(double));
     cplx* work = pool.c(std::max(lwork_heevd, 1));
     TN_SOLVER(cusolverDnSetStream(so.h, st));
+    int* ci = call_info(pool, st);
     TN_SOLVER(cusolverDnZheevd(so.h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, nl, (cuDoubleComplex*)G2, nl,
-                               lam, (cuDoubleComplex*)work, lwork_heevd, info));
+                               lam, (cuDoubleComplex*)work, lwork_heevd, ci));
+    info_accum(st, info, ci);
     cplx* rot = pool.c((int64_t)nl * nl);
     eig_to_svd(st, rot, S + n_hi, G2, lam, nl);
     cplx* old = pool.c((int64_t)nl * R);

@@ -506,6 +506,8 @@ __global__ void out_leg_split_kernel(cplx* __restrict__ dst, const cplx* __restr
   }
 }
 
+__global__ void info_accum_kernel(int* acc, const int* info) { atomicMax(acc, abs(*info)); }
+
 __global__ void conj_copy_kernel(cplx* __restrict__ dst, const cplx* __restrict__ src, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = cconj(src[i]);
@@ -679,6 +681,12 @@ void out_leg_split(cudaStream_t st, cplx* dst, const cplx* src, int X, int Y) {
   const int64_t n = (int64_t)X * 16 * Y;
   if (!n) return;
   out_leg_split_kernel<<<nblocks(n), TPB, 0, st>>>(dst, src, X, Y);
+  TN_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+void info_accum(cudaStream_t st, int* acc, const int* info) {
+  info_accum_kernel<<<1, 1, 0, st>>>(acc, info);
   TN_CUDA(cudaGetLastError());
   count_launch();
 }

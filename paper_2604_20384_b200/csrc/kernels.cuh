@@ -49,6 +49,8 @@ void eig_to_svd(cudaStream_t st, cplx* uhf, double* S, const cplx* W, const doub
 void s_from_norms(cudaStream_t st, const double* nrm, const double* S, int mn, int r, double* s_out, double* diag);
 // dst[(o1 o2)][x][i1 i2][y] = src[x][(o1 i1)][(o2 i2)][y]
 void out_leg_split(cudaStream_t st, cplx* dst, const cplx* src, int X, int Y);
+// *acc = max(*acc, |*info|)  (cuSOLVER status accumulation)
+void info_accum(cudaStream_t st, int* acc, const int* info);
 // dst = conj(src), n elements
 void conj_copy(cudaStream_t st, cplx* dst, const cplx* src, int64_t n);
 // out_k = polar(G_k + alpha xi_k) (unitary retraction); status[0] = 1 on a singular iterate

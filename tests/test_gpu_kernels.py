@@ -93,3 +93,27 @@ def test_primal_export_import_roundtrip():
     primal_import(eng, blob, g1)
     H2 = eng.apply(torch.tensor(V, device=dev)).cpu().numpy()
     assert np.array_equal(H1, H2)
+
+
+def test_error_statuses():
+    """TN_ESTATE before a primal pass; TN_ENUMERIC on non-finite gates."""
+    from paper_2604_20384_b200 import _native as N
+    from paper_2604_20384_b200.api import HVPEngine
+    from tn_inputs.reference import reference_mpo
+    cfg = C.small_case(81, 6, 4, 8, batch=1)
+    ref = reference_mpo(C.reference_layers(cfg), cfg.n, cfg.chi)
+    K = C.num_gates(cfg.n, cfg.depth)
+    G = C.haar_gates(81, K)
+    dev = torch.device("cuda")
+    eng = HVPEngine(cfg.n, cfg.depth, cfg.chi, [a.to(dev) for a in ref], max_batch=1)
+    V = torch.tensor(C.tangent_directions(81, G, 1), device=dev)
+    with pytest.raises(N.TNError) as e:
+        eng.apply(V)
+    assert e.value.status == N.TN_ESTATE
+    Gbad = G.copy()
+    Gbad[3, 1, 2] = np.nan
+    with pytest.raises(N.TNError) as e:
+        eng.environments(torch.tensor(Gbad, device=dev))
+    assert e.value.status == N.TN_ENUMERIC
+    eng.environments(torch.tensor(G, device=dev))         # recovers
+    assert torch.isfinite(eng.apply(V)).all()
