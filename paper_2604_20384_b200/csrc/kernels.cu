@@ -2,6 +2,8 @@
 // out legs of two-site blocks, elementwise complex updates, gate-environment
 // extraction (warp-shuffle reductions), Alg. 2 postprocessing and the unitary
 // tangent projection (App. E).  All complex128 interleaved, row-major.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -575,12 +577,13 @@ __global__ void retract_kernel(int K, const cplx* __restrict__ G, const cplx* __
   for (int e = 0; e < 16; ++e) out[k * 16 + e] = x[e];
 }
 
-// out[b] = Re sum_i conj(A[b,i]) B[b,i]   (metric Re Tr(A^dag B), X15)
+// out[b] = Re sum_i conj(A[b,i]) B[b,i]   (metric Re Tr(A^dag B), X15):
+// grid (nblk, batch) block partials, then an ordered sum (deterministic).
 __global__ void tangent_dot_kernel(int64_t n, const cplx* __restrict__ A, const cplx* __restrict__ B,
-                                   double* __restrict__ out) {
-  const int b = blockIdx.x;
+                                   double* __restrict__ part) {
+  const int b = blockIdx.y;
   double acc = 0;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const cplx a = A[b * n + i], c = B[b * n + i];
     acc += a.x * c.x + a.y * c.y;
   }
@@ -591,6 +594,15 @@ __global__ void tangent_dot_kernel(int64_t n, const cplx* __restrict__ A, const 
   if (threadIdx.x == 0) {
     double t = 0;
     for (int j = 0; j < (int)(blockDim.x >> 5); ++j) t += red[j];
+    part[(int64_t)b * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+__global__ void dot_finish_kernel(const double* __restrict__ part, int nblk, double* __restrict__ out) {
+  const int b = blockIdx.x;
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int j = 0; j < nblk; ++j) t += part[(int64_t)b * nblk + j];
     out[b] = t;
   }
 }
@@ -707,9 +719,17 @@ void retract(cudaStream_t st, int K, const cplx* G, const cplx* xi, double alpha
 
 void tangent_dot(cudaStream_t st, int64_t n, int batch, const cplx* A, const cplx* B, double* out) {
   if (!batch) return;
-  tangent_dot_kernel<<<batch, 256, 0, st>>>(n, A, B, out);
+  int nblk = (int)std::min<int64_t>((n + 2047) / 2048, 256);
+  if (nblk < 1) nblk = 1;
+  double* part = nullptr;
+  TN_CUDA(cudaMallocAsync((void**)&part, sizeof(double) * (size_t)nblk * batch, st));
+  tangent_dot_kernel<<<dim3(nblk, batch), 256, 0, st>>>(n, A, B, part);
   TN_CUDA(cudaGetLastError());
   count_launch();
+  dot_finish_kernel<<<batch, 32, 0, st>>>(part, nblk, out);
+  TN_CUDA(cudaGetLastError());
+  count_launch();
+  TN_CUDA(cudaFreeAsync(part, st));
 }
 
 void finish_cost(cudaStream_t st, double* scalars, const cplx* T11) {
