@@ -269,7 +269,7 @@ def main():
     peak, peak_src = fp64_peak()
     achieved = 8 * gemm_cmac / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", f"traffic_c{cfg.cid}.json")
+    tpath = os.path.join(ROOT, "profiles", f"traffic_c{cfg.cid}.json")  # ncu dram bytes/launch (committed)
     if os.path.exists(tpath):
         with open(tpath) as f:
             traffic = json.load(f).get("bytes_per_launch")
@@ -282,7 +282,9 @@ def main():
                    "l2": "working set (primal store, tangent caches: GBs) > 126 MB L2; no flush"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "kernel": "zgemm_kernel (DMMA m8n8k4 f64)", "peak_source": peak_src,
+                     "kernel": "tn::zgemm3m_kernel (DMMA m8n8k4 f64, 3M: 3 real DMMA per complex k-step; "
+                               "algorithmic 8 flop per complex MAC, so frac can exceed 1 up to 4/3)",
+                     "peak_source": peak_src,
                      "gemm_share_of_step": gemm_ms / ms if ms else None,
                      "flops_per_step": 8 * gemm_cmac, "apply_cmac_per_direction": cmac_dir,
                      "primal_cmac": cmac_primal},
