@@ -12,6 +12,17 @@ most significant; a gate's 4x4 index is 2 q_i + q_{i+1} (X6).
 from __future__ import annotations
 
 import numpy as np
+import scipy.linalg as _sla
+
+
+def _svd(a):
+    """Thin SVD (LAPACK gesdd); if divide-and-conquer does not converge (seen
+    on blocks with many singular values at the noise floor), the QR-iteration
+    driver gesvd computes the same decomposition."""
+    try:
+        return np.linalg.svd(a, full_matrices=False)
+    except np.linalg.LinAlgError:
+        return _sla.svd(a, full_matrices=False, lapack_driver="gesvd")
 
 from .common import apply_out_gate, bottom_order_lr, layers, top_order_lr
 
@@ -215,7 +226,7 @@ class DenseTruncated:
         xp = vec_apply(x, n, s, M)
         dxp = [vec_apply(d, n, s, M) + vec_apply(x, n, s, vm) for d, vm in zip(dx, VM)]
         mat = xp.reshape(4 ** c, -1)
-        U, S, Vh = np.linalg.svd(mat, full_matrices=False)
+        U, S, Vh = _svd(mat)
         r = min(self.chi, 4 * bonds[c], 4 * bonds[c - 1], 4 * bonds[c + 1], len(S))
         Ur, Vr = U[:, :r], Vh[:r]
         y = Ur @ (Ur.conj().T @ mat)

@@ -26,6 +26,17 @@ S or of a QR factor is ever formed.
 from __future__ import annotations
 
 import numpy as np
+import scipy.linalg as _sla
+
+
+def _svd(a):
+    """Thin SVD (LAPACK gesdd); if divide-and-conquer does not converge (seen
+    on blocks with many singular values at the noise floor), the QR-iteration
+    driver gesvd computes the same decomposition."""
+    try:
+        return np.linalg.svd(a, full_matrices=False)
+    except np.linalg.LinAlgError:
+        return _sla.svd(a, full_matrices=False, lapack_driver="gesvd")
 
 from .common import apply_out_gate, bottom_order_lr, layers, top_order_lr
 
@@ -107,7 +118,7 @@ class MPOSweep:
         bl, m, br = P[i].shape[0], P[i].shape[2], P[i + 1].shape[2]
         theta = np.einsum("apb,bqc->apqc", P[i], P[i + 1])
         thp = apply_out_gate(theta, M).reshape(bl * 4, 4 * br)
-        U, S, Vh = np.linalg.svd(thp, full_matrices=False)
+        U, S, Vh = _svd(thp)
         r = min(self.chi, 4 * m, 4 * bl, 4 * br, len(S))
         Ur, Sr, Vr = U[:, :r], S[:r], Vh[:r]
         W = Vr.conj().T

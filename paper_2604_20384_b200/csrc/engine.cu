@@ -143,8 +143,8 @@ struct Engine {
   std::atomic<int> n_fallback{0}, n_deflate{0}, n_noise{0};
   size_t svd_dws = 0, svd_hws = 0;
   int lwork_geqrf = 0, lwork_ungqr = 0;
-  cudaStream_t st2 = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t st2 = nullptr, st1 = nullptr;  // top / bottom sweep streams (non-blocking)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join1 = nullptr;
   bool primal_valid = false;
   double work_primal = 0, work_apply = 0;
   std::atomic<double> work_counter{0.0};
@@ -379,8 +379,10 @@ struct Engine {
       svd_method = v == "gesvdj" ? 0 : v == "gesvd" ? 2 : v == "gesvdp" ? 1 : 3;
     }
     TN_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+    TN_CUDA(cudaStreamCreateWithFlags(&st1, cudaStreamNonBlocking));
     TN_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     TN_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    TN_CUDA(cudaEventCreateWithFlags(&ev_join1, cudaEventDisableTiming));
     for (Solver& so : sol) {
       TN_SOLVER(cusolverDnCreate(&so.h));
       TN_SOLVER(cusolverDnCreateParams(&so.prm));
@@ -459,7 +461,9 @@ struct Engine {
     }
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
+    if (ev_join1) cudaEventDestroy(ev_join1);
     if (st2) cudaStreamDestroy(st2);
+    if (st1) cudaStreamDestroy(st1);
     if (arena) cudaFree(arena);
     if (ref) cudaFree(ref);
   }
@@ -854,10 +858,14 @@ struct Engine {
         top_err = std::current_exception();
       }
     });
+    // bottom sweep on its own non-blocking stream as well: the caller's stream
+    // may be the legacy default stream, which serialises with blocking work
+    TN_CUDA(cudaStreamWaitEvent(st1, ev_fork, 0));
     try {
       if (!serial) {
-        Mps BD = primal_side(st, sol[0], pool, false, true, info, dg);
-        for (cplx*& p : BD.a) ddel(p, st);
+        Pool pool1(st1);
+        Mps BD = primal_side(st1, sol[0], pool1, false, true, info, dg);
+        for (cplx*& p : BD.a) ddel(p, st1);
       }
     } catch (...) {
       th.join();
@@ -867,6 +875,8 @@ struct Engine {
     if (top_err) std::rethrow_exception(top_err);
     TN_CUDA(cudaEventRecord(ev_join, st2));
     TN_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
+    TN_CUDA(cudaEventRecord(ev_join1, st1));
+    TN_CUDA(cudaStreamWaitEvent(st, ev_join1, 0));
     combine_diag(st, at<double>(o_diag), dg);
     // T = <<T_0|B_0>>  (Alg. 1)
     cplx* T11 = overlap(st, pool, snap_ptrs(top, D), top.snap[D].p, snap_ptrs(bot, 0), bot.snap[0].p);
