@@ -192,11 +192,11 @@ def main():
             dist.destroy_process_group()
         return
     from paper_2604_20384_b200 import _native as N
-    from paper_2604_20384_b200.api import HVPEngine
+    from paper_2604_20384_b200.api import SUB_BATCH, HVPEngine
 
     dev = torch.device("cuda", torch.cuda.current_device())
     B = args.batch or cfg.batch
-    mb = args.max_batch or {1: 1, 2: 16, 3: 64, 4: 32, 5: 1}[cfg.cid]
+    mb = args.max_batch or SUB_BATCH[cfg.cid]
     K = C.num_gates(cfg.n, cfg.depth, cfg.first_offset)
     ref = C.reference_mpo(cfg, device=dev)
     Gnp = C.haar_gates(cfg.cid, K)

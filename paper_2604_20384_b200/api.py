@@ -9,6 +9,11 @@ import torch
 
 from . import _native as N
 
+# Directions per tn_hvp_apply sub-batch at the five BASELINE.json configs (the
+# launch configuration bench.py times and the full-size GPU tests use): the
+# largest that keeps the tangent caches within HBM with the GEMM grids full.
+SUB_BATCH = {1: 1, 2: 16, 3: 64, 4: 32, 5: 1}
+
 
 def _require_cuda(t: torch.Tensor, name: str):
     if not (t.is_cuda and t.dtype == torch.complex128 and t.is_contiguous()):

@@ -92,21 +92,21 @@ def _layer_sites(cfg):
     return layers(cfg.n, cfg.depth, cfg.first_offset)
 
 
-@pytest.mark.parametrize("cid", [3])
+@pytest.mark.parametrize("cid", [3, 4])
 def test_full_size_properties(cid):
-    """Properties that hold at any size, at the bench's full config and launch
-    configuration: per-layer Euler identity of E (X9), grad_R and Hess_R in the
-    tangent space, Hess_R real-linear in V, results independent of the
-    direction's position in the batch (bitwise)."""
+    """Properties that hold at any size, at the full config and in the launch
+    configuration bench.py times (cfg.batch directions in SUB_BATCH sub-batches):
+    per-layer Euler identity of E (X9), grad_R and Hess_R in the tangent space,
+    Hess_R real-linear in V, results independent of the direction's position in
+    the batch (bitwise)."""
     cfg = C.CONFIGS[cid]
-    from paper_2604_20384_b200.api import HVPEngine, riemannian_project
-    from tn_inputs.reference import reference_mpo as _ref
+    from paper_2604_20384_b200.api import SUB_BATCH, HVPEngine, riemannian_project
     dev = torch.device("cuda")
     ref = C.reference_mpo(cfg, device=dev)
     K = C.num_gates(cfg.n, cfg.depth)
     G = C.haar_gates(cfg.cid, K)
     V = C.tangent_directions(cfg.cid, G, cfg.batch)
-    eng = HVPEngine(cfg.n, cfg.depth, cfg.chi, ref, max_batch=cfg.batch)
+    eng = HVPEngine(cfg.n, cfg.depth, cfg.chi, ref, max_batch=SUB_BATCH[cid])
     Gt = torch.tensor(G, device=dev)
     sc, gR = eng.environments(Gt)
     E = eng.gradient_T().cpu().numpy()
@@ -124,6 +124,32 @@ def test_full_size_properties(cid):
     assert rel(Hc[1], H[1]) < 1e-13                     # other batch size (split-K choices may differ)
     Hr = eng.apply(torch.flip(Vt, [0]).contiguous()).cpu().numpy()[::-1]
     assert np.array_equal(Hr, H)                        # same batch size, reversed order: bitwise
+    eng.close()
+
+
+def test_full_size_properties_config5():
+    """Config 5 (n=128, D=24, chi=256) at a trust-region starting point (X17),
+    max_batch 1 as in truncated CG: the identities of test_full_size_properties
+    (Euler per layer, tangency, real linearity)."""
+    cfg = C.CONFIGS[5]
+    from paper_2604_20384_b200.api import HVPEngine, riemannian_project
+    dev = torch.device("cuda")
+    ref = C.reference_mpo(cfg, device=dev)
+    G = C.trotter_init_gates(cfg, 0)
+    V = C.tangent_directions(cfg.cid, G, 2)
+    eng = HVPEngine(cfg.n, cfg.depth, cfg.chi, ref, max_batch=1)
+    Gt = torch.tensor(G, device=dev)
+    sc, gR = eng.environments(Gt)
+    assert np.isfinite(sc.cpu().numpy()[:6]).all()
+    E = eng.gradient_T().cpu().numpy()
+    for ly in _layer_sites(cfg):
+        vals = np.array([np.sum(G[k] * E[k]) for k, _ in ly])
+        assert np.abs(vals - vals[0]).max() <= 1e-11 * np.abs(vals[0])
+    assert rel(riemannian_project(Gt, gR).cpu().numpy(), gR.cpu().numpy()) < 1e-13
+    comb = np.stack([V[0], V[1], V[0] + 3.0 * V[1]])
+    H = eng.apply(torch.tensor(comb, device=dev)).cpu().numpy()
+    assert rel(riemannian_project(Gt, torch.tensor(H, device=dev)).cpu().numpy(), H) < 1e-13
+    assert rel(H[2], H[0] + 3.0 * H[1]) < 1e-11
     eng.close()
 
 
