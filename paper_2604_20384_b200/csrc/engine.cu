@@ -18,6 +18,10 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
+#include <numeric>
 #include <cstdlib>
 #include <exception>
 #include <thread>
@@ -144,7 +148,9 @@ struct Engine {
   size_t svd_dws = 0, svd_hws = 0;
   int lwork_geqrf = 0, lwork_ungqr = 0;
   cudaStream_t st2 = nullptr, st1 = nullptr;  // top / bottom sweep streams (non-blocking)
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join1 = nullptr;
+  cudaStream_t stg = nullptr;                 // layer gradients, overlapped with the sweeps
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join1 = nullptr, ev_joing = nullptr;
+  std::vector<cudaEvent_t> ev_snap[2];        // per side: layer snapshot idx is in the arena
   bool primal_valid = false;
   double work_primal = 0, work_apply = 0;
   std::atomic<double> work_counter{0.0};
@@ -383,6 +389,12 @@ struct Engine {
     TN_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     TN_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     TN_CUDA(cudaEventCreateWithFlags(&ev_join1, cudaEventDisableTiming));
+    TN_CUDA(cudaStreamCreateWithFlags(&stg, cudaStreamNonBlocking));
+    TN_CUDA(cudaEventCreateWithFlags(&ev_joing, cudaEventDisableTiming));
+    for (auto& v : ev_snap) {
+      v.assign(D + 1, nullptr);
+      for (auto& e : v) TN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     for (Solver& so : sol) {
       TN_SOLVER(cusolverDnCreate(&so.h));
       TN_SOLVER(cusolverDnCreateParams(&so.prm));
@@ -462,6 +474,11 @@ struct Engine {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (ev_join1) cudaEventDestroy(ev_join1);
+    if (ev_joing) cudaEventDestroy(ev_joing);
+    for (auto& v : ev_snap)
+      for (auto& e : v)
+        if (e) cudaEventDestroy(e);
+    if (stg) cudaStreamDestroy(stg);
     if (st2) cudaStreamDestroy(st2);
     if (st1) cudaStreamDestroy(st1);
     if (arena) cudaFree(arena);
@@ -625,7 +642,9 @@ struct Engine {
 
   // Runs one side's primal sweep.  store: write snapshots / replay data to the arena.
   // Returns the final MPS (pool-owned) -- the top side's T_0.
-  Mps primal_side(cudaStream_t st, Solver& so, Pool& pool, bool is_top, bool store, int* info, double* diag) {
+  // on_snap(idx): called after layer snapshot idx has been enqueued on st
+  Mps primal_side(cudaStream_t st, Solver& so, Pool& pool, bool is_top, bool store, int* info, double* diag,
+                  const std::function<void(int)>& on_snap = nullptr) {
     SidePlan& sp = is_top ? top : bot;
     const cplx* G = is_top ? at(o_gdag) : at(o_gates);
     Mps P;
@@ -644,6 +663,7 @@ struct Engine {
     }
     for (size_t li = 0; li < sp.steps.size(); ++li) {
       if (store) snapshot(st, P, sp.o_snap[li]);
+      if (on_snap) on_snap((int)li);
       for (const Step& s : sp.steps[li]) {
         Pool tmp(st);  // step temporaries
         if (s.type == MOVE_R) {
@@ -770,6 +790,7 @@ struct Engine {
       }
     }
     if (store) snapshot(st, P, sp.o_snap.back());
+    if (on_snap) on_snap((int)sp.steps.size());
     return P;
   }
 
@@ -835,53 +856,106 @@ struct Engine {
     double* dg = (double*)pool.raw(16 * sizeof(double));
     double hdiag[16] = {0, 1.0, 0, 0, 0, 0, 0, 0, 0, 1.0, 0, 0, 0, 0, 0, 0};
     TN_CUDA(cudaMemcpyAsync(dg, hdiag, sizeof(hdiag), cudaMemcpyHostToDevice, st));
-    // fork: the top sweep runs on st2 from a second host thread (cuSOLVER's
-    // Xgesvdp returns to the host per call, so two threads keep both in flight)
+    // fork: the top sweep runs on st2 from a second host thread (the split
+    // decisions return to the host per step, so two threads keep both in
+    // flight), the bottom sweep on st1 from this thread, and a third thread
+    // issues the layer gradients of layer ell on stg as soon as both of its
+    // snapshots (B_{ell-1}, T_ell) are enqueued: layers near the middle are
+    // ready halfway through the sweeps, so their GEMMs overlap the eigensolves.
     TN_CUDA(cudaEventRecord(ev_fork, st));
     TN_CUDA(cudaStreamWaitEvent(st2, ev_fork, 0));
-    std::exception_ptr top_err;
+    TN_CUDA(cudaStreamWaitEvent(st1, ev_fork, 0));
+    TN_CUDA(cudaStreamWaitEvent(stg, ev_fork, 0));
     const bool serial = std::getenv("TN_SERIAL_PRIMAL") != nullptr;
-    if (serial) {  // diagnostic: bottom then top on the caller's stream
+    if (serial) {  // diagnostic: bottom, top, then gradients on the caller's stream
       Mps BD = primal_side(st, sol[0], pool, false, true, info, dg);
       for (cplx*& p : BD.a) ddel(p, st);
       Mps T0 = primal_side(st, sol[0], pool, true, true, info + 2, dg + 8);
       for (cplx*& p : T0.a) ddel(p, st);
-    }
-    std::thread th([&] {
-      if (serial) return;
+      layer_gradients(st);
+    } else {
+      std::mutex mu;
+      std::condition_variable cv;
+      int ready[2] = {0, 0};  // snapshots enqueued per side (0 bottom, 1 top)
+      bool abort = false;
+      auto publisher = [&](int side, cudaStream_t s) {
+        return std::function<void(int)>([&, side, s](int idx) {
+          TN_CUDA(cudaEventRecord(ev_snap[side][idx], s));
+          {
+            std::lock_guard<std::mutex> g(mu);
+            ready[side] = idx + 1;
+          }
+          cv.notify_all();
+        });
+      };
+      auto fail = [&] {
+        {
+          std::lock_guard<std::mutex> g(mu);
+          abort = true;
+        }
+        cv.notify_all();
+      };
+      std::exception_ptr top_err, grad_err;
+      std::thread th([&] {
+        try {
+          TN_CUDA(cudaSetDevice(device));
+          Pool pool2(st2);
+          Mps T0 = primal_side(st2, sol[1], pool2, true, true, info + 2, dg + 8, publisher(1, st2));
+          for (cplx*& p : T0.a) ddel(p, st2);
+        } catch (...) {
+          top_err = std::current_exception();
+          fail();
+        }
+      });
+      std::thread tg([&] {
+        try {
+          TN_CUDA(cudaSetDevice(device));
+          TN_CUDA(cudaMemsetAsync(at(o_E), 0, (size_t)K * 16 * sizeof(cplx), stg));
+          std::vector<int> order(D);
+          std::iota(order.begin(), order.end(), 1);
+          std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+            return std::max(a - 1, D - a) < std::max(b - 1, D - b);
+          });
+          for (int ell : order) {
+            {
+              std::unique_lock<std::mutex> lk(mu);
+              cv.wait(lk, [&] { return abort || (ready[0] > ell - 1 && ready[1] > D - ell); });
+              if (abort) return;
+            }
+            TN_CUDA(cudaStreamWaitEvent(stg, ev_snap[0][ell - 1], 0));
+            TN_CUDA(cudaStreamWaitEvent(stg, ev_snap[1][D - ell], 0));
+            layer_gradient(stg, ell);
+          }
+        } catch (...) {
+          grad_err = std::current_exception();
+          fail();
+        }
+      });
       try {
-        TN_CUDA(cudaSetDevice(device));
-        Pool pool2(st2);
-        Mps T0 = primal_side(st2, sol[1], pool2, true, true, info + 2, dg + 8);
-        for (cplx*& p : T0.a) ddel(p, st2);
-      } catch (...) {
-        top_err = std::current_exception();
-      }
-    });
-    // bottom sweep on its own non-blocking stream as well: the caller's stream
-    // may be the legacy default stream, which serialises with blocking work
-    TN_CUDA(cudaStreamWaitEvent(st1, ev_fork, 0));
-    try {
-      if (!serial) {
         Pool pool1(st1);
-        Mps BD = primal_side(st1, sol[0], pool1, false, true, info, dg);
+        Mps BD = primal_side(st1, sol[0], pool1, false, true, info, dg, publisher(0, st1));
         for (cplx*& p : BD.a) ddel(p, st1);
+      } catch (...) {
+        fail();
+        th.join();
+        tg.join();
+        throw;
       }
-    } catch (...) {
       th.join();
-      throw;
+      tg.join();
+      if (top_err) std::rethrow_exception(top_err);
+      if (grad_err) std::rethrow_exception(grad_err);
+      TN_CUDA(cudaEventRecord(ev_join, st2));
+      TN_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
+      TN_CUDA(cudaEventRecord(ev_join1, st1));
+      TN_CUDA(cudaStreamWaitEvent(st, ev_join1, 0));
+      TN_CUDA(cudaEventRecord(ev_joing, stg));
+      TN_CUDA(cudaStreamWaitEvent(st, ev_joing, 0));
     }
-    th.join();
-    if (top_err) std::rethrow_exception(top_err);
-    TN_CUDA(cudaEventRecord(ev_join, st2));
-    TN_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
-    TN_CUDA(cudaEventRecord(ev_join1, st1));
-    TN_CUDA(cudaStreamWaitEvent(st, ev_join1, 0));
     combine_diag(st, at<double>(o_diag), dg);
     // T = <<T_0|B_0>>  (Alg. 1)
     cplx* T11 = overlap(st, pool, snap_ptrs(top, D), top.snap[D].p, snap_ptrs(bot, 0), bot.snap[0].p);
     finish_cost(st, at<double>(o_scal), T11);
-    layer_gradients(st);
     gradient_post(st, K, at(o_gates), at(o_E), at<double>(o_scal), at(o_gradf), grad_R);
     // host copies: scalars/diag, frozen s, solver info
     for (SidePlan* sp : {&bot, &top})
@@ -921,7 +995,12 @@ struct Engine {
   // a4: per layer right sweep, left sweep with E_k (primal envs stored for apply)
   void layer_gradients(cudaStream_t st) {
     TN_CUDA(cudaMemsetAsync(at(o_E), 0, (size_t)K * 16 * sizeof(cplx), st));
-    for (int ell = 1; ell <= D; ++ell) {
+    for (int ell = 1; ell <= D; ++ell) layer_gradient(st, ell);
+  }
+
+  // layer ell's environments o_L/o_R and its gates' E_k (disjoint per layer)
+  void layer_gradient(cudaStream_t st, int ell) {
+    {
       const auto tp = snap_ptrs(top, D - ell);
       const auto bp = snap_ptrs(bot, ell - 1);
       const auto& tb = top.snap[D - ell].p;

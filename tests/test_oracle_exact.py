@@ -10,8 +10,8 @@ from scipy.linalg import expm
 
 from oracle import common as cm
 from oracle import dense as O
+from oracle import spectrum as S
 from tn_inputs import configs as C
-from tn_inputs.models import PAULI
 from tn_inputs.reference import mpo_to_dense_operator, reference_mpo
 
 
@@ -218,27 +218,19 @@ def test_geodesic_derivatives():
 
 
 def pauli_basis(G):
-    """{i G (P_a (x) P_b)/2} per gate, orthonormal."""
-    out = []
-    for k in range(G.shape[0]):
-        for a in range(4):
-            for b in range(4):
-                E = np.zeros_like(G)
-                E[k] = 1j * G[k] @ np.kron(PAULI[a], PAULI[b]) / 2
-                out.append(E)
-    return out
+    return list(S.pauli_basis(G))
 
 
 def dense_riemannian_hessian(n, sites, G, U):
+    """(H_R)_ij = <B_i, H_R[B_j]> from the exact O1 HVP (oracle.spectrum)."""
     T, E, _ = O.alg1(n, sites, G, U)
     _, grad_f, _ = cm.postprocess_gradient(T, E)
-    basis = pauli_basis(G)
-    cols = []
-    for Ej in basis:
-        _, _, H = O.alg1(n, sites, G, U, Ej)
-        Hf, _ = cm.postprocess_hvp(T, E, H, Ej)
-        cols.append(cm.riemannian_hvp(G, grad_f, Hf, Ej))
-    return np.array([[cm.inner(Ei, c) for c in cols] for Ei in basis])
+
+    def hvp(V):
+        _, _, H = O.alg1(n, sites, G, U, V)
+        Hf, _ = cm.postprocess_hvp(T, E, H, V)
+        return cm.riemannian_hvp(G, grad_f, Hf, V)
+    return S.hessian_matrix(S.pauli_basis(G), hvp)
 
 
 def test_pauli_basis_orthonormal_and_dense_hessian_symmetric():
