@@ -126,6 +126,31 @@ tn_status tn_retract(int32_t K, const void* gates, const void* xi, double alpha,
 tn_status tn_tangent_dot(int64_t n, int32_t batch, const void* A, const void* B, void* out, void* stream);
 tn_status tn_tangent_axpby(int64_t n, const double* a, const void* x, const double* b, void* y, void* stream);
 
+/* ---- N3: Hessian spectrum in the Pauli tangent basis (
+ * PAPER.md:1161-1190, App. "Spectral analysis") --------------------------------
+ * Basis: B_{16k+4a+b} = (0, .., i G_k (P_a (x) P_b)/2, .., 0),
+ * 16K vectors, orthonormal under <A,B> = Re sum_k Tr(A_k^dag B_k); P_a in
+ * {I, X, Y, Z}, 4x4 index 2 q_i + q_{i+1}.  With it, column j of the matrix
+ * (H_R)_ij = <B_i, H_R[B_j]> is pauli_coords(tn_hvp_apply(B_j)).
+ *
+ * tn_pauli_basis: writes basis vectors first .. first+count-1 to out
+ *   (DEVICE complex128 [count][K][4][4]); gates DEVICE [K][4][4].
+ *   TN_EINVAL if first < 0, count < 0 or first + count > 16 K.
+ * tn_pauli_coords: out[j][i] = <B_i, X_j> for i < 16K (DEVICE double
+ *   [count][16K]); X DEVICE complex128 [count][K][4][4].  Filling the rows j of
+ *   a [16K][16K] buffer with the coordinates of H_R[B_j] stores H_R^T
+ *   row-major (= H_R column-major).
+ * tn_sym_eig: A (DEVICE double [n][n], overwritten) -> w (DEVICE double [n]),
+ *   the eigenvalues of the symmetric part (A + A^T)/2 in ascending order
+ *   (reading X19: the truncated HVP is only approximately self-adjoint);
+ *   asym (DEVICE double [2]) = (||A - A^T||_F, ||A||_F) of the input.  With
+ *   vectors = 1 the orthonormal eigenvectors overwrite A (row i = vector i);
+ *   else A holds workspace garbage.  cuSOLVER syevd; synchronises the stream
+ *   (host-visible info); TN_ENUMERIC if it does not converge. */
+tn_status tn_pauli_basis(int32_t K, int64_t first, int32_t count, const void* gates, void* out, void* stream);
+tn_status tn_pauli_coords(int32_t K, int32_t count, const void* gates, const void* X, void* out, void* stream);
+tn_status tn_sym_eig(int32_t n, void* A, void* w, void* asym, int32_t vectors, void* stream);
+
 /* Copy the primal store to (into_ctx = 0) or from (into_ctx = 1) a caller
  * DEVICE buffer of exactly tn_hvp_primal_blob's size (broadcast support). */
 tn_status tn_hvp_primal_copy(tn_hvp_ctx* ctx, void* buf, size_t bytes, int32_t into_ctx, void* stream);

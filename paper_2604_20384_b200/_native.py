@@ -17,7 +17,8 @@ STATUS = {0: "TN_OK", 1: "TN_EINVAL", 2: "TN_ENOMEM", 3: "TN_ECUDA", 4: "TN_ENUM
 EXPORTS = ["tn_hvp_num_gates", "tn_hvp_setup", "tn_hvp_environments", "tn_hvp_apply", "tn_hvp_gradient_T",
            "tn_hvp_cost", "tn_hvp_primal_blob", "tn_hvp_primal_imported", "tn_riemannian_project", "tn_zgemm",
            "tn_hvp_work", "tn_retract", "tn_tangent_dot", "tn_tangent_axpby", "tn_hvp_primal_copy",
-           "tn_hvp_launch_count", "tn_gemm_profile", "tn_hvp_destroy", "tn_hvp_last_error"]
+           "tn_hvp_launch_count", "tn_gemm_profile", "tn_pauli_basis", "tn_pauli_coords", "tn_sym_eig",
+           "tn_hvp_destroy", "tn_hvp_last_error"]
 
 
 class TNError(RuntimeError):
@@ -58,7 +59,11 @@ def lib():
         L.tn_tangent_dot.argtypes = [i64, i32, vp, vp, vp, vp]
         L.tn_tangent_axpby.argtypes = [i64, C.POINTER(C.c_double), vp, C.POINTER(C.c_double), vp, vp]
         L.tn_hvp_primal_copy.argtypes = [vp, vp, C.c_size_t, i32, vp]
-        for name in ("tn_retract", "tn_tangent_dot", "tn_tangent_axpby", "tn_hvp_primal_copy"):
+        L.tn_pauli_basis.argtypes = [i32, i64, i32, vp, vp, vp]
+        L.tn_pauli_coords.argtypes = [i32, i32, vp, vp, vp, vp]
+        L.tn_sym_eig.argtypes = [i32, vp, vp, vp, i32, vp]
+        for name in ("tn_retract", "tn_tangent_dot", "tn_tangent_axpby", "tn_hvp_primal_copy", "tn_pauli_basis",
+                     "tn_pauli_coords", "tn_sym_eig"):
             getattr(L, name).restype = C.c_int
         L.tn_hvp_launch_count.argtypes = []
         L.tn_hvp_launch_count.restype = C.c_int64
@@ -171,3 +176,17 @@ def tn_gemm_profile(mode):
 
 def tn_hvp_destroy(ctx):
     lib().tn_hvp_destroy(ctx)
+
+
+def tn_pauli_basis(K, first, count, gates_ptr, out_ptr, stream):
+    check(lib().tn_pauli_basis(K, first, count, C.c_void_p(gates_ptr), C.c_void_p(out_ptr), C.c_void_p(stream)))
+
+
+def tn_pauli_coords(K, count, gates_ptr, X_ptr, out_ptr, stream):
+    check(lib().tn_pauli_coords(K, count, C.c_void_p(gates_ptr), C.c_void_p(X_ptr), C.c_void_p(out_ptr),
+                                C.c_void_p(stream)))
+
+
+def tn_sym_eig(n, A_ptr, w_ptr, asym_ptr, vectors, stream):
+    check(lib().tn_sym_eig(n, C.c_void_p(A_ptr), C.c_void_p(w_ptr), C.c_void_p(asym_ptr), int(vectors),
+                           C.c_void_p(stream)))

@@ -165,3 +165,36 @@ def primal_import(eng: "HVPEngine", buf: torch.Tensor, gates: torch.Tensor):
     """Fill the primal store from a buffer produced by primal_export (same shapes)."""
     N.tn_hvp_primal_copy(eng.ctx, buf.data_ptr(), buf.numel(), 1, _stream())
     eng.primal_imported(gates)
+
+
+def pauli_basis(gates: torch.Tensor, first: int, count: int) -> torch.Tensor:
+    """Pauli tangent basis vectors first..first+count-1 -> [count, K, 4, 4] (tn_pauli_basis)."""
+    _require_cuda(gates, "gates")
+    K = gates.shape[0]
+    out = torch.empty((count, K, 4, 4), dtype=torch.complex128, device=gates.device)
+    N.tn_pauli_basis(K, first, count, gates.data_ptr(), out.data_ptr(), _stream())
+    return out
+
+
+def pauli_coords(gates: torch.Tensor, X: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """<B_i, X_j> for every basis vector -> float64 [count, 16K] (tn_pauli_coords)."""
+    _require_cuda(gates, "gates")
+    _require_cuda(X, "X")
+    K = gates.shape[0]
+    X = X.reshape(-1, K, 4, 4)
+    if out is None:
+        out = torch.empty((X.shape[0], 16 * K), dtype=torch.float64, device=gates.device)
+    N.tn_pauli_coords(K, X.shape[0], gates.data_ptr(), X.data_ptr(), out.data_ptr(), _stream())
+    return out
+
+
+def sym_eig(A: torch.Tensor, vectors: bool = False):
+    """Eigenvalues (ascending) of the symmetric part of A (overwritten), the
+    asymmetry (||A - A^T||_F, ||A||_F), and with vectors=True the eigenvectors
+    as rows of A (tn_sym_eig)."""
+    _require_cuda(A, "A")
+    n = A.shape[0]
+    w = torch.empty(n, dtype=torch.float64, device=A.device)
+    asym = torch.empty(2, dtype=torch.float64, device=A.device)
+    N.tn_sym_eig(n, A.data_ptr(), w.data_ptr(), asym.data_ptr(), vectors, _stream())
+    return (w, asym, A) if vectors else (w, asym)

@@ -18,7 +18,7 @@ LIB = os.path.join(HERE, "libtn_hvp.so")
 BIN = os.path.join(HERE, "bin")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC", "-Xptxas", "-O3"]
-SOURCES = ["zgemm.cu", "kernels.cu", "engine.cu", "abi.cu"]
+SOURCES = ["zgemm.cu", "kernels.cu", "spectrum.cu", "engine.cu", "abi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 

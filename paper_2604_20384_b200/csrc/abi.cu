@@ -166,6 +166,31 @@ tn_status tn_tangent_axpby(int64_t n, const double* a, const void* x, const doub
   });
 }
 
+tn_status tn_pauli_basis(int32_t K, int64_t first, int32_t count, const void* gates, void* out, void* stream) {
+  if (K < 0 || count < 0 || first < 0 || first + count > (int64_t)16 * K)
+    return fail(nullptr, TN_EINVAL, "tn_pauli_basis: need 0 <= first, 0 <= count, first + count <= 16 K");
+  if (K && count && (!gates || !out)) return fail(nullptr, TN_EINVAL, "tn_pauli_basis: null pointer");
+  return guarded(nullptr, [&] {
+    tn::pauli_basis((cudaStream_t)stream, K, first, count, (const tn::cplx*)gates, (tn::cplx*)out);
+  });
+}
+
+tn_status tn_pauli_coords(int32_t K, int32_t count, const void* gates, const void* X, void* out, void* stream) {
+  if (K < 0 || count < 0) return fail(nullptr, TN_EINVAL, "tn_pauli_coords: negative size");
+  if (K && count && (!gates || !X || !out)) return fail(nullptr, TN_EINVAL, "tn_pauli_coords: null pointer");
+  return guarded(nullptr, [&] {
+    tn::pauli_coords((cudaStream_t)stream, K, count, (const tn::cplx*)gates, (const tn::cplx*)X, (double*)out);
+  });
+}
+
+tn_status tn_sym_eig(int32_t n, void* A, void* w, void* asym, int32_t vectors, void* stream) {
+  if (n < 0 || (vectors != 0 && vectors != 1)) return fail(nullptr, TN_EINVAL, "tn_sym_eig: n >= 0, vectors in {0,1}");
+  if (n && (!A || !w || !asym)) return fail(nullptr, TN_EINVAL, "tn_sym_eig: null pointer");
+  return guarded(nullptr, [&] {
+    tn::sym_eig((cudaStream_t)stream, n, (double*)A, (double*)w, (double*)asym, vectors == 1);
+  });
+}
+
 tn_status tn_hvp_primal_copy(tn_hvp_ctx* ctx, void* buf, size_t bytes, int32_t into_ctx, void* stream) {
   if (!ctx || !buf || (into_ctx != 0 && into_ctx != 1)) return fail(ctx, TN_EINVAL, "tn_hvp_primal_copy: bad argument");
   return guarded(ctx, [&] {

@@ -60,3 +60,11 @@ void tangent_dot(cudaStream_t st, int64_t n, int batch, const cplx* A, const cpl
 // scalars[0] = -|T|^2, [1..2] = T from a 1x1 complex env; keeps [3..] untouched.
 void finish_cost(cudaStream_t st, double* scalars, const cplx* T11);
 }  // namespace tn
+
+namespace tn {
+// N3 (spectrum.cu): Pauli tangent basis window, Pauli coordinates of tangent
+// vectors, eigenvalues of the symmetric part of a real n x n matrix.
+void pauli_basis(cudaStream_t st, int K, int64_t first, int count, const cplx* G, cplx* out);
+void pauli_coords(cudaStream_t st, int K, int count, const cplx* G, const cplx* X, double* out);
+void sym_eig(cudaStream_t st, int n, double* A, double* w, double* asym, bool vectors);
+}  // namespace tn

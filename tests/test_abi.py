@@ -45,6 +45,13 @@ def test_invalid_arguments_rejected_without_gpu():
     with pytest.raises(N.TNError) as e:
         N.tn_riemannian_project(-1, 1, 1, 1, 1, 0)
     assert e.value.status == N.TN_EINVAL
+    for call in (lambda: N.tn_pauli_basis(3, 40, 9, 1, 1, 0),     # first + count > 16 K
+                 lambda: N.tn_pauli_basis(3, -1, 1, 1, 1, 0),
+                 lambda: N.tn_pauli_coords(3, 2, 0, 1, 1, 0),     # null gates
+                 lambda: N.tn_sym_eig(4, 1, 1, 1, 2, 0)):         # vectors not in {0, 1}
+        with pytest.raises(N.TNError) as e:
+            call()
+        assert e.value.status == N.TN_EINVAL
 
 
 def test_product_path_has_no_oracle_import():
