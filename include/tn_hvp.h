@@ -99,6 +99,24 @@ tn_status tn_hvp_apply(tn_hvp_ctx* ctx, int32_t batch, const void* dirs, void* h
 /* Euclidean pieces of the last environments call: E [K][4][4] (DEVICE out). */
 tn_status tn_hvp_gradient_T(tn_hvp_ctx* ctx, void* E_out, void* stream);
 
+/* ---- N2: translation-invariant circuits ----
+ * Every gate of layer ell is the layer gate g_ell and directions are
+ * layer-wise constant.  Reading X20 (chain rule,
+ * the equations before Alg. 3): dT/dg_ell = sum_{k in I_ell} dT/dG_k (:1040),
+ * H_T[v]_ell = sum_{k in I_ell} D_v(dT/dG_k) (:1063-1066); f, gradient and HVP
+ * then follow Alg. 2 and App. E on U(4)^D.
+ * tn_hvp_ti_environments: layer_gates DEVICE complex128 [D][4][4] (unitary);
+ *   runs the per-gate primal pass at G_k = g_ell; scalars_out as
+ *   tn_hvp_environments (f, T are the circuit's); grad_R_out DEVICE [D][4][4].
+ *   A layer without gates (n = 2, even layer) gets a zero gradient.
+ *   Invalidates the per-gate state's TI view on the next tn_hvp_environments.
+ * tn_hvp_ti_apply: layer_dirs DEVICE [B][D][4][4] tangent at g; hess_R_out
+ *   DEVICE [B][D][4][4].  TN_ESTATE before tn_hvp_ti_environments (or after a
+ *   later per-gate tn_hvp_environments).  Synchronises the stream. */
+tn_status tn_hvp_ti_environments(tn_hvp_ctx* ctx, const void* layer_gates, void* scalars_out, void* grad_R_out,
+                                 void* stream);
+tn_status tn_hvp_ti_apply(tn_hvp_ctx* ctx, int32_t batch, const void* layer_dirs, void* hess_R_out, void* stream);
+
 /* Cost only (a3, top sweep): T and f at the given gates without touching the
  * stored primal (for the trust-region rho test).  scalars_out as above. */
 tn_status tn_hvp_cost(tn_hvp_ctx* ctx, const void* gates, void* scalars_out, void* stream);

@@ -79,6 +79,20 @@ class HVPEngine:
             return hess, ax[: B * self.K * 16].view(B, self.K, 4, 4), ax[B * self.K * 16:]
         return hess
 
+    def ti_environments(self, layer_gates: torch.Tensor):
+        """Translation-invariant circuit (N2): layer gates [D,4,4] -> (scalars[8], grad_R [D,4,4])."""
+        _require_cuda(layer_gates, "layer_gates")
+        gR = torch.empty(self.depth, 4, 4, dtype=torch.complex128, device=self.device)
+        N.tn_hvp_ti_environments(self.ctx, layer_gates.data_ptr(), self.scalars.data_ptr(), gR.data_ptr(), _stream())
+        return self.scalars, gR
+
+    def ti_apply(self, layer_dirs: torch.Tensor):
+        """Riemannian HVPs on U(4)^D for layer-wise directions [B,D,4,4] -> [B,D,4,4]."""
+        _require_cuda(layer_dirs, "layer_dirs")
+        hess = torch.empty_like(layer_dirs)
+        N.tn_hvp_ti_apply(self.ctx, layer_dirs.shape[0], layer_dirs.data_ptr(), hess.data_ptr(), _stream())
+        return hess
+
     def cost(self, gates: torch.Tensor):
         _require_cuda(gates, "gates")
         sc = torch.zeros(8, dtype=torch.float64, device=self.device)

@@ -108,6 +108,24 @@ tn_status tn_hvp_apply(tn_hvp_ctx* ctx, int32_t batch, const void* dirs, void* h
   });
 }
 
+tn_status tn_hvp_ti_environments(tn_hvp_ctx* ctx, const void* layer_gates, void* scalars_out, void* grad_R_out,
+                                 void* stream) {
+  if (!ctx || !layer_gates || !scalars_out || !grad_R_out)
+    return fail(ctx, TN_EINVAL, "tn_hvp_ti_environments: null argument");
+  return guarded(ctx, [&] {
+    tn::engine_ti_environments(ctx, (const tn::cplx*)layer_gates, (double*)scalars_out, (tn::cplx*)grad_R_out,
+                               (cudaStream_t)stream);
+  });
+}
+
+tn_status tn_hvp_ti_apply(tn_hvp_ctx* ctx, int32_t batch, const void* layer_dirs, void* hess_R_out, void* stream) {
+  if (!ctx || batch < 0 || (batch && (!layer_dirs || !hess_R_out)))
+    return fail(ctx, TN_EINVAL, "tn_hvp_ti_apply: null argument or negative batch");
+  return guarded(ctx, [&] {
+    tn::engine_ti_apply(ctx, batch, (const tn::cplx*)layer_dirs, (tn::cplx*)hess_R_out, (cudaStream_t)stream);
+  });
+}
+
 tn_status tn_hvp_gradient_T(tn_hvp_ctx* ctx, void* E_out, void* stream) {
   if (!ctx || !E_out) return fail(ctx, TN_EINVAL, "tn_hvp_gradient_T: null argument");
   return guarded(ctx, [&] { tn::engine_gradient_T(ctx, (tn::cplx*)E_out, (cudaStream_t)stream); });

@@ -152,6 +152,11 @@ struct Engine {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join1 = nullptr, ev_joing = nullptr;
   std::vector<cudaEvent_t> ev_snap[2];        // per side: layer snapshot idx is in the arena
   bool primal_valid = false;
+  // N2: translation-invariant mode (layer gates), valid after ti_environments
+  int* d_layer_of = nullptr;   // [K] layer index of each gate
+  int* d_layer_start = nullptr;  // [D+1] first gate of each layer
+  cplx* ti_buf = nullptr;      // [3][D][16]: layer gates g, dT/dg, grad_f
+  bool ti_valid = false;
   double work_primal = 0, work_apply = 0;
   std::atomic<double> work_counter{0.0};
   std::string err;
@@ -353,6 +358,18 @@ struct Engine {
     device = c.device;
     TN_CUDA(cudaSetDevice(device));
     build_layers();
+    {
+      std::vector<int> lo, ls(1, 0);
+      for (int ell = 1; ell <= D; ++ell) {
+        for (size_t j = 0; j < layers[ell - 1].size(); ++j) lo.push_back(ell - 1);
+        ls.push_back((int)lo.size());
+      }
+      TN_CUDA(cudaMalloc(&d_layer_of, sizeof(int) * std::max<size_t>(lo.size(), 1)));
+      TN_CUDA(cudaMalloc(&d_layer_start, sizeof(int) * ls.size()));
+      TN_CUDA(cudaMalloc(&ti_buf, sizeof(cplx) * 3 * 16 * std::max(D, 1)));
+      if (!lo.empty()) TN_CUDA(cudaMemcpy(d_layer_of, lo.data(), sizeof(int) * lo.size(), cudaMemcpyHostToDevice));
+      TN_CUDA(cudaMemcpy(d_layer_start, ls.data(), sizeof(int) * ls.size(), cudaMemcpyHostToDevice));
+    }
     ref_bonds.assign(rb, rb + n + 1);
     std::vector<int> ones(n + 1, 1);
     plan_side(bot, ones, false);
@@ -466,6 +483,9 @@ struct Engine {
   }
 
   ~Engine() {
+    if (d_layer_of) cudaFree(d_layer_of);
+    if (d_layer_start) cudaFree(d_layer_start);
+    if (ti_buf) cudaFree(ti_buf);
     for (Solver& so : sol) {
       if (so.svdj) cusolverDnDestroyGesvdjInfo(so.svdj);
       if (so.prm) cusolverDnDestroyParams(so.prm);
@@ -839,9 +859,44 @@ struct Engine {
     return out;
   }
 
+  // N2 (reading X20): the per-gate pass at G_k = g_ell,
+  // then dT/dg_ell = sum_{k in I_ell} E_k and Alg. 2 + App. E on U(4)^D.
+  void ti_environments(cudaStream_t st, const cplx* g, double* scalars, cplx* grad_R) {
+    Pool pool(st);
+    cplx* G = pool.c((int64_t)K * 16);
+    cplx* gR = pool.c((int64_t)K * 16);
+    ti_expand(st, D, K, 1, d_layer_of, g, G);
+    environments(st, G, scalars, gR);
+    cplx *tg = ti_buf, *tE = ti_buf + 16 * D, *tf = ti_buf + 32 * D;
+    TN_CUDA(cudaMemcpyAsync(tg, g, (size_t)D * 16 * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+    ti_reduce(st, D, K, 1, d_layer_start, at(o_E), tE);
+    gradient_post(st, D, tg, tE, at<double>(o_scal), tf, grad_R);
+    TN_CUDA(cudaStreamSynchronize(st));
+    ti_valid = true;
+  }
+
+  // H_T[v]_ell = sum_{k in I_ell} H_T[expand(v)]_k, then Alg. 2 + App. E on U(4)^D
+  void ti_apply(cudaStream_t st, int batch, const cplx* v, cplx* hess) {
+    if (!ti_valid || !primal_valid) throw StateError("tn_hvp_ti_apply before tn_hvp_ti_environments");
+    if (batch == 0) return;
+    Pool pool(st);
+    const int64_t KK = (int64_t)K * 16;
+    cplx* V = pool.c(KK * batch);
+    cplx* H = pool.c(KK * batch);
+    cplx* aux = pool.c(KK * batch + batch);
+    cplx* HT = pool.c((int64_t)D * 16 * batch);
+    cplx* om = pool.c(batch);
+    ti_expand(st, D, K, batch, d_layer_of, v, V);
+    apply(st, batch, V, H, aux);
+    ti_reduce(st, D, K, batch, d_layer_start, aux, HT);
+    hessian_post(st, D, batch, ti_buf, ti_buf + 16 * D, ti_buf + 32 * D, at<double>(o_scal), HT, v, om, hess);
+    TN_CUDA(cudaStreamSynchronize(st));  // pool temporaries are freed on return
+  }
+
   void environments(cudaStream_t st, const cplx* gates, double* scalars, cplx* grad_R) {
     TN_CUDA(cudaSetDevice(device));
     primal_valid = false;
+    ti_valid = false;
     n_fallback = 0;
     n_deflate = 0;
     n_noise = 0;
@@ -1684,6 +1739,12 @@ void engine_environments(tn_hvp_ctx* ctx, const cplx* gates, double* scalars, cp
 }
 void engine_apply(tn_hvp_ctx* ctx, int batch, const cplx* dirs, cplx* hess_R, cplx* aux, cudaStream_t st) {
   ctx->e.apply(st, batch, dirs, hess_R, aux);
+}
+void engine_ti_environments(tn_hvp_ctx* ctx, const cplx* g, double* scalars, cplx* grad_R, cudaStream_t st) {
+  ctx->e.ti_environments(st, g, scalars, grad_R);
+}
+void engine_ti_apply(tn_hvp_ctx* ctx, int batch, const cplx* v, cplx* hess_R, cudaStream_t st) {
+  ctx->e.ti_apply(st, batch, v, hess_R);
 }
 void engine_gradient_T(tn_hvp_ctx* ctx, cplx* E, cudaStream_t st) {
   if (!ctx->e.primal_valid) throw StateError("no primal pass");

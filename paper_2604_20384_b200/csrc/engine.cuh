@@ -15,6 +15,8 @@ tn_hvp_ctx* engine_create(const tn_hvp_config& cfg, const int32_t* ref_bonds, co
 void engine_environments(tn_hvp_ctx* ctx, const cplx* gates, double* scalars, cplx* grad_R, cudaStream_t st);
 void engine_apply(tn_hvp_ctx* ctx, int batch, const cplx* dirs, cplx* hess_R, cplx* aux, cudaStream_t st);
 void engine_gradient_T(tn_hvp_ctx* ctx, cplx* E, cudaStream_t st);
+void engine_ti_environments(tn_hvp_ctx* ctx, const cplx* g, double* scalars, cplx* grad_R, cudaStream_t st);
+void engine_ti_apply(tn_hvp_ctx* ctx, int batch, const cplx* v, cplx* hess_R, cudaStream_t st);
 void engine_cost(tn_hvp_ctx* ctx, const cplx* gates, double* scalars, cudaStream_t st);
 void engine_primal_blob(tn_hvp_ctx* ctx, void** ptr, size_t* bytes);
 void engine_primal_imported(tn_hvp_ctx* ctx, const cplx* gates, cudaStream_t st);

@@ -737,4 +737,47 @@ void finish_cost(cudaStream_t st, double* scalars, const cplx* T11) {
   TN_CUDA(cudaGetLastError());
   count_launch();
 }
+// ---- N2 (translation-invariant circuits) ----
+namespace {
+// dst[b][k] = src[b][layer_of[k]]
+__global__ void ti_expand_kernel(int L, int K, int batch, const int* __restrict__ layer_of,
+                                 const cplx* __restrict__ src, cplx* __restrict__ dst) {
+  const int64_t total = (int64_t)batch * K * 16;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int e = (int)(i & 15);
+    const int64_t bk = i >> 4;
+    const int b = (int)(bk / K), k = (int)(bk % K);
+    dst[i] = src[((int64_t)b * L + layer_of[k]) * 16 + e];
+  }
+}
+// dst[b][l] = sum_{k = start[l]}^{start[l+1]-1} src[b][k], in gate order
+__global__ void ti_reduce_kernel(int L, int K, int batch, const int* __restrict__ start,
+                                 const cplx* __restrict__ src, cplx* __restrict__ dst) {
+  const int64_t total = (int64_t)batch * L * 16;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int e = (int)(i & 15);
+    const int64_t bl = i >> 4;
+    const int b = (int)(bl / L), l = (int)(bl % L);
+    cplx acc = make_double2(0.0, 0.0);
+    for (int k = start[l]; k < start[l + 1]; ++k) acc = cadd(acc, src[((int64_t)b * K + k) * 16 + e]);
+    dst[i] = acc;
+  }
+}
+int ti_grid(int64_t total) { return (int)std::min<int64_t>(std::max<int64_t>((total + 255) / 256, 1), 148 * 8); }
+}  // namespace
+
+void ti_expand(cudaStream_t st, int L, int K, int batch, const int* layer_of, const cplx* src, cplx* dst) {
+  if ((int64_t)batch * K == 0) return;
+  ti_expand_kernel<<<ti_grid((int64_t)batch * K * 16), 256, 0, st>>>(L, K, batch, layer_of, src, dst);
+  TN_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+void ti_reduce(cudaStream_t st, int L, int K, int batch, const int* start, const cplx* src, cplx* dst) {
+  if ((int64_t)batch * L == 0) return;
+  ti_reduce_kernel<<<ti_grid((int64_t)batch * L * 16), 256, 0, st>>>(L, K, batch, start, src, dst);
+  TN_CUDA(cudaGetLastError());
+  count_launch();
+}
+
 }  // namespace tn

@@ -68,3 +68,11 @@ void pauli_basis(cudaStream_t st, int K, int64_t first, int count, const cplx* G
 void pauli_coords(cudaStream_t st, int K, int count, const cplx* G, const cplx* X, double* out);
 void sym_eig(cudaStream_t st, int n, double* A, double* w, double* asym, bool vectors);
 }  // namespace tn
+
+namespace tn {
+// N2 (kernels.cu): tied layer gates.  ti_expand: dst[b][k] = src[b][layer_of[k]]
+// ([batch][L][4][4] -> [batch][K][4][4]); ti_reduce: dst[b][l] = sum of
+// src[b][k] over the layer's contiguous gates start[l] <= k < start[l+1].
+void ti_expand(cudaStream_t st, int L, int K, int batch, const int* layer_of, const cplx* src, cplx* dst);
+void ti_reduce(cudaStream_t st, int L, int K, int batch, const int* start, const cplx* src, cplx* dst);
+}  // namespace tn
