@@ -1055,54 +1055,55 @@ struct Engine {
 
   // layer ell's environments o_L/o_R and its gates' E_k (disjoint per layer)
   void layer_gradient(cudaStream_t st, int ell) {
-    {
-      const auto tp = snap_ptrs(top, D - ell);
-      const auto bp = snap_ptrs(bot, ell - 1);
-      const auto& tb = top.snap[D - ell].p;
-      const auto& bb = bot.snap[ell - 1].p;
-      const auto blks = blocks(ell);
-      TN_CUDA(cudaMemcpyAsync(at(o_L[ell][0]), &ONE, sizeof(cplx), cudaMemcpyHostToDevice, st));
-      TN_CUDA(cudaMemcpyAsync(at(o_R[ell][n]), &ONE, sizeof(cplx), cudaMemcpyHostToDevice, st));
-      // right sweep
-      for (int j = (int)blks.size() - 1; j >= 0; --j) {
-        const int s = blks[j].first, k = blks[j].second;
-        Pool pool(st);  // block temporaries
-        if (k < 0) {
-          cplx* Y = pool.c((int64_t)bb[s] * 4 * tb[s + 1]);
-          nn(st, 4 * bb[s], tb[s + 1], bb[s + 1], bp[s], 0, at(o_R[ell][s + 1]), 0, Y, 0, 1);
-          nc(st, bb[s], tb[s], 4 * tb[s + 1], Y, 0, tp[s], 0, at(o_R[ell][s]), 0, 1);
-        } else {
-          cplx* TB = pool.c((int64_t)16 * bb[s] * bb[s + 2]);
-          pair(st, TB, bp[s], 0, bp[s + 1], 0, bb[s], bb[s + 1], bb[s + 2], 1);
-          cplx* TT = pool.c((int64_t)16 * tb[s] * tb[s + 2]);
-          pair(st, TT, tp[s], 0, tp[s + 1], 0, tb[s], tb[s + 1], tb[s + 2], 1);
-          apply_gate(st, TT, 0, TT, 0, at(o_gdag) + (int64_t)k * 16, 0, tb[s], tb[s + 2], 1, ONE, false);
-          cplx* Y = pool.c((int64_t)16 * bb[s] * tb[s + 2]);
-          nn(st, 16 * bb[s], tb[s + 2], bb[s + 2], TB, 0, at(o_R[ell][s + 2]), 0, Y, 0, 1);
-          nc(st, bb[s], tb[s], 16 * tb[s + 2], Y, 0, TT, 0, at(o_R[ell][s]), 0, 1);
-        }
+    const auto tp = snap_ptrs(top, D - ell);
+    const auto bp = snap_ptrs(bot, ell - 1);
+    const auto& tb = top.snap[D - ell].p;
+    const auto& bb = bot.snap[ell - 1].p;
+    const auto blks = blocks(ell);
+    TN_CUDA(cudaMemcpyAsync(at(o_L[ell][0]), &ONE, sizeof(cplx), cudaMemcpyHostToDevice, st));
+    TN_CUDA(cudaMemcpyAsync(at(o_R[ell][n]), &ONE, sizeof(cplx), cudaMemcpyHostToDevice, st));
+    // two-site blocks of the gate pairs, formed once for both sweeps:
+    // TB[s] = B_s B_{s+1}, TT[s] = T_s T_{s+1} (ungated)
+    Pool lp(st);
+    std::vector<cplx*> TBs(n, nullptr), TTs(n, nullptr);
+    // right sweep
+    for (int j = (int)blks.size() - 1; j >= 0; --j) {
+      const int s = blks[j].first, k = blks[j].second;
+      Pool pool(st);  // block temporaries
+      if (k < 0) {
+        cplx* Y = pool.c((int64_t)bb[s] * 4 * tb[s + 1]);
+        nn(st, 4 * bb[s], tb[s + 1], bb[s + 1], bp[s], 0, at(o_R[ell][s + 1]), 0, Y, 0, 1);
+        nc(st, bb[s], tb[s], 4 * tb[s + 1], Y, 0, tp[s], 0, at(o_R[ell][s]), 0, 1);
+      } else {
+        cplx* TB = TBs[s] = lp.c((int64_t)16 * bb[s] * bb[s + 2]);
+        pair(st, TB, bp[s], 0, bp[s + 1], 0, bb[s], bb[s + 1], bb[s + 2], 1);
+        cplx* TT = TTs[s] = lp.c((int64_t)16 * tb[s] * tb[s + 2]);
+        pair(st, TT, tp[s], 0, tp[s + 1], 0, tb[s], tb[s + 1], tb[s + 2], 1);
+        cplx* TTg = pool.c((int64_t)16 * tb[s] * tb[s + 2]);
+        apply_gate(st, TTg, 0, TT, 0, at(o_gdag) + (int64_t)k * 16, 0, tb[s], tb[s + 2], 1, ONE, false);
+        cplx* Y = pool.c((int64_t)16 * bb[s] * tb[s + 2]);
+        nn(st, 16 * bb[s], tb[s + 2], bb[s + 2], TB, 0, at(o_R[ell][s + 2]), 0, Y, 0, 1);
+        nc(st, bb[s], tb[s], 16 * tb[s + 2], Y, 0, TTg, 0, at(o_R[ell][s]), 0, 1);
       }
-      // left sweep + extraction
-      for (size_t j = 0; j < blks.size(); ++j) {
-        const int s = blks[j].first, k = blks[j].second;
-        Pool pool(st);  // block temporaries
-        if (k < 0) {
-          cplx* Y = pool.c((int64_t)tb[s] * 4 * bb[s + 1]);
-          nn(st, tb[s], 4 * bb[s + 1], bb[s], at(o_L[ell][s]), 0, bp[s], 0, Y, 0, 1);
-          cn(st, tb[s + 1], bb[s + 1], 4 * tb[s], tp[s], 0, Y, 0, at(o_L[ell][s + 1]), 0, 1);
-        } else {
-          cplx* TB = pool.c((int64_t)16 * bb[s] * bb[s + 2]);
-          pair(st, TB, bp[s], 0, bp[s + 1], 0, bb[s], bb[s + 1], bb[s + 2], 1);
-          cplx* TT = pool.c((int64_t)16 * tb[s] * tb[s + 2]);
-          pair(st, TT, tp[s], 0, tp[s + 1], 0, tb[s], tb[s + 1], tb[s + 2], 1);
-          cplx* Y = pool.c((int64_t)16 * tb[s] * bb[s + 2]);
-          nn(st, tb[s], 16 * bb[s + 2], bb[s], at(o_L[ell][s]), 0, TB, 0, Y, 0, 1);
-          cplx* Z = pool.c((int64_t)16 * tb[s] * tb[s + 2]);
-          nn(st, 16 * tb[s], tb[s + 2], bb[s + 2], Y, 0, at(o_R[ell][s + 2]), 0, Z, 0, 1);
-          extract_env(st, at(o_E) + (int64_t)k * 16, 0, TT, 0, Z, 0, tb[s], tb[s + 2], 1, ONE);
-          apply_gate(st, TT, 0, TT, 0, at(o_gdag) + (int64_t)k * 16, 0, tb[s], tb[s + 2], 1, ONE, false);
-          cn(st, tb[s + 2], bb[s + 2], 16 * tb[s], TT, 0, Y, 0, at(o_L[ell][s + 2]), 0, 1);
-        }
+    }
+    // left sweep + extraction
+    for (size_t j = 0; j < blks.size(); ++j) {
+      const int s = blks[j].first, k = blks[j].second;
+      Pool pool(st);  // block temporaries
+      if (k < 0) {
+        cplx* Y = pool.c((int64_t)tb[s] * 4 * bb[s + 1]);
+        nn(st, tb[s], 4 * bb[s + 1], bb[s], at(o_L[ell][s]), 0, bp[s], 0, Y, 0, 1);
+        cn(st, tb[s + 1], bb[s + 1], 4 * tb[s], tp[s], 0, Y, 0, at(o_L[ell][s + 1]), 0, 1);
+      } else {
+        cplx* TB = TBs[s];
+        cplx* TT = TTs[s];
+        cplx* Y = pool.c((int64_t)16 * tb[s] * bb[s + 2]);
+        nn(st, tb[s], 16 * bb[s + 2], bb[s], at(o_L[ell][s]), 0, TB, 0, Y, 0, 1);
+        cplx* Z = pool.c((int64_t)16 * tb[s] * tb[s + 2]);
+        nn(st, 16 * tb[s], tb[s + 2], bb[s + 2], Y, 0, at(o_R[ell][s + 2]), 0, Z, 0, 1);
+        extract_env(st, at(o_E) + (int64_t)k * 16, 0, TT, 0, Z, 0, tb[s], tb[s + 2], 1, ONE);
+        apply_gate(st, TT, 0, TT, 0, at(o_gdag) + (int64_t)k * 16, 0, tb[s], tb[s + 2], 1, ONE, false);
+        cn(st, tb[s + 2], bb[s + 2], 16 * tb[s], TT, 0, Y, 0, at(o_L[ell][s + 2]), 0, 1);
       }
     }
   }
@@ -1321,35 +1322,27 @@ struct Engine {
     return sn;
   }
 
-  // Shared left env sweep: Lout[c] for every block boundary, Lout[0] = 1.
-  // top side tensors (tp, bonds tb) gated per gate block with Gd; bottom (bp, bb).
-  void shared_left(cudaStream_t st, Pool& pool, int ell, std::vector<cplx*>& L, const std::vector<const cplx*>& tp,
-                   const std::vector<int>& tb, const std::vector<const cplx*>& bp, const std::vector<int>& bb) {
+  // Shared (direction-independent) environment sweeps of layer ell over its
+  // blocks: TT[s] / TB[s] = top (already gated with G^dag) / bottom block
+  // tensor starting at site s (two-site pair for a gate block, the site
+  // tensor for an idle site), taken from layer_hvp's block cache.
+  // Left: L[0] = 1, L[e] = TT^H (L[s] TB); right: R[n] = 1, R[s] = (TB R[e]) TT^H.
+  void shared_left(cudaStream_t st, Pool& pool, int ell, std::vector<cplx*>& L, const std::vector<const cplx*>& TT,
+                   const std::vector<int>& tb, const std::vector<const cplx*>& TB, const std::vector<int>& bb) {
     L.assign(n + 1, nullptr);
     L[0] = pool.c(1);
     TN_CUDA(cudaMemcpyAsync(L[0], &ONE, sizeof(cplx), cudaMemcpyHostToDevice, st));
     for (auto [s, k] : blocks(ell)) {
       const int w = k < 0 ? 4 : 16, e = k < 0 ? s + 1 : s + 2;
-      const cplx* TB = bp[s];
-      const cplx* TT = tp[s];
-      if (k >= 0) {
-        cplx* tbk = pool.c((int64_t)16 * bb[s] * bb[e]);
-        pair(st, tbk, bp[s], 0, bp[s + 1], 0, bb[s], bb[s + 1], bb[e], 1);
-        cplx* ttk = pool.c((int64_t)16 * tb[s] * tb[e]);
-        pair(st, ttk, tp[s], 0, tp[s + 1], 0, tb[s], tb[s + 1], tb[e], 1);
-        apply_gate(st, ttk, 0, ttk, 0, at(o_gdag) + (int64_t)k * 16, 0, tb[s], tb[e], 1, ONE, false);
-        TB = tbk;
-        TT = ttk;
-      }
       cplx* Y = pool.c((int64_t)tb[s] * w * bb[e]);
-      nn(st, tb[s], w * bb[e], bb[s], L[s], 0, TB, 0, Y, 0, 1);
+      nn(st, tb[s], w * bb[e], bb[s], L[s], 0, TB[s], 0, Y, 0, 1);
       L[e] = pool.c((int64_t)tb[e] * bb[e]);
-      cn(st, tb[e], bb[e], w * tb[s], TT, 0, Y, 0, L[e], 0, 1);
+      cn(st, tb[e], bb[e], w * tb[s], TT[s], 0, Y, 0, L[e], 0, 1);
     }
   }
 
-  void shared_right(cudaStream_t st, Pool& pool, int ell, std::vector<cplx*>& R, const std::vector<const cplx*>& tp,
-                    const std::vector<int>& tb, const std::vector<const cplx*>& bp, const std::vector<int>& bb) {
+  void shared_right(cudaStream_t st, Pool& pool, int ell, std::vector<cplx*>& R, const std::vector<const cplx*>& TT,
+                    const std::vector<int>& tb, const std::vector<const cplx*>& TB, const std::vector<int>& bb) {
     R.assign(n + 1, nullptr);
     R[n] = pool.c(1);
     TN_CUDA(cudaMemcpyAsync(R[n], &ONE, sizeof(cplx), cudaMemcpyHostToDevice, st));
@@ -1357,21 +1350,10 @@ struct Engine {
     for (int j = (int)blks.size() - 1; j >= 0; --j) {
       const int s = blks[j].first, k = blks[j].second;
       const int w = k < 0 ? 4 : 16, e = k < 0 ? s + 1 : s + 2;
-      const cplx* TB = bp[s];
-      const cplx* TT = tp[s];
-      if (k >= 0) {
-        cplx* tbk = pool.c((int64_t)16 * bb[s] * bb[e]);
-        pair(st, tbk, bp[s], 0, bp[s + 1], 0, bb[s], bb[s + 1], bb[e], 1);
-        cplx* ttk = pool.c((int64_t)16 * tb[s] * tb[e]);
-        pair(st, ttk, tp[s], 0, tp[s + 1], 0, tb[s], tb[s + 1], tb[e], 1);
-        apply_gate(st, ttk, 0, ttk, 0, at(o_gdag) + (int64_t)k * 16, 0, tb[s], tb[e], 1, ONE, false);
-        TB = tbk;
-        TT = ttk;
-      }
       cplx* Y = pool.c((int64_t)bb[s] * w * tb[e]);
-      nn(st, w * bb[s], tb[e], bb[e], TB, 0, R[e], 0, Y, 0, 1);
+      nn(st, w * bb[s], tb[e], bb[e], TB[s], 0, R[e], 0, Y, 0, 1);
       R[s] = pool.c((int64_t)bb[s] * tb[s]);
-      nc(st, bb[s], tb[s], w * tb[e], Y, 0, TT, 0, R[s], 0, 1);
+      nc(st, bb[s], tb[s], w * tb[e], Y, 0, TT[s], 0, R[s], 0, 1);
     }
   }
 
@@ -1390,16 +1372,6 @@ struct Engine {
     std::vector<const cplx*> BAb(DBs.Ab.begin(), DBs.Ab.end()), BAa(DBs.Aa.begin(), DBs.Aa.end());
     std::vector<const cplx*> TAb(DT.Ab.begin(), DT.Ab.end()), TAa(DT.Aa.begin(), DT.Aa.end());
     const int64_t KK = (int64_t)K * 16;
-    // shared chain environments
-    std::vector<cplx*> LBb, RBa, LTb, RTa;
-    if (!skipB) {
-      shared_left(st, pool, ell, LBb, tpv, tb, BAb, xb);
-      shared_right(st, pool, ell, RBa, tpv, tb, BAa, ya);
-    }
-    if (!skipT) {
-      shared_left(st, pool, ell, LTb, TAb, ub, bpv, bb);
-      shared_right(st, pool, ell, RTa, TAa, va, bpv, bb);
-    }
     auto blks = blocks(ell);
     // per-direction right environments at every block boundary
     std::vector<cplx*> dRB(n + 1, nullptr), dRT(n + 1, nullptr), dRV(n + 1, nullptr);
@@ -1472,6 +1444,27 @@ struct Engine {
           q.TBdG = pool.c(sz * nb);
           apply_gate(st, q.TBdG, sz, q.TBd, sz, at(o_gdag) + (int64_t)k * 16, 0, ub[s], va[e], nb, ONE, false);
         }
+      }
+    }
+    // shared chain environments from the cached block tensors
+    std::vector<cplx*> LBb, RBa, LTb, RTa;
+    {
+      std::vector<const cplx*> TTg(n), BAbB(n), BAaB(n), BBs(n), TAbG(n), TAaG(n);
+      for (auto [s, k] : blks) {
+        TTg[s] = bk[s].TTg;
+        BAbB[s] = bk[s].BAbB;
+        BAaB[s] = bk[s].BAaB;
+        BBs[s] = bk[s].BB;
+        TAbG[s] = bk[s].TAbG;
+        TAaG[s] = bk[s].TAaG;
+      }
+      if (!skipB) {
+        shared_left(st, pool, ell, LBb, TTg, tb, BAbB, xb);
+        shared_right(st, pool, ell, RBa, TTg, tb, BAaB, ya);
+      }
+      if (!skipT) {
+        shared_left(st, pool, ell, LTb, TAbG, ub, BBs, bb);
+        shared_right(st, pool, ell, RTa, TAaG, va, BBs, bb);
       }
     }
     const cplx* Vd = V;  // [nb][K][16]
