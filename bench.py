@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--max-batch", type=int, default=None, help="internal sub-batch (memory)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--unfused", action="store_true",
+                    help="time tn_hvp_environments + tn_hvp_apply instead of the fused tn_hvp_step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -207,19 +209,26 @@ def main():
     out = torch.empty_like(V)
 
     def step():
-        eng.environments(G)
-        eng.apply(V, out=out)
+        if args.unfused:
+            eng.environments(G)
+            eng.apply(V, out=out)
+        else:
+            eng.step(G, V, out=out)
 
     for _ in range(max(args.warmup - 1, 0)):
         step()
     torch.cuda.synchronize()
-    # the last warm-up step is instrumented (untimed): GEMM kernel time, work, launches
-    l0 = N.tn_hvp_launch_count()
+    # the last warm-up step is instrumented (untimed) and unfused, so that the
+    # apply phase's GEMMs run alone on one stream: per-launch GEMM time (CUDA
+    # events around every GEMM) and exact complex MACs of each phase
     N.tn_gemm_profile(1)
-    step()
+    eng.environments(G)
+    torch.cuda.synchronize()
+    env_gemm_ms, env_gemm_cmac = N.tn_gemm_profile(0)
+    N.tn_gemm_profile(1)
+    eng.apply(V, out=out)
     torch.cuda.synchronize()
     gemm_ms, gemm_cmac = N.tn_gemm_profile(0)
-    launches = N.tn_hvp_launch_count() - l0
     cmac_dir, cmac_primal = eng.work()
 
     st = torch.cuda.current_stream()
@@ -227,11 +236,13 @@ def main():
     barrier(world)
     torch.cuda.synchronize()
     with Clocks(local) as clk:
+        l0 = N.tn_hvp_launch_count()
         e0.record(st)
         for _ in range(args.steps):
             step()
         e1.record(st)
         torch.cuda.synchronize()
+        launches = N.tn_hvp_launch_count() - l0
     barrier(world)
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
     value = world * B / (ms / 1e3)
@@ -248,8 +259,11 @@ def main():
         def step_e2e():
             Gd.copy_(Gh, non_blocking=True)
             Vd.copy_(Vh, non_blocking=True)
-            sc, _ = eng.environments(Gd)
-            eng.apply(Vd, out=out)
+            if args.unfused:
+                sc, _ = eng.environments(Gd)
+                eng.apply(Vd, out=out)
+            else:
+                sc, _, _ = eng.step(Gd, Vd, out=out)
             Hh.copy_(out, non_blocking=True)
             Sh.copy_(sc, non_blocking=True)
 
@@ -279,17 +293,22 @@ def main():
         "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": cfg.name, "n": cfg.n, "depth": cfg.depth, "chi": cfg.chi, "gates": K,
                    "directions_per_gpu": B, "sub_batch": mb, "parallelism": f"weak x{world} (directions)",
+                   "step": "tn_hvp_environments + tn_hvp_apply" if args.unfused else
+                           "tn_hvp_step (fused: first sub-batch's forward tangents overlap the primal pass)",
                    "l2": "working set (primal store, tangent caches: GBs) > 126 MB L2; no flush"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "kernel": "tn::zgemm3m_kernel (DMMA m8n8k4 f64, 3M: 3 real DMMA per complex k-step; "
                                "algorithmic 8 flop per complex MAC, so frac can exceed 1 up to 4/3)",
                      "peak_source": peak_src,
-                     "gemm_share_of_step": gemm_ms / ms if ms else None,
-                     "flops_per_step": 8 * gemm_cmac, "apply_cmac_per_direction": cmac_dir,
+                     "measured_on": "apply phase of an instrumented unfused warm-up step (GEMMs serialised on "
+                                    "one stream; CUDA events around every GEMM launch)",
+                     "apply_gemm_ms": gemm_ms, "primal_gemm_ms": env_gemm_ms,
+                     "gemm_share_of_step": gemm_ms / ms if ms else None,   # apply-phase GEMM time / step
+                     "flops_per_step": 8 * (gemm_cmac + env_gemm_cmac), "apply_cmac_per_direction": cmac_dir,
                      "primal_cmac": cmac_primal},
         "clocks": clk.summary(),
-        "gpu_launches": int(launches),
+        "gpu_launches": int(launches),      # library kernel launches inside the timed region (all steps)
         "e2e": e2e,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

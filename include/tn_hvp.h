@@ -96,6 +96,17 @@ tn_status tn_hvp_environments(tn_hvp_ctx* ctx, const void* gates, void* scalars_
 tn_status tn_hvp_apply(tn_hvp_ctx* ctx, int32_t batch, const void* dirs, void* hess_R_out, void* aux_out,
                        void* stream);
 
+/* One whole step of the hot path: tn_hvp_environments(gates) followed by
+ * tn_hvp_apply(batch, dirs) with the same arguments, outputs and state
+ * afterwards, bitwise identical results.  Fused: the forward tangents of the
+ * first sub-batch (min(batch, max_batch) directions) are replayed on their own
+ * stream while the top sweep and the layer environments are still running
+ * (the forward tangent of bottom layer l needs only the bottom sweep up to l,
+ * Alg. 1), so their GEMMs fill the SMs during the
+ * latency-bound eigensolves.  batch = 0 is tn_hvp_environments. */
+tn_status tn_hvp_step(tn_hvp_ctx* ctx, const void* gates, void* scalars_out, void* grad_R_out, int32_t batch,
+                      const void* dirs, void* hess_R_out, void* aux_out, void* stream);
+
 /* Euclidean pieces of the last environments call: E [K][4][4] (DEVICE out). */
 tn_status tn_hvp_gradient_T(tn_hvp_ctx* ctx, void* E_out, void* stream);
 

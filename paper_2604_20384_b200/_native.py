@@ -18,7 +18,7 @@ EXPORTS = ["tn_hvp_num_gates", "tn_hvp_setup", "tn_hvp_environments", "tn_hvp_ap
            "tn_hvp_cost", "tn_hvp_primal_blob", "tn_hvp_primal_imported", "tn_riemannian_project", "tn_zgemm",
            "tn_hvp_work", "tn_retract", "tn_tangent_dot", "tn_tangent_axpby", "tn_hvp_primal_copy",
            "tn_hvp_launch_count", "tn_gemm_profile", "tn_pauli_basis", "tn_pauli_coords", "tn_sym_eig",
-           "tn_hvp_ti_environments", "tn_hvp_ti_apply",
+           "tn_hvp_ti_environments", "tn_hvp_ti_apply", "tn_hvp_step",
            "tn_hvp_destroy", "tn_hvp_last_error"]
 
 
@@ -60,13 +60,15 @@ def lib():
         L.tn_tangent_dot.argtypes = [i64, i32, vp, vp, vp, vp]
         L.tn_tangent_axpby.argtypes = [i64, C.POINTER(C.c_double), vp, C.POINTER(C.c_double), vp, vp]
         L.tn_hvp_primal_copy.argtypes = [vp, vp, C.c_size_t, i32, vp]
+        L.tn_hvp_step.argtypes = [vp, vp, vp, vp, i32, vp, vp, vp, vp]
         L.tn_hvp_ti_environments.argtypes = [vp, vp, vp, vp, vp]
         L.tn_hvp_ti_apply.argtypes = [vp, i32, vp, vp, vp]
         L.tn_pauli_basis.argtypes = [i32, i64, i32, vp, vp, vp]
         L.tn_pauli_coords.argtypes = [i32, i32, vp, vp, vp, vp]
         L.tn_sym_eig.argtypes = [i32, vp, vp, vp, i32, vp]
         for name in ("tn_retract", "tn_tangent_dot", "tn_tangent_axpby", "tn_hvp_primal_copy", "tn_pauli_basis",
-                     "tn_pauli_coords", "tn_sym_eig", "tn_hvp_ti_environments", "tn_hvp_ti_apply"):
+                     "tn_pauli_coords", "tn_sym_eig", "tn_hvp_ti_environments", "tn_hvp_ti_apply",
+                     "tn_hvp_step"):
             getattr(L, name).restype = C.c_int
         L.tn_hvp_launch_count.argtypes = []
         L.tn_hvp_launch_count.restype = C.c_int64
@@ -202,3 +204,8 @@ def tn_hvp_ti_environments(ctx, g_ptr, scalars_ptr, grad_R_ptr, stream):
 
 def tn_hvp_ti_apply(ctx, batch, v_ptr, hess_ptr, stream):
     check(lib().tn_hvp_ti_apply(ctx, batch, C.c_void_p(v_ptr), C.c_void_p(hess_ptr), C.c_void_p(stream)), ctx)
+
+
+def tn_hvp_step(ctx, gates_ptr, scalars_ptr, grad_R_ptr, batch, dirs_ptr, hess_ptr, aux_ptr, stream):
+    check(lib().tn_hvp_step(ctx, C.c_void_p(gates_ptr), C.c_void_p(scalars_ptr), C.c_void_p(grad_R_ptr), batch,
+                            C.c_void_p(dirs_ptr), C.c_void_p(hess_ptr), C.c_void_p(aux_ptr), C.c_void_p(stream)), ctx)

@@ -79,6 +79,17 @@ class HVPEngine:
             return hess, ax[: B * self.K * 16].view(B, self.K, 4, 4), ax[B * self.K * 16:]
         return hess
 
+    def step(self, gates: torch.Tensor, dirs: torch.Tensor, out: torch.Tensor | None = None):
+        """environments(gates) + apply(dirs) in one fused call (tn_hvp_step):
+        -> (scalars[8], grad_R [K,4,4], hess [B,K,4,4])."""
+        _require_cuda(gates, "gates")
+        _require_cuda(dirs, "dirs")
+        gR = torch.empty(self.K, 4, 4, dtype=torch.complex128, device=self.device)
+        hess = out if out is not None else torch.empty_like(dirs)
+        N.tn_hvp_step(self.ctx, gates.data_ptr(), self.scalars.data_ptr(), gR.data_ptr(), dirs.shape[0],
+                      dirs.data_ptr(), hess.data_ptr(), 0, _stream())
+        return self.scalars, gR, hess
+
     def ti_environments(self, layer_gates: torch.Tensor):
         """Translation-invariant circuit (N2): layer gates [D,4,4] -> (scalars[8], grad_R [D,4,4])."""
         _require_cuda(layer_gates, "layer_gates")

@@ -126,6 +126,16 @@ tn_status tn_hvp_ti_apply(tn_hvp_ctx* ctx, int32_t batch, const void* layer_dirs
   });
 }
 
+tn_status tn_hvp_step(tn_hvp_ctx* ctx, const void* gates, void* scalars_out, void* grad_R_out, int32_t batch,
+                      const void* dirs, void* hess_R_out, void* aux_out, void* stream) {
+  if (!ctx || !gates || !scalars_out || !grad_R_out || batch < 0 || (batch && (!dirs || !hess_R_out)))
+    return fail(ctx, TN_EINVAL, "tn_hvp_step: null argument or negative batch");
+  return guarded(ctx, [&] {
+    tn::engine_step(ctx, (const tn::cplx*)gates, (double*)scalars_out, (tn::cplx*)grad_R_out, batch,
+                    (const tn::cplx*)dirs, (tn::cplx*)hess_R_out, (tn::cplx*)aux_out, (cudaStream_t)stream);
+  });
+}
+
 tn_status tn_hvp_gradient_T(tn_hvp_ctx* ctx, void* E_out, void* stream) {
   if (!ctx || !E_out) return fail(ctx, TN_EINVAL, "tn_hvp_gradient_T: null argument");
   return guarded(ctx, [&] { tn::engine_gradient_T(ctx, (tn::cplx*)E_out, (cudaStream_t)stream); });

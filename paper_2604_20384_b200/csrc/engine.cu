@@ -117,6 +117,9 @@ struct Pool {  // stream-ordered transient device buffers
 
 }  // namespace
 
+// set on the fused step's forward-tangent thread: its GEMMs count as apply work
+thread_local bool g_fwd_thread = false;
+
 struct Engine {
   tn_hvp_config cfg{};
   int n = 0, D = 0, off = 0, chi = 0, K = 0;
@@ -149,7 +152,8 @@ struct Engine {
   int lwork_geqrf = 0, lwork_ungqr = 0;
   cudaStream_t st2 = nullptr, st1 = nullptr;  // top / bottom sweep streams (non-blocking)
   cudaStream_t stg = nullptr;                 // layer gradients, overlapped with the sweeps
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join1 = nullptr, ev_joing = nullptr;
+  cudaStream_t stf = nullptr, sth = nullptr;  // fused step: forward tangents; host reads of s
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join1 = nullptr, ev_joing = nullptr, ev_joinf = nullptr;
   std::vector<cudaEvent_t> ev_snap[2];        // per side: layer snapshot idx is in the arena
   bool primal_valid = false;
   // N2: translation-invariant mode (layer gates), valid after ti_environments
@@ -157,8 +161,17 @@ struct Engine {
   int* d_layer_start = nullptr;  // [D+1] first gate of each layer
   cplx* ti_buf = nullptr;      // [3][D][16]: layer gates g, dT/dg, grad_f
   bool ti_valid = false;
-  double work_primal = 0, work_apply = 0;
+  struct Tangent {  // channel-form tangents for nb directions
+    std::vector<cplx*> Ab, Aa, B;  // B[s]: nb blocks, direction stride = size(B[s])
+    Bonds bd;                      // bonds: ab / aa used (p = primal)
+  };
+  struct TanSnap {
+    std::vector<cplx*> Ab, Aa, B;
+    Bonds bd;
+  };
+  double work_primal = 0, work_apply = 0, work_fwd_first = 0;
   std::atomic<double> work_counter{0.0};
+  std::atomic<double> work_counter_fwd{0.0};  // GEMMs issued by the fused step's forward-tangent thread
   std::string err;
   int device = 0;
 
@@ -171,7 +184,8 @@ struct Engine {
   void mm(cudaStream_t st, char oa, char ob, int M, int N, int Kd, cplx a, const cplx* A, int64_t lda, int64_t sA,
           const cplx* B, int64_t ldb, int64_t sB, cplx b, cplx* C, int64_t ldc, int64_t sC, int batch) {
     if (M <= 0 || N <= 0 || batch <= 0) return;
-    work_counter.fetch_add((double)M * N * std::max(Kd, 0) * batch, std::memory_order_relaxed);
+    (g_fwd_thread ? work_counter_fwd : work_counter)
+        .fetch_add((double)M * N * std::max(Kd, 0) * batch, std::memory_order_relaxed);
     zgemm(st, oa, ob, M, N, Kd, a, A, lda, sA, B, ldb, sB, b, C, ldc, sC, batch);
   }
   // C(MxN) = a A(MxK) B(KxN) + b C
@@ -407,6 +421,9 @@ struct Engine {
     TN_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     TN_CUDA(cudaEventCreateWithFlags(&ev_join1, cudaEventDisableTiming));
     TN_CUDA(cudaStreamCreateWithFlags(&stg, cudaStreamNonBlocking));
+    TN_CUDA(cudaStreamCreateWithFlags(&stf, cudaStreamNonBlocking));
+    TN_CUDA(cudaStreamCreateWithFlags(&sth, cudaStreamNonBlocking));
+    TN_CUDA(cudaEventCreateWithFlags(&ev_joinf, cudaEventDisableTiming));
     TN_CUDA(cudaEventCreateWithFlags(&ev_joing, cudaEventDisableTiming));
     for (auto& v : ev_snap) {
       v.assign(D + 1, nullptr);
@@ -499,6 +516,9 @@ struct Engine {
       for (auto& e : v)
         if (e) cudaEventDestroy(e);
     if (stg) cudaStreamDestroy(stg);
+    if (stf) cudaStreamDestroy(stf);
+    if (sth) cudaStreamDestroy(sth);
+    if (ev_joinf) cudaEventDestroy(ev_joinf);
     if (st2) cudaStreamDestroy(st2);
     if (st1) cudaStreamDestroy(st1);
     if (arena) cudaFree(arena);
@@ -893,7 +913,10 @@ struct Engine {
     TN_CUDA(cudaStreamSynchronize(st));  // pool temporaries are freed on return
   }
 
-  void environments(cudaStream_t st, const cplx* gates, double* scalars, cplx* grad_R) {
+  // fwd_out (fused step): also replay the forward tangents of fwd_nb directions
+  // fwd_V on stream stf while the sweeps run (see step()).
+  void environments(cudaStream_t st, const cplx* gates, double* scalars, cplx* grad_R, int fwd_nb = 0,
+                    const cplx* fwd_V = nullptr, std::vector<TanSnap>* fwd_out = nullptr) {
     TN_CUDA(cudaSetDevice(device));
     primal_valid = false;
     ti_valid = false;
@@ -986,20 +1009,60 @@ struct Engine {
           fail();
         }
       });
+      std::exception_ptr fwd_err;
+      const double wf0 = work_counter_fwd.load();
+      std::thread tf;
+      if (fwd_out) {
+        TN_CUDA(cudaStreamWaitEvent(stf, ev_fork, 0));
+        tf = std::thread([&] {
+          try {
+            TN_CUDA(cudaSetDevice(device));
+            g_fwd_thread = true;
+            *fwd_out = forward_tangents(stf, fwd_nb, fwd_V, [&](int li) {
+              {  // bottom layer li fully enqueued (its end snapshot published)
+                std::unique_lock<std::mutex> lk(mu);
+                cv.wait(lk, [&] { return abort || ready[0] > li + 1; });
+                if (abort) throw std::runtime_error("fused step: primal pass failed");
+              }
+              TN_CUDA(cudaStreamWaitEvent(stf, ev_snap[0][li + 1], 0));
+              // the layer's frozen s (host scalars of tangent_step), read on a side stream
+              TN_CUDA(cudaStreamWaitEvent(sth, ev_snap[0][li + 1], 0));
+              for (const Step& s : bot.steps[li])
+                if (s.type == PAIR)
+                  TN_CUDA(cudaMemcpyAsync(&h_s[s.s_index], at<double>(s.o_s), sizeof(double),
+                                          cudaMemcpyDeviceToHost, sth));
+              TN_CUDA(cudaStreamSynchronize(sth));
+            });
+          } catch (...) {
+            fwd_err = std::current_exception();
+            fail();
+          }
+          g_fwd_thread = false;
+        });
+      }
+      auto join_all = [&] {
+        th.join();
+        tg.join();
+        if (tf.joinable()) tf.join();
+      };
       try {
         Pool pool1(st1);
         Mps BD = primal_side(st1, sol[0], pool1, false, true, info, dg, publisher(0, st1));
         for (cplx*& p : BD.a) ddel(p, st1);
       } catch (...) {
         fail();
-        th.join();
-        tg.join();
+        join_all();
         throw;
       }
-      th.join();
-      tg.join();
+      join_all();
       if (top_err) std::rethrow_exception(top_err);
       if (grad_err) std::rethrow_exception(grad_err);
+      if (fwd_err) std::rethrow_exception(fwd_err);
+      if (fwd_out) {
+        work_fwd_first = work_counter_fwd.load() - wf0;
+        TN_CUDA(cudaEventRecord(ev_joinf, stf));
+        TN_CUDA(cudaStreamWaitEvent(st, ev_joinf, 0));
+      }
       TN_CUDA(cudaEventRecord(ev_join, st2));
       TN_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
       TN_CUDA(cudaEventRecord(ev_join1, st1));
@@ -1144,10 +1207,6 @@ struct Engine {
   }
 
   // ---------------------------------------------------- tangent pass --
-  struct Tangent {  // channel-form tangents for nb directions
-    std::vector<cplx*> Ab, Aa, B;  // B[s]: nb blocks, direction stride = size(B[s])
-    Bonds bd;                      // bonds: ab / aa used (p = primal)
-  };
 
   int64_t bsize(const Bonds& b, int s) const { return (int64_t)b.ab[s] * 4 * b.aa[s + 1]; }
 
@@ -1297,10 +1356,6 @@ struct Engine {
     }
   }
 
-  struct TanSnap {
-    std::vector<cplx*> Ab, Aa, B;
-    Bonds bd;
-  };
 
   TanSnap take_snapshot(cudaStream_t st, const Tangent& t, int nb) {
     TanSnap sn;
@@ -1633,7 +1688,25 @@ struct Engine {
     ddel(dLT, st);
   }
 
-  void apply(cudaStream_t st, int batch, const cplx* dirs, cplx* hess, cplx* aux) {
+  // a6: forward (bottom) tangents of nb directions, cached per layer: DB[ell-1]
+  // holds DB_{ell-1}.  before_layer(li), when given, runs on the host before
+  // the steps of bottom layer li are issued (fused step: waits for the sweep).
+  std::vector<TanSnap> forward_tangents(cudaStream_t st, int nb, const cplx* V,
+                                        const std::function<void(int)>& before_layer = nullptr) {
+    std::vector<TanSnap> DB(D);
+    Tangent t;
+    tangent_init(st, t, bot, false, nb);
+    for (size_t li = 0; li < bot.steps.size(); ++li) {
+      DB[li] = take_snapshot(st, t, nb);
+      if (before_layer) before_layer((int)li);
+      for (const Step& s : bot.steps[li]) tangent_step(st, t, s, at(o_gates), V, nb);
+    }
+    release(t, st);
+    return DB;
+  }
+
+  void apply(cudaStream_t st, int batch, const cplx* dirs, cplx* hess, cplx* aux,
+             std::vector<TanSnap>* first_fwd = nullptr) {
     TN_CUDA(cudaSetDevice(device));
     if (!primal_valid) throw StateError("tn_hvp_apply before tn_hvp_environments");
     const double wc0 = work_counter.load();
@@ -1652,17 +1725,10 @@ struct Engine {
         for (auto& e : pe) TN_CUDA(cudaEventCreate(&e));
       float t_fwd = 0, t_bwd = 0, t_hvp = 0;
       if (phases) TN_CUDA(cudaEventRecord(pe[0], st));
-      // forward (bottom) tangent, cached per layer: DB_{ell-1}
-      std::vector<TanSnap> DB(D);
-      {
-        Tangent t;
-        tangent_init(st, t, bot, false, nb);
-        for (size_t li = 0; li < bot.steps.size(); ++li) {
-          DB[li] = take_snapshot(st, t, nb);
-          for (const Step& s : bot.steps[li]) tangent_step(st, t, s, at(o_gates), V, nb);
-        }
-        release(t, st);
-      }
+      // forward (bottom) tangent, cached per layer: DB_{ell-1} (precomputed
+      // for the first sub-batch by the fused step)
+      std::vector<TanSnap> DB = (b0 == 0 && first_fwd && !first_fwd->empty()) ? std::move(*first_fwd)
+                                                                               : forward_tangents(st, nb, V);
       if (phases) {
         TN_CUDA(cudaEventRecord(pe[1], st));
         TN_CUDA(cudaEventSynchronize(pe[1]));
@@ -1709,7 +1775,23 @@ struct Engine {
                                 cudaMemcpyDeviceToDevice, st));
       }
     }
-    work_apply = (work_counter.load() - wc0) / std::max(batch, 1);
+    work_apply = (work_counter.load() - wc0 + work_fwd_first) / std::max(batch, 1);
+    work_fwd_first = 0;
+  }
+
+  // Fused step (tn_hvp_step): environments + HVPs of `batch` directions, with
+  // the first sub-batch's forward tangents replayed on a fourth stream while
+  // the top sweep and the layer gradients still run (the forward tangent of
+  // bottom layer li needs only the bottom sweep's replay data up to li).
+  void step(cudaStream_t st, const cplx* gates, double* scalars, cplx* grad_R, int batch, const cplx* dirs,
+            cplx* hess, cplx* aux) {
+    if (batch == 0) {
+      environments(st, gates, scalars, grad_R);
+      return;
+    }
+    std::vector<TanSnap> DB0;
+    environments(st, gates, scalars, grad_R, std::min(batch, cfg.max_batch), dirs, &DB0);
+    apply(st, batch, dirs, hess, aux, &DB0);
   }
 };
 
@@ -1732,6 +1814,10 @@ void engine_environments(tn_hvp_ctx* ctx, const cplx* gates, double* scalars, cp
 }
 void engine_apply(tn_hvp_ctx* ctx, int batch, const cplx* dirs, cplx* hess_R, cplx* aux, cudaStream_t st) {
   ctx->e.apply(st, batch, dirs, hess_R, aux);
+}
+void engine_step(tn_hvp_ctx* ctx, const cplx* gates, double* scalars, cplx* grad_R, int batch, const cplx* dirs,
+                 cplx* hess_R, cplx* aux, cudaStream_t st) {
+  ctx->e.step(st, gates, scalars, grad_R, batch, dirs, hess_R, aux);
 }
 void engine_ti_environments(tn_hvp_ctx* ctx, const cplx* g, double* scalars, cplx* grad_R, cudaStream_t st) {
   ctx->e.ti_environments(st, g, scalars, grad_R);

@@ -14,6 +14,8 @@ struct StateError : std::runtime_error {
 tn_hvp_ctx* engine_create(const tn_hvp_config& cfg, const int32_t* ref_bonds, const void* ref_mpo, cudaStream_t st);
 void engine_environments(tn_hvp_ctx* ctx, const cplx* gates, double* scalars, cplx* grad_R, cudaStream_t st);
 void engine_apply(tn_hvp_ctx* ctx, int batch, const cplx* dirs, cplx* hess_R, cplx* aux, cudaStream_t st);
+void engine_step(tn_hvp_ctx* ctx, const cplx* gates, double* scalars, cplx* grad_R, int batch, const cplx* dirs,
+                 cplx* hess_R, cplx* aux, cudaStream_t st);
 void engine_gradient_T(tn_hvp_ctx* ctx, cplx* E, cudaStream_t st);
 void engine_ti_environments(tn_hvp_ctx* ctx, const cplx* g, double* scalars, cplx* grad_R, cudaStream_t st);
 void engine_ti_apply(tn_hvp_ctx* ctx, int batch, const cplx* v, cplx* hess_R, cudaStream_t st);

@@ -166,3 +166,26 @@ def test_parity_config3_sampled():
     assert abs(g["f"] - o["f"]) <= TOL * abs(o["f"])
     assert rel(g["grad_R"], o["grad_R"]) < TOL
     assert rel(g["HR"][0], o["HR"][0]) < TOL
+
+
+@pytest.mark.parametrize("cid,max_batch", [(2, 8), (3, 64)])
+def test_fused_step_equals_environments_plus_apply(cid, max_batch):
+    """tn_hvp_step (first sub-batch's forward tangents replayed during the
+    primal pass) gives bitwise the results of tn_hvp_environments + tn_hvp_apply."""
+    from paper_2604_20384_b200.api import HVPEngine
+    cfg = C.CONFIGS[cid]
+    dev = torch.device("cuda")
+    ref = C.reference_mpo(cfg, device=dev)
+    K = C.num_gates(cfg.n, cfg.depth)
+    G = torch.tensor(C.haar_gates(cfg.cid, K), device=dev)
+    V = torch.tensor(C.tangent_directions(cfg.cid, G.cpu().numpy(), 16), device=dev)
+    eng = HVPEngine(cfg.n, cfg.depth, cfg.chi, ref, max_batch=max_batch)
+    sc1, gR1 = eng.environments(G)
+    sc1, gR1 = sc1.clone(), gR1.clone()
+    H1 = eng.apply(V)
+    sc2, gR2, H2 = eng.step(G, V)
+    torch.cuda.synchronize()
+    assert torch.equal(sc1[:6], sc2[:6]) and torch.equal(gR1, gR2) and torch.equal(H1, H2)
+    H3 = eng.apply(V)                                  # state after the fused step is the same
+    assert torch.equal(H3, H1)
+    eng.close()
