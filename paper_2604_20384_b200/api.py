@@ -15,9 +15,9 @@ from . import _native as N
 SUB_BATCH = {1: 1, 2: 16, 3: 64, 4: 32, 5: 1}
 
 
-def _require_cuda(t: torch.Tensor, name: str):
-    if not (t.is_cuda and t.dtype == torch.complex128 and t.is_contiguous()):
-        raise ValueError(f"{name}: expected a contiguous complex128 CUDA tensor")
+def _require_cuda(t: torch.Tensor, name: str, dtype=torch.complex128):
+    if not (t.is_cuda and t.dtype == dtype and t.is_contiguous()):
+        raise ValueError(f"{name}: expected a contiguous {dtype} CUDA tensor")
 
 
 def _stream():
@@ -217,7 +217,7 @@ def sym_eig(A: torch.Tensor, vectors: bool = False):
     """Eigenvalues (ascending) of the symmetric part of A (overwritten), the
     asymmetry (||A - A^T||_F, ||A||_F), and with vectors=True the eigenvectors
     as rows of A (tn_sym_eig)."""
-    _require_cuda(A, "A")
+    _require_cuda(A, "A", torch.float64)
     n = A.shape[0]
     w = torch.empty(n, dtype=torch.float64, device=A.device)
     asym = torch.empty(2, dtype=torch.float64, device=A.device)

@@ -79,9 +79,18 @@ struct SidePlan {
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// TN_POISON=1 (diagnostic): every new device buffer is filled with NaN bytes,
+// so a read of uninitialised memory that reaches an output shows up as NaN.
+const bool g_poison = std::getenv("TN_POISON") != nullptr;
+void poison(void* p, size_t bytes, cudaStream_t st) {
+  if (g_poison) TN_CUDA(cudaMemsetAsync(p, 0xFF, bytes, st));
+}
+
 cplx* dnew(int64_t n, cudaStream_t st) {
   void* p = nullptr;
-  TN_CUDA(cudaMallocAsync(&p, (size_t)std::max<int64_t>(n, 1) * sizeof(cplx), st));
+  const size_t bytes = (size_t)std::max<int64_t>(n, 1) * sizeof(cplx);
+  TN_CUDA(cudaMallocAsync(&p, bytes, st));
+  poison(p, bytes, st);
   return (cplx*)p;
 }
 void ddel(cplx*& p, cudaStream_t st) {
@@ -101,12 +110,14 @@ struct Pool {  // stream-ordered transient device buffers
     void* p = nullptr;
     if (n <= 0) n = 1;
     TN_CUDA(cudaMallocAsync(&p, (size_t)n * sizeof(cplx), st));
+    poison(p, (size_t)n * sizeof(cplx), st);
     ptrs.push_back(p);
     return (cplx*)p;
   }
   void* raw(size_t bytes) {
     void* p = nullptr;
     TN_CUDA(cudaMallocAsync(&p, std::max<size_t>(bytes, 16), st));
+    poison(p, std::max<size_t>(bytes, 16), st);
     ptrs.push_back(p);
     return p;
   }
@@ -390,6 +401,7 @@ struct Engine {
     plan_side(top, ref_bonds, true);
     layout_arena();
     TN_CUDA(cudaMalloc(&arena, std::max<size_t>(arena_bytes, 256)));
+    if (g_poison) TN_CUDA(cudaMemset(arena, 0xFF, std::max<size_t>(arena_bytes, 256)));
     // reference copy
     ref_off.assign(n, 0);
     size_t e = 0;
@@ -1045,6 +1057,11 @@ struct Engine {
         tg.join();
         if (tf.joinable()) tf.join();
       };
+      // failure: let every side stream drain before the caller's stream frees
+      // this call's buffers (info, diagnostics, pools) during unwinding
+      auto drain = [&] {
+        for (cudaStream_t x : {st1, st2, stg, stf, sth}) cudaStreamSynchronize(x);
+      };
       try {
         Pool pool1(st1);
         Mps BD = primal_side(st1, sol[0], pool1, false, true, info, dg, publisher(0, st1));
@@ -1052,9 +1069,11 @@ struct Engine {
       } catch (...) {
         fail();
         join_all();
+        drain();
         throw;
       }
       join_all();
+      if (top_err || grad_err || fwd_err) drain();
       if (top_err) std::rethrow_exception(top_err);
       if (grad_err) std::rethrow_exception(grad_err);
       if (fwd_err) std::rethrow_exception(fwd_err);

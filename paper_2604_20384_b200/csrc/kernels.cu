@@ -4,6 +4,8 @@
 // tangent projection (App. E).  All complex128 interleaved, row-major.
 #include <algorithm>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -56,9 +58,11 @@ __global__ void apply_gate_kernel(cplx* out, int64_t sout, const cplx* x, int64_
   }
 }
 
+// b == 0: y is write-only (BLAS convention; y may be uninitialised, 0 * NaN = NaN)
 __global__ void axpby_kernel(cplx* __restrict__ y, const cplx* __restrict__ x, cplx a, cplx b, int64_t n) {
+  const bool read_y = b.x != 0.0 || b.y != 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    y[i] = cadd(cmul(a, x[i]), cmul(b, y[i]));
+    y[i] = read_y ? cadd(cmul(a, x[i]), cmul(b, y[i])) : cmul(a, x[i]);
 }
 
 __global__ void scale_kernel(cplx* __restrict__ y, const double* __restrict__ s, double pw, int64_t n) {
@@ -306,6 +310,7 @@ void extract_env(cudaStream_t st, cplx* E, int64_t sE, const cplx* top, int64_t 
   if (bx > 64) bx = 64;
   double* part = nullptr;
   TN_CUDA(cudaMallocAsync((void**)&part, sizeof(double) * 32 * bx * (size_t)batch, st));
+  if (std::getenv("TN_POISON")) TN_CUDA(cudaMemsetAsync(part, 0xFF, sizeof(double) * 32 * bx * (size_t)batch, st));
   dim3 grid(bx, batch);
   extract_env_kernel<<<grid, TPB, 0, st>>>(part, top, stop, z, sz, T, U);
   TN_CUDA(cudaGetLastError());
@@ -723,6 +728,7 @@ void tangent_dot(cudaStream_t st, int64_t n, int batch, const cplx* A, const cpl
   if (nblk < 1) nblk = 1;
   double* part = nullptr;
   TN_CUDA(cudaMallocAsync((void**)&part, sizeof(double) * (size_t)nblk * batch, st));
+  if (std::getenv("TN_POISON")) TN_CUDA(cudaMemsetAsync(part, 0xFF, sizeof(double) * (size_t)nblk * batch, st));
   tangent_dot_kernel<<<dim3(nblk, batch), 256, 0, st>>>(n, A, B, part);
   TN_CUDA(cudaGetLastError());
   count_launch();

@@ -363,6 +363,7 @@ void launch(const Params& p, int batch, cudaStream_t st) {
     if (ks > 1) {
       q.ksplit = ks;
       TN_CUDA(cudaMallocAsync((void**)&q.part, sizeof(cplx) * (size_t)ks * p.M * p.N * batch, st));
+      if (std::getenv("TN_POISON")) TN_CUDA(cudaMemsetAsync(q.part, 0xFF, sizeof(cplx) * (size_t)ks * p.M * p.N * batch, st));
       grid.z = batch * ks;
     }
   }

@@ -117,3 +117,19 @@ def test_error_statuses():
     assert e.value.status == N.TN_ENUMERIC
     eng.environments(torch.tensor(G, device=dev))         # recovers
     assert torch.isfinite(eng.apply(V)).all()
+
+
+def test_no_uninitialised_reads_under_nan_poison():
+    """TN_POISON=1 fills every new device buffer (pools, owned tensors, arena,
+    reduction partials) with NaN bytes: any read of uninitialised memory that
+    reaches an output turns it into NaN.  The small parity cases must still
+    pass (the library reads the flag at load, hence the subprocess)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TN_POISON="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_gpu_parity.py"), "-k", "small or config1 or linear"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
