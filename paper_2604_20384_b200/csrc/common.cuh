@@ -42,6 +42,7 @@ void count_launch(int64_t n = 1);
 int64_t launch_count();
 void gemm_profile_begin();                      // enable + reset (host side)
 void gemm_profile_end(double* ms, double* cmac);  // sync, disable, read totals
+bool gemm_profile_active();
 
 // Batched row-major complex GEMM on DMMA (zgemm.cu).
 // C[b] = alpha * op(A[b]) * op(B[b]) + beta * C[b]; op(A): M x K, op(B): K x N.

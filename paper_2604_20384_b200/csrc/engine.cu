@@ -180,6 +180,23 @@ struct Engine {
     std::vector<cplx*> Ab, Aa, B;
     Bonds bd;
   };
+  // CUDA-graph replay of tn_hvp_apply: a (batch, aux) key seen a second time
+  // since the last primal pass is captured once (engine-owned I/O buffers) and
+  // replayed; host scalars baked into the graph (frozen s) are per point, so
+  // every primal pass drops the graphs.  TN_NO_GRAPH=1 disables.
+  struct ApplyGraph {
+    int batch = 0;
+    bool aux = false;
+    int calls = 0;
+    bool failed = false;
+    cudaGraphExec_t exec = nullptr;
+    cplx *in = nullptr, *out = nullptr, *auxb = nullptr;
+    int64_t launches = 0;
+    double work = 0, work_apply = 0;
+  };
+  std::vector<ApplyGraph> graphs;
+  cudaStream_t stc = nullptr;  // capture stream
+  const bool graphs_enabled = std::getenv("TN_NO_GRAPH") == nullptr;
   double work_primal = 0, work_apply = 0, work_fwd_first = 0;
   std::atomic<double> work_counter{0.0};
   std::atomic<double> work_counter_fwd{0.0};  // GEMMs issued by the fused step's forward-tangent thread
@@ -434,6 +451,7 @@ struct Engine {
     TN_CUDA(cudaEventCreateWithFlags(&ev_join1, cudaEventDisableTiming));
     TN_CUDA(cudaStreamCreateWithFlags(&stg, cudaStreamNonBlocking));
     TN_CUDA(cudaStreamCreateWithFlags(&stf, cudaStreamNonBlocking));
+    TN_CUDA(cudaStreamCreateWithFlags(&stc, cudaStreamNonBlocking));
     TN_CUDA(cudaStreamCreateWithFlags(&sth, cudaStreamNonBlocking));
     TN_CUDA(cudaEventCreateWithFlags(&ev_joinf, cudaEventDisableTiming));
     TN_CUDA(cudaEventCreateWithFlags(&ev_joing, cudaEventDisableTiming));
@@ -528,7 +546,9 @@ struct Engine {
       for (auto& e : v)
         if (e) cudaEventDestroy(e);
     if (stg) cudaStreamDestroy(stg);
+    drop_graphs();
     if (stf) cudaStreamDestroy(stf);
+    if (stc) cudaStreamDestroy(stc);
     if (sth) cudaStreamDestroy(sth);
     if (ev_joinf) cudaEventDestroy(ev_joinf);
     if (st2) cudaStreamDestroy(st2);
@@ -919,7 +939,7 @@ struct Engine {
     cplx* HT = pool.c((int64_t)D * 16 * batch);
     cplx* om = pool.c(batch);
     ti_expand(st, D, K, batch, d_layer_of, v, V);
-    apply(st, batch, V, H, aux);
+    apply_call(st, batch, V, H, aux);
     ti_reduce(st, D, K, batch, d_layer_start, aux, HT);
     hessian_post(st, D, batch, ti_buf, ti_buf + 16 * D, ti_buf + 32 * D, at<double>(o_scal), HT, v, om, hess);
     TN_CUDA(cudaStreamSynchronize(st));  // pool temporaries are freed on return
@@ -932,6 +952,7 @@ struct Engine {
     TN_CUDA(cudaSetDevice(device));
     primal_valid = false;
     ti_valid = false;
+    drop_graphs();
     n_fallback = 0;
     n_deflate = 0;
     n_noise = 0;
@@ -1245,8 +1266,8 @@ struct Engine {
       } else {
         const double h = 1.0 / std::sqrt(2.0);
         cplx id[4] = {{h, 0}, {0, 0}, {0, 0}, {h, 0}};
-        TN_CUDA(cudaMemcpyAsync(t.Ab[s], id, sizeof(id), cudaMemcpyHostToDevice, st));
-        TN_CUDA(cudaMemcpyAsync(t.Aa[s], id, sizeof(id), cudaMemcpyHostToDevice, st));
+        set_small(st, t.Ab[s], 4, id[0], id[1], id[2], id[3]);
+        set_small(st, t.Aa[s], 4, id[0], id[1], id[2], id[3]);
       }
       t.B[s] = dnew(e * nb, st);
       TN_CUDA(cudaMemsetAsync(t.B[s], 0, (size_t)e * nb * sizeof(cplx), st));
@@ -1405,7 +1426,7 @@ struct Engine {
                    const std::vector<int>& tb, const std::vector<const cplx*>& TB, const std::vector<int>& bb) {
     L.assign(n + 1, nullptr);
     L[0] = pool.c(1);
-    TN_CUDA(cudaMemcpyAsync(L[0], &ONE, sizeof(cplx), cudaMemcpyHostToDevice, st));
+    set_small(st, L[0], 1, ONE);
     for (auto [s, k] : blocks(ell)) {
       const int w = k < 0 ? 4 : 16, e = k < 0 ? s + 1 : s + 2;
       cplx* Y = pool.c((int64_t)tb[s] * w * bb[e]);
@@ -1419,7 +1440,7 @@ struct Engine {
                     const std::vector<int>& tb, const std::vector<const cplx*>& TB, const std::vector<int>& bb) {
     R.assign(n + 1, nullptr);
     R[n] = pool.c(1);
-    TN_CUDA(cudaMemcpyAsync(R[n], &ONE, sizeof(cplx), cudaMemcpyHostToDevice, st));
+    set_small(st, R[n], 1, ONE);
     auto blks = blocks(ell);
     for (int j = (int)blks.size() - 1; j >= 0; --j) {
       const int s = blks[j].first, k = blks[j].second;
@@ -1798,6 +1819,90 @@ struct Engine {
     work_fwd_first = 0;
   }
 
+  void drop_graphs() {
+    if (graphs.empty()) return;
+    cudaDeviceSynchronize();  // no replay may still read the buffers
+    for (ApplyGraph& g : graphs) {
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+      for (cplx* p : {g.in, g.out, g.auxb})
+        if (p) cudaFree(p);
+    }
+    graphs.clear();
+  }
+
+  bool capture(ApplyGraph& g) {
+    const int64_t n = (int64_t)g.batch * K * 16;
+    TN_CUDA(cudaMalloc(&g.in, sizeof(cplx) * n));
+    TN_CUDA(cudaMalloc(&g.out, sizeof(cplx) * n));
+    if (g.aux) TN_CUDA(cudaMalloc(&g.auxb, sizeof(cplx) * (n + g.batch)));
+    TN_CUDA(cudaMemset(g.in, 0, sizeof(cplx) * n));
+    const int64_t l0 = launch_count();
+    const double w0 = work_counter.load();
+    cudaGraph_t graph = nullptr;
+    TN_CUDA(cudaStreamBeginCapture(stc, cudaStreamCaptureModeThreadLocal));
+    bool ok = true;
+    try {
+      apply(stc, g.batch, g.in, g.out, g.aux ? g.auxb : nullptr);
+    } catch (...) {
+      ok = false;
+    }
+    const cudaError_t e = cudaStreamEndCapture(stc, &graph);
+    g.launches = launch_count() - l0;
+    g.work = work_counter.load() - w0;
+    g.work_apply = work_apply;
+    count_launch(-g.launches);  // captured, not executed: credited per replay
+    work_counter.fetch_add(-g.work, std::memory_order_relaxed);
+    if (!ok || e != cudaSuccess || !graph) {
+      cudaGetLastError();
+      if (graph) cudaGraphDestroy(graph);
+      return false;
+    }
+    const cudaError_t ei = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) {
+      cudaGetLastError();
+      g.exec = nullptr;
+      return false;
+    }
+    return true;
+  }
+
+  // tn_hvp_apply entry: eager, or graph replay for a repeated (batch, aux)
+  void apply_call(cudaStream_t st, int batch, const cplx* dirs, cplx* hess, cplx* aux) {
+    TN_CUDA(cudaSetDevice(device));
+    if (!primal_valid) throw StateError("tn_hvp_apply before tn_hvp_environments");
+    if (!graphs_enabled || batch <= 0 || gemm_profile_active() || std::getenv("TN_PHASES")) {
+      apply(st, batch, dirs, hess, aux);
+      return;
+    }
+    ApplyGraph* g = nullptr;
+    for (ApplyGraph& x : graphs)
+      if (x.batch == batch && x.aux == (aux != nullptr)) g = &x;
+    if (!g) {
+      graphs.push_back(ApplyGraph{});
+      g = &graphs.back();
+      g->batch = batch;
+      g->aux = aux != nullptr;
+    }
+    if (++g->calls == 1 || g->failed) {
+      apply(st, batch, dirs, hess, aux);
+      return;
+    }
+    if (!g->exec && !capture(*g)) {
+      g->failed = true;
+      apply(st, batch, dirs, hess, aux);
+      return;
+    }
+    const int64_t n = (int64_t)batch * K * 16;
+    TN_CUDA(cudaMemcpyAsync(g->in, dirs, sizeof(cplx) * n, cudaMemcpyDeviceToDevice, st));
+    TN_CUDA(cudaGraphLaunch(g->exec, st));
+    TN_CUDA(cudaMemcpyAsync(hess, g->out, sizeof(cplx) * n, cudaMemcpyDeviceToDevice, st));
+    if (aux) TN_CUDA(cudaMemcpyAsync(aux, g->auxb, sizeof(cplx) * (n + batch), cudaMemcpyDeviceToDevice, st));
+    count_launch(g->launches);
+    work_counter.fetch_add(g->work, std::memory_order_relaxed);
+    work_apply = g->work_apply;
+  }
+
   // Fused step (tn_hvp_step): environments + HVPs of `batch` directions, with
   // the first sub-batch's forward tangents replayed on a fourth stream while
   // the top sweep and the layer gradients still run (the forward tangent of
@@ -1832,7 +1937,7 @@ void engine_environments(tn_hvp_ctx* ctx, const cplx* gates, double* scalars, cp
   ctx->e.environments(st, gates, scalars, grad_R);
 }
 void engine_apply(tn_hvp_ctx* ctx, int batch, const cplx* dirs, cplx* hess_R, cplx* aux, cudaStream_t st) {
-  ctx->e.apply(st, batch, dirs, hess_R, aux);
+  ctx->e.apply_call(st, batch, dirs, hess_R, aux);
 }
 void engine_step(tn_hvp_ctx* ctx, const cplx* gates, double* scalars, cplx* grad_R, int batch, const cplx* dirs,
                  cplx* hess_R, cplx* aux, cudaStream_t st) {
@@ -1859,6 +1964,7 @@ void engine_primal_blob(tn_hvp_ctx* ctx, void** ptr, size_t* bytes) {
 void engine_primal_imported(tn_hvp_ctx* ctx, const cplx* gates, cudaStream_t st) {
   Engine& e = ctx->e;
   (void)gates;
+  e.drop_graphs();
   for (SidePlan* sp : {&e.bot, &e.top})
     for (auto& ls : sp->steps)
       for (Step& s : ls)

@@ -786,4 +786,17 @@ void ti_reduce(cudaStream_t st, int L, int K, int batch, const int* start, const
   count_launch();
 }
 
+namespace {
+__global__ void set_small_kernel(cplx* p, int n, cplx v0, cplx v1, cplx v2, cplx v3) {
+  const int i = threadIdx.x;
+  if (i < n) p[i] = i == 0 ? v0 : i == 1 ? v1 : i == 2 ? v2 : v3;
+}
+}  // namespace
+
+void set_small(cudaStream_t st, cplx* p, int n, cplx v0, cplx v1, cplx v2, cplx v3) {
+  set_small_kernel<<<1, 32, 0, st>>>(p, n, v0, v1, v2, v3);
+  TN_CUDA(cudaGetLastError());
+  count_launch();
+}
+
 }  // namespace tn

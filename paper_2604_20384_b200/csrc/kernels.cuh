@@ -76,3 +76,10 @@ namespace tn {
 void ti_expand(cudaStream_t st, int L, int K, int batch, const int* layer_of, const cplx* src, cplx* dst);
 void ti_reduce(cudaStream_t st, int L, int K, int batch, const int* start, const cplx* src, cplx* dst);
 }  // namespace tn
+
+namespace tn {
+// p[0..n) = (v0, v1, v2, v3)[0..n), n <= 4: device-side constants (no pageable
+// host copies, so the apply path can be captured into a CUDA graph)
+void set_small(cudaStream_t st, cplx* p, int n, cplx v0, cplx v1 = {0.0, 0.0}, cplx v2 = {0.0, 0.0},
+               cplx v3 = {0.0, 0.0});
+}  // namespace tn

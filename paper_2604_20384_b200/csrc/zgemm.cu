@@ -413,6 +413,11 @@ void dispatch_b(char opb, const Params& p, int batch, cudaStream_t st) {
 void count_launch(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 int64_t launch_count() { return g_launches.load(); }
 
+bool gemm_profile_active() {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  return g_prof.on;
+}
+
 void gemm_profile_begin() {
   std::lock_guard<std::mutex> lk(g_prof_mu);
   for (auto& e : g_prof.ev) {

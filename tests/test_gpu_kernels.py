@@ -133,3 +133,36 @@ def test_no_uninitialised_reads_under_nan_poison():
                         os.path.join(root, "tests", "test_gpu_parity.py"), "-k", "small or config1 or linear"],
                        cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_apply_graph_replay_is_bitwise_eager():
+    """Repeated same-batch tn_hvp_apply calls (tCG) run eagerly, then are
+    captured into a CUDA graph and replayed: results bitwise equal, launch and
+    work counters credited per replay, graphs dropped by the next primal pass."""
+    from paper_2604_20384_b200 import _native as N
+    from paper_2604_20384_b200.api import HVPEngine
+    from tn_inputs.reference import reference_mpo
+    cfg = C.small_case(82, 8, 5, 16, batch=3)
+    ref = reference_mpo(C.reference_layers(cfg), cfg.n, cfg.chi)
+    K = C.num_gates(cfg.n, cfg.depth)
+    G = C.haar_gates(82, K)
+    dev = torch.device("cuda")
+    eng = HVPEngine(cfg.n, cfg.depth, cfg.chi, [a.to(dev) for a in ref], max_batch=2)
+    V = torch.tensor(C.tangent_directions(82, G, 3), device=dev)
+    for rep in range(2):                                   # second primal pass drops and re-captures
+        eng.environments(torch.tensor(G, device=dev))
+        outs, counts, works = [], [], []
+        for call in range(4):
+            l0 = N.tn_hvp_launch_count()
+            Vc = V.clone()                                 # fresh input buffer each call, as in tCG
+            outs.append(eng.apply(Vc).clone())
+            torch.cuda.synchronize()
+            counts.append(N.tn_hvp_launch_count() - l0)
+            works.append(eng.work()[0])
+        for o in outs[1:]:
+            assert torch.equal(o, outs[0])
+        assert len(set(counts)) == 1 and counts[0] > 0
+        assert len(set(works)) == 1
+        H1 = eng.apply(V[1:2].contiguous())                # other batch size: its own key
+        assert torch.equal(H1, eng.apply(V[1:2].contiguous()))
+    eng.close()
