@@ -17,6 +17,7 @@
 #include <cusolverDn.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <condition_variable>
 #include <functional>
@@ -172,14 +173,30 @@ struct Engine {
   int* d_layer_start = nullptr;  // [D+1] first gate of each layer
   cplx* ti_buf = nullptr;      // [3][D][16]: layer gates g, dT/dg, grad_f
   bool ti_valid = false;
+  // Direction-independent tangent chains of one side at the current point:
+  // every chain tensor the replay creates (and the move factors X), recorded
+  // by the first apply after a primal pass and borrowed by later ones.
+  struct ChainCache {
+    bool built = false;
+    std::vector<cplx*> init_Ab, init_Aa;
+    std::vector<std::array<cplx*, 4>> step;  // per replayed step, in order
+    std::vector<cplx*> owned;                // everything to free on drop
+  };
+  enum ChainMode { CHAIN_OWN = 0, CHAIN_RECORD = 1, CHAIN_REPLAY = 2 };
   struct Tangent {  // channel-form tangents for nb directions
     std::vector<cplx*> Ab, Aa, B;  // B[s]: nb blocks, direction stride = size(B[s])
     Bonds bd;                      // bonds: ab / aa used (p = primal)
+    ChainMode mode = CHAIN_OWN;    // RECORD / REPLAY: chains belong to `cache`
+    ChainCache* cache = nullptr;
+    size_t step_no = 0;
   };
   struct TanSnap {
     std::vector<cplx*> Ab, Aa, B;
     Bonds bd;
+    bool chains_owned = true;
   };
+  ChainCache chain_cache[2];  // 0 bottom (forward tangents), 1 top (backward)
+  const bool chain_cache_enabled = std::getenv("TN_NO_CHAIN_CACHE") == nullptr;
   // CUDA-graph replay of tn_hvp_apply: a (batch, aux) key seen a second time
   // since the last primal pass is captured once (engine-owned I/O buffers) and
   // replayed; host scalars baked into the graph (frozen s) are per point, so
@@ -547,6 +564,7 @@ struct Engine {
         if (e) cudaEventDestroy(e);
     if (stg) cudaStreamDestroy(stg);
     drop_graphs();
+    drop_chain_cache();
     if (stf) cudaStreamDestroy(stf);
     if (stc) cudaStreamDestroy(stc);
     if (sth) cudaStreamDestroy(sth);
@@ -953,6 +971,7 @@ struct Engine {
     primal_valid = false;
     ti_valid = false;
     drop_graphs();
+    drop_chain_cache();
     n_fallback = 0;
     n_deflate = 0;
     n_noise = 0;
@@ -1250,13 +1269,29 @@ struct Engine {
 
   int64_t bsize(const Bonds& b, int s) const { return (int64_t)b.ab[s] * 4 * b.aa[s + 1]; }
 
-  void tangent_init(cudaStream_t st, Tangent& t, const SidePlan& sp, bool is_top, int nb) {
+  void tangent_init(cudaStream_t st, Tangent& t, const SidePlan& sp, bool is_top, int nb,
+                    ChainCache* cache = nullptr) {
     t.bd = sp.init;
     t.Ab.assign(n, nullptr);
     t.Aa.assign(n, nullptr);
     t.B.assign(n, nullptr);
+    t.cache = cache;
+    t.step_no = 0;
+    t.mode = !cache ? CHAIN_OWN : cache->built ? CHAIN_REPLAY : CHAIN_RECORD;
+    if (t.mode == CHAIN_RECORD) {
+      cache->step.clear();
+      cache->init_Ab.assign(n, nullptr);
+      cache->init_Aa.assign(n, nullptr);
+    }
     for (int s = 0; s < n; ++s) {
       const int64_t e = (int64_t)t.bd.p[s] * 4 * t.bd.p[s + 1];
+      t.B[s] = dnew(e * nb, st);
+      TN_CUDA(cudaMemsetAsync(t.B[s], 0, (size_t)e * nb * sizeof(cplx), st));
+      if (t.mode == CHAIN_REPLAY) {
+        t.Ab[s] = cache->init_Ab[s];
+        t.Aa[s] = cache->init_Aa[s];
+        continue;
+      }
       t.Ab[s] = dnew(e, st);
       t.Aa[s] = dnew(e, st);
       const cplx* src = is_top ? ref + ref_off[s] : nullptr;
@@ -1269,32 +1304,99 @@ struct Engine {
         set_small(st, t.Ab[s], 4, id[0], id[1], id[2], id[3]);
         set_small(st, t.Aa[s], 4, id[0], id[1], id[2], id[3]);
       }
-      t.B[s] = dnew(e * nb, st);
-      TN_CUDA(cudaMemsetAsync(t.B[s], 0, (size_t)e * nb * sizeof(cplx), st));
+      if (t.mode == CHAIN_RECORD) {
+        cache->init_Ab[s] = t.Ab[s];
+        cache->init_Aa[s] = t.Aa[s];
+        cache->owned.push_back(t.Ab[s]);
+        cache->owned.push_back(t.Aa[s]);
+      }
     }
   }
 
-  template <class T>
-  void release(T& t, cudaStream_t st) {
-    for (auto* v : {&t.Ab, &t.Aa, &t.B})
-      for (cplx*& p : *v) ddel(p, st);
+  // end of a side's replay: free what the tangent owns (recorded chains stay
+  // in the cache, which is complete from now on)
+  void release(Tangent& t, cudaStream_t st) {
+    for (cplx*& p : t.B) ddel(p, st);
+    if (t.mode == CHAIN_OWN) {
+      for (auto* v : {&t.Ab, &t.Aa})
+        for (cplx*& p : *v) ddel(p, st);
+    } else if (t.mode == CHAIN_RECORD) {
+      t.cache->built = true;
+    }
+  }
+  void release(TanSnap& t, cudaStream_t st) {
+    for (cplx*& p : t.B) ddel(p, st);
+    if (t.chains_owned)
+      for (auto* v : {&t.Ab, &t.Aa})
+        for (cplx*& p : *v) ddel(p, st);
+  }
+  // a chain slot takes a new tensor: freed if the tangent owns its chains
+  void chain_set(Tangent& t, cplx*& slot, cplx* nw, cudaStream_t st) {
+    if (t.mode == CHAIN_OWN) dset(slot, nw, st);
+    else slot = nw;
+  }
+  void record(Tangent& t, std::array<cplx*, 4> c) {
+    t.cache->step.push_back(c);
+    for (cplx* p : c)
+      if (p) t.cache->owned.push_back(p);
+  }
+
+  int64_t chain_cache_elems(const SidePlan& sp) const {
+    int64_t e = 0;
+    for (int s = 0; s < n; ++s) e += 2LL * sp.init.p[s] * 4 * sp.init.p[s + 1];
+    for (auto& ls : sp.steps)
+      for (const Step& x : ls) {
+        if (x.type == MOVE_R) e += (int64_t)x.kq * x.ab1 + 4LL * x.b * x.kq + (int64_t)x.kq * 4 * x.ab2;
+        else if (x.type == MOVE_L) e += (int64_t)x.aa0 * x.kq + (int64_t)x.kq * 4 * x.bp + (int64_t)x.aam * 4 * x.kq;
+        else e += 4LL * x.aa0 * x.r + (int64_t)x.r * 4 * x.br + 4LL * x.bl * x.r + (int64_t)x.r * 4 * x.ab2;
+      }
+    return e;
+  }
+  // the side's cache if enabled and it fits (keeping half the free memory)
+  ChainCache* chain_cache_for(int side) {
+    if (!chain_cache_enabled) return nullptr;
+    ChainCache& c = chain_cache[side];
+    if (c.built) return &c;
+    size_t fr = 0, tot = 0;
+    TN_CUDA(cudaMemGetInfo(&fr, &tot));
+    const size_t need = sizeof(cplx) * (size_t)chain_cache_elems(side ? top : bot);
+    return need < fr / 2 ? &c : nullptr;
+  }
+  void drop_chain_cache() {
+    bool any = false;
+    for (ChainCache& c : chain_cache) any = any || !c.owned.empty();
+    if (!any) return;
+    cudaDeviceSynchronize();
+    for (ChainCache& c : chain_cache) {
+      for (cplx* p : c.owned) cudaFreeAsync(p, stc);
+      c = ChainCache{};
+    }
+    cudaStreamSynchronize(stc);
   }
 
   // One replayed step on a batch of tangents.  M: gate array (G or G^dag),
   // VM: per-direction gate variations [nb][K][16] (V or V^dag).
   void tangent_step(cudaStream_t st, Tangent& t, const Step& s, const cplx* M, const cplx* VM, int nb) {
     const int64_t KK = (int64_t)K * 16;
+    const size_t sn = t.step_no++;  // index of this step in the side's chain cache
     Pool pool(st);  // step temporaries
     if (s.type == MOVE_R) {
       const int c = s.site, b = s.b, kq = s.kq;
       const int ab1 = s.ab1, ab2 = s.ab2, aa1 = s.aa1, aa2 = s.aa2;
       const cplx* Q = at(s.o_q);                        // (4b x kq)
-      cplx* X = pool.c((int64_t)kq * ab1);              // Q^H Ab_c
-      cn(st, kq, ab1, 4 * b, Q, 0, t.Ab[c], 0, X, 0, 1);
-      cplx* nAbc = dnew((int64_t)4 * b * kq, st);
-      TN_CUDA(cudaMemcpyAsync(nAbc, Q, (size_t)4 * b * kq * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-      cplx* nAb1 = dnew((int64_t)kq * 4 * ab2, st);
-      nn(st, kq, 4 * ab2, ab1, X, 0, t.Ab[c + 1], 0, nAb1, 0, 1);
+      cplx *X, *nAbc, *nAb1;                            // X = Q^H Ab_c; chains
+      if (t.mode == CHAIN_REPLAY) {
+        const auto& cc = t.cache->step.at(sn);
+        X = cc[0], nAbc = cc[1], nAb1 = cc[2];
+      } else {
+        X = t.mode == CHAIN_RECORD ? dnew((int64_t)kq * ab1, st) : pool.c((int64_t)kq * ab1);
+        cn(st, kq, ab1, 4 * b, Q, 0, t.Ab[c], 0, X, 0, 1);
+        nAbc = dnew((int64_t)4 * b * kq, st);
+        TN_CUDA(cudaMemcpyAsync(nAbc, Q, (size_t)4 * b * kq * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+        nAb1 = dnew((int64_t)kq * 4 * ab2, st);
+        nn(st, kq, 4 * ab2, ab1, X, 0, t.Ab[c + 1], 0, nAb1, 0, 1);
+        if (t.mode == CHAIN_RECORD) record(t, {X, nAbc, nAb1, nullptr});
+      }
       // blocks: B_c (b,4,aa1), B_{c+1} (ab1,4,aa2)
       const int64_t sc0 = (int64_t)4 * b * aa1, sc1o = (int64_t)ab1 * 4 * aa2, sc1n = (int64_t)kq * 4 * aa2;
       cplx* Y = pool.c((int64_t)kq * aa1 * nb);
@@ -1303,8 +1405,8 @@ struct Engine {
       cplx* nB1 = dnew(sc1n * nb, st);
       nn(st, kq, 4 * aa2, ab1, X, 0, t.B[c + 1], sc1o, nB1, sc1n, nb);
       nn(st, kq, 4 * aa2, aa1, Y, (int64_t)kq * aa1, t.Aa[c + 1], 0, nB1, sc1n, nb, ONE, ONE);
-      dset(t.Ab[c], nAbc, st);
-      dset(t.Ab[c + 1], nAb1, st);
+      chain_set(t, t.Ab[c], nAbc, st);
+      chain_set(t, t.Ab[c + 1], nAb1, st);
       dset(t.B[c + 1], nB1, st);
       t.bd.p[c + 1] = kq;
       t.bd.ab[c + 1] = kq;
@@ -1312,12 +1414,19 @@ struct Engine {
       const int c = s.site, bp = s.bp, kq = s.kq;
       const int aa0 = s.aa0, aam = s.aam, ab0 = s.ab0, abm = s.abm;
       const cplx* Q = at(s.o_q);                        // (kq x 4bp)
-      cplx* X = pool.c((int64_t)aa0 * kq);              // Aa_c Q^H
-      nc(st, aa0, kq, 4 * bp, t.Aa[c], 0, Q, 0, X, 0, 1);
-      cplx* nAac = dnew((int64_t)kq * 4 * bp, st);
-      TN_CUDA(cudaMemcpyAsync(nAac, Q, (size_t)kq * 4 * bp * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-      cplx* nAam = dnew((int64_t)aam * 4 * kq, st);
-      nn(st, aam * 4, kq, aa0, t.Aa[c - 1], 0, X, 0, nAam, 0, 1);
+      cplx *X, *nAac, *nAam;                            // X = Aa_c Q^H; chains
+      if (t.mode == CHAIN_REPLAY) {
+        const auto& cc = t.cache->step.at(sn);
+        X = cc[0], nAac = cc[1], nAam = cc[2];
+      } else {
+        X = t.mode == CHAIN_RECORD ? dnew((int64_t)aa0 * kq, st) : pool.c((int64_t)aa0 * kq);
+        nc(st, aa0, kq, 4 * bp, t.Aa[c], 0, Q, 0, X, 0, 1);
+        nAac = dnew((int64_t)kq * 4 * bp, st);
+        TN_CUDA(cudaMemcpyAsync(nAac, Q, (size_t)kq * 4 * bp * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+        nAam = dnew((int64_t)aam * 4 * kq, st);
+        nn(st, aam * 4, kq, aa0, t.Aa[c - 1], 0, X, 0, nAam, 0, 1);
+        if (t.mode == CHAIN_RECORD) record(t, {X, nAac, nAam, nullptr});
+      }
       // blocks: B_c (ab0,4,bp), B_{c-1} (abm,4,aa0)
       const int64_t sc0 = (int64_t)ab0 * 4 * bp, sm_o = (int64_t)abm * 4 * aa0, sm_n = (int64_t)abm * 4 * kq;
       cplx* Y = pool.c((int64_t)ab0 * kq * nb);
@@ -1326,8 +1435,8 @@ struct Engine {
       cplx* nBm = dnew(sm_n * nb, st);
       nn(st, abm * 4, kq, aa0, t.B[c - 1], sm_o, X, 0, nBm, sm_n, nb);
       nn(st, abm * 4, kq, ab0, t.Ab[c - 1], 0, Y, (int64_t)ab0 * kq, nBm, sm_n, nb, ONE, ONE);
-      dset(t.Aa[c], nAac, st);
-      dset(t.Aa[c - 1], nAam, st);
+      chain_set(t, t.Aa[c], nAac, st);
+      chain_set(t, t.Aa[c - 1], nAam, st);
       dset(t.B[c - 1], nBm, st);
       t.bd.p[c] = kq;
       t.bd.aa[c] = kq;
@@ -1369,25 +1478,32 @@ struct Engine {
         nn(st, r, 4 * br, r, UDW, sRR, vh, 0, nBj, sUD, nb, cmsc, csc);
         axpby(st, nBi, Z, csc, ZERO, sZ * nb);
       }
-      // chains
-      cplx* aa2t = pool.c((int64_t)16 * aa0 * br);
-      nn(st, 4 * aa0, 4 * br, aa1, t.Aa[i], 0, t.Aa[i + 1], 0, aa2t, 0, 1);
-      apply_gate(st, aa2t, 0, aa2t, 0, Mk, 0, aa0, br, 1, ONE, false);
-      cplx* nAai = dnew((int64_t)4 * aa0 * r, st);
-      nc(st, 4 * aa0, r, 4 * br, aa2t, 0, vh, 0, nAai, 0, 1, csc);
-      cplx* nAaj = dnew((int64_t)r * 4 * br, st);
-      TN_CUDA(cudaMemcpyAsync(nAaj, vh, (size_t)r * 4 * br * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-      cplx* ab2t = pool.c((int64_t)16 * bl * ab2);
-      nn(st, 4 * bl, 4 * ab2, ab1, t.Ab[i], 0, t.Ab[i + 1], 0, ab2t, 0, 1);
-      apply_gate(st, ab2t, 0, ab2t, 0, Mk, 0, bl, ab2, 1, ONE, false);
-      cplx* nAbj = dnew((int64_t)r * 4 * ab2, st);
-      nn(st, r, 4 * ab2, 4 * bl, uh, 0, ab2t, 0, nAbj, 0, 1, csc);
-      cplx* nAbi = dnew((int64_t)4 * bl * r, st);
-      conjT_scale_cols(st, nAbi, uh, r, 4 * bl, nullptr, nullptr);
-      dset(t.Aa[i], nAai, st);
-      dset(t.Aa[i + 1], nAaj, st);
-      dset(t.Ab[i], nAbi, st);
-      dset(t.Ab[i + 1], nAbj, st);
+      // chains (direction-independent; recorded / replayed per point)
+      cplx *nAai, *nAaj, *nAbi, *nAbj;
+      if (t.mode == CHAIN_REPLAY) {
+        const auto& cc = t.cache->step.at(sn);
+        nAai = cc[0], nAaj = cc[1], nAbi = cc[2], nAbj = cc[3];
+      } else {
+        cplx* aa2t = pool.c((int64_t)16 * aa0 * br);
+        nn(st, 4 * aa0, 4 * br, aa1, t.Aa[i], 0, t.Aa[i + 1], 0, aa2t, 0, 1);
+        apply_gate(st, aa2t, 0, aa2t, 0, Mk, 0, aa0, br, 1, ONE, false);
+        nAai = dnew((int64_t)4 * aa0 * r, st);
+        nc(st, 4 * aa0, r, 4 * br, aa2t, 0, vh, 0, nAai, 0, 1, csc);
+        nAaj = dnew((int64_t)r * 4 * br, st);
+        TN_CUDA(cudaMemcpyAsync(nAaj, vh, (size_t)r * 4 * br * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+        cplx* ab2t = pool.c((int64_t)16 * bl * ab2);
+        nn(st, 4 * bl, 4 * ab2, ab1, t.Ab[i], 0, t.Ab[i + 1], 0, ab2t, 0, 1);
+        apply_gate(st, ab2t, 0, ab2t, 0, Mk, 0, bl, ab2, 1, ONE, false);
+        nAbj = dnew((int64_t)r * 4 * ab2, st);
+        nn(st, r, 4 * ab2, 4 * bl, uh, 0, ab2t, 0, nAbj, 0, 1, csc);
+        nAbi = dnew((int64_t)4 * bl * r, st);
+        conjT_scale_cols(st, nAbi, uh, r, 4 * bl, nullptr, nullptr);
+        if (t.mode == CHAIN_RECORD) record(t, {nAai, nAaj, nAbi, nAbj});
+      }
+      chain_set(t, t.Aa[i], nAai, st);
+      chain_set(t, t.Aa[i + 1], nAaj, st);
+      chain_set(t, t.Ab[i], nAbi, st);
+      chain_set(t, t.Ab[i + 1], nAbj, st);
       dset(t.B[i], nBi, st);
       dset(t.B[i + 1], nBj, st);
       t.bd.p[i + 1] = r;
@@ -1403,6 +1519,17 @@ struct Engine {
     sn.Ab.resize(n);
     sn.Aa.resize(n);
     sn.B.resize(n);
+    if (t.mode != CHAIN_OWN) {  // chains live in the cache: borrow them
+      sn.chains_owned = false;
+      sn.Ab = t.Ab;
+      sn.Aa = t.Aa;
+      for (int s = 0; s < n; ++s) {
+        const int64_t e = bsize(t.bd, s) * nb;
+        sn.B[s] = dnew(e, st);
+        TN_CUDA(cudaMemcpyAsync(sn.B[s], t.B[s], e * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+      }
+      return sn;
+    }
     for (int s = 0; s < n; ++s) {
       const int64_t eb = (int64_t)t.bd.ab[s] * 4 * t.bd.ab[s + 1];
       const int64_t ea = (int64_t)t.bd.aa[s] * 4 * t.bd.aa[s + 1];
@@ -1735,7 +1862,7 @@ struct Engine {
                                         const std::function<void(int)>& before_layer = nullptr) {
     std::vector<TanSnap> DB(D);
     Tangent t;
-    tangent_init(st, t, bot, false, nb);
+    tangent_init(st, t, bot, false, nb, chain_cache_for(0));
     for (size_t li = 0; li < bot.steps.size(); ++li) {
       DB[li] = take_snapshot(st, t, nb);
       if (before_layer) before_layer((int)li);
@@ -1776,7 +1903,7 @@ struct Engine {
       }
       // backward (top) tangent on the fly + layer HVP extraction
       Tangent t;
-      tangent_init(st, t, top, true, nb);
+      tangent_init(st, t, top, true, nb, chain_cache_for(1));
       for (size_t li = 0; li < top.steps.size(); ++li) {
         const int ell = top.ell[li];
         if (phases) TN_CUDA(cudaEventRecord(pe[2], st));
@@ -1965,6 +2092,7 @@ void engine_primal_imported(tn_hvp_ctx* ctx, const cplx* gates, cudaStream_t st)
   Engine& e = ctx->e;
   (void)gates;
   e.drop_graphs();
+  e.drop_chain_cache();
   for (SidePlan* sp : {&e.bot, &e.top})
     for (auto& ls : sp->steps)
       for (Step& s : ls)

@@ -161,8 +161,41 @@ def test_apply_graph_replay_is_bitwise_eager():
             works.append(eng.work()[0])
         for o in outs[1:]:
             assert torch.equal(o, outs[0])
-        assert len(set(counts)) == 1 and counts[0] > 0
-        assert len(set(works)) == 1
+        # call 0 also records the point's chain cache; calls 1 (capture + launch)
+        # and 2, 3 (replays) run the same kernels and are credited the same
+        assert len(set(counts[1:])) == 1 and 0 < counts[1] <= counts[0]
+        assert len(set(works[1:])) == 1
         H1 = eng.apply(V[1:2].contiguous())                # other batch size: its own key
         assert torch.equal(H1, eng.apply(V[1:2].contiguous()))
     eng.close()
+
+
+def test_chain_cache_is_bitwise_uncached():
+    """The per-point cache of direction-independent tangent chains (recorded by
+    the first apply after a primal pass, borrowed afterwards) changes no bit:
+    same HVPs as an engine built with TN_NO_CHAIN_CACHE=1, over several
+    sub-batches, repeated calls and two primal passes."""
+    import os
+    from paper_2604_20384_b200.api import HVPEngine
+    from tn_inputs.reference import reference_mpo
+    cfg = C.small_case(83, 8, 6, 12, batch=5, first_offset=1)
+    ref = [a.to("cuda") for a in reference_mpo(C.reference_layers(cfg), cfg.n, cfg.chi)]
+    K = C.num_gates(cfg.n, cfg.depth, 1)
+    dev = torch.device("cuda")
+    os.environ["TN_NO_CHAIN_CACHE"] = "1"
+    try:
+        plain = HVPEngine(cfg.n, cfg.depth, cfg.chi, ref, 1, max_batch=2)
+    finally:
+        del os.environ["TN_NO_CHAIN_CACHE"]
+    cached = HVPEngine(cfg.n, cfg.depth, cfg.chi, ref, 1, max_batch=2)
+    for seed in (83, 84):
+        G = torch.tensor(C.haar_gates(seed, K), device=dev)
+        V = torch.tensor(C.tangent_directions(seed, G.cpu().numpy(), 5), device=dev)
+        plain.environments(G)
+        cached.environments(G)
+        want = plain.apply(V)
+        for _ in range(3):
+            assert torch.equal(cached.apply(V), want)
+        assert torch.equal(cached.apply(V[2:3].contiguous()), want[2:3])
+    plain.close()
+    cached.close()
