@@ -30,6 +30,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "engine.cuh"
@@ -197,6 +198,14 @@ struct Engine {
   };
   ChainCache chain_cache[2];  // 0 bottom (forward tangents), 1 top (backward)
   const bool chain_cache_enabled = std::getenv("TN_NO_CHAIN_CACHE") == nullptr;
+  // Per-point memo of the direction-independent tensors of layer_hvp (block
+  // pairs, shared chain environments, shared products), keyed (layer, site,
+  // tag); recorded by the first apply after a primal pass within a memory
+  // budget (a third of the free memory then), borrowed afterwards.
+  std::unordered_map<uint64_t, cplx*> memo_map;
+  std::vector<cplx*> memo_owned;
+  size_t memo_bytes = 0, memo_budget = 0;
+  bool memo_budget_set = false;
   // CUDA-graph replay of tn_hvp_apply: a (batch, aux) key seen a second time
   // since the last primal pass is captured once (engine-owned I/O buffers) and
   // replayed; host scalars baked into the graph (frozen s) are per point, so
@@ -1363,7 +1372,8 @@ struct Engine {
     return need < fr / 2 ? &c : nullptr;
   }
   void drop_chain_cache() {
-    bool any = false;
+    memo_budget_set = false;
+    bool any = !memo_owned.empty();
     for (ChainCache& c : chain_cache) any = any || !c.owned.empty();
     if (!any) return;
     cudaDeviceSynchronize();
@@ -1371,7 +1381,42 @@ struct Engine {
       for (cplx* p : c.owned) cudaFreeAsync(p, stc);
       c = ChainCache{};
     }
+    for (cplx* p : memo_owned) cudaFreeAsync(p, stc);
+    memo_owned.clear();
+    memo_map.clear();
+    memo_bytes = 0;
     cudaStreamSynchronize(stc);
+  }
+
+  template <class F>
+  cplx* memo(cudaStream_t st, Pool& tmp, int ell, int s, int tag, int64_t elems, F&& fill) {
+    const uint64_t key = ((uint64_t)ell << 40) | ((uint64_t)(s + 1) << 16) | (uint64_t)tag;
+    if (chain_cache_enabled) {
+      auto it = memo_map.find(key);
+      if (it != memo_map.end()) return it->second;
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      TN_CUDA(cudaStreamIsCapturing(st, &cs));
+      if (cs == cudaStreamCaptureStatusNone) {
+        if (!memo_budget_set) {
+          size_t fr = 0, tot = 0;
+          TN_CUDA(cudaMemGetInfo(&fr, &tot));
+          memo_budget = fr / 3;
+          memo_budget_set = true;
+        }
+        const size_t bytes = (size_t)std::max<int64_t>(elems, 1) * sizeof(cplx);
+        if (memo_bytes + bytes <= memo_budget) {
+          cplx* p = dnew(elems, st);
+          fill(p);
+          memo_map.emplace(key, p);
+          memo_owned.push_back(p);
+          memo_bytes += bytes;
+          return p;
+        }
+      }
+    }
+    cplx* p = tmp.c(elems);
+    fill(p);
+    return p;
   }
 
   // One replayed step on a batch of tangents.  M: gate array (G or G^dag),
@@ -1549,33 +1594,37 @@ struct Engine {
   // tensor starting at site s (two-site pair for a gate block, the site
   // tensor for an idle site), taken from layer_hvp's block cache.
   // Left: L[0] = 1, L[e] = TT^H (L[s] TB); right: R[n] = 1, R[s] = (TB R[e]) TT^H.
-  void shared_left(cudaStream_t st, Pool& pool, int ell, std::vector<cplx*>& L, const std::vector<const cplx*>& TT,
-                   const std::vector<int>& tb, const std::vector<const cplx*>& TB, const std::vector<int>& bb) {
+  void shared_left(cudaStream_t st, Pool& pool, int ell, int tag, std::vector<cplx*>& L,
+                   const std::vector<const cplx*>& TT, const std::vector<int>& tb, const std::vector<const cplx*>& TB,
+                   const std::vector<int>& bb) {
     L.assign(n + 1, nullptr);
-    L[0] = pool.c(1);
-    set_small(st, L[0], 1, ONE);
+    L[0] = memo(st, pool, ell, 0, tag, 1, [&](cplx* o) { set_small(st, o, 1, ONE); });
     for (auto [s, k] : blocks(ell)) {
       const int w = k < 0 ? 4 : 16, e = k < 0 ? s + 1 : s + 2;
-      cplx* Y = pool.c((int64_t)tb[s] * w * bb[e]);
-      nn(st, tb[s], w * bb[e], bb[s], L[s], 0, TB[s], 0, Y, 0, 1);
-      L[e] = pool.c((int64_t)tb[e] * bb[e]);
-      cn(st, tb[e], bb[e], w * tb[s], TT[s], 0, Y, 0, L[e], 0, 1);
+      L[e] = memo(st, pool, ell, e, tag, (int64_t)tb[e] * bb[e], [&](cplx* o) {
+        Pool tmp(st);
+        cplx* Y = tmp.c((int64_t)tb[s] * w * bb[e]);
+        nn(st, tb[s], w * bb[e], bb[s], L[s], 0, TB[s], 0, Y, 0, 1);
+        cn(st, tb[e], bb[e], w * tb[s], TT[s], 0, Y, 0, o, 0, 1);
+      });
     }
   }
 
-  void shared_right(cudaStream_t st, Pool& pool, int ell, std::vector<cplx*>& R, const std::vector<const cplx*>& TT,
-                    const std::vector<int>& tb, const std::vector<const cplx*>& TB, const std::vector<int>& bb) {
+  void shared_right(cudaStream_t st, Pool& pool, int ell, int tag, std::vector<cplx*>& R,
+                    const std::vector<const cplx*>& TT, const std::vector<int>& tb, const std::vector<const cplx*>& TB,
+                    const std::vector<int>& bb) {
     R.assign(n + 1, nullptr);
-    R[n] = pool.c(1);
-    set_small(st, R[n], 1, ONE);
+    R[n] = memo(st, pool, ell, n, tag, 1, [&](cplx* o) { set_small(st, o, 1, ONE); });
     auto blks = blocks(ell);
     for (int j = (int)blks.size() - 1; j >= 0; --j) {
       const int s = blks[j].first, k = blks[j].second;
       const int w = k < 0 ? 4 : 16, e = k < 0 ? s + 1 : s + 2;
-      cplx* Y = pool.c((int64_t)bb[s] * w * tb[e]);
-      nn(st, w * bb[s], tb[e], bb[e], TB[s], 0, R[e], 0, Y, 0, 1);
-      R[s] = pool.c((int64_t)bb[s] * tb[s]);
-      nc(st, bb[s], tb[s], w * tb[e], Y, 0, TT[s], 0, R[s], 0, 1);
+      R[s] = memo(st, pool, ell, s, tag, (int64_t)bb[s] * tb[s], [&](cplx* o) {
+        Pool tmp(st);
+        cplx* Y = tmp.c((int64_t)bb[s] * w * tb[e]);
+        nn(st, w * bb[s], tb[e], bb[e], TB[s], 0, R[e], 0, Y, 0, 1);
+        nc(st, bb[s], tb[s], w * tb[e], Y, 0, TT[s], 0, o, 0, 1);
+      });
     }
   }
 
@@ -1617,28 +1666,26 @@ struct Engine {
       Blk& q = bk[s];
       const int e = k < 0 ? s + 1 : s + 2;
       const int w = k < 0 ? 4 : 16;
-      auto mk2 = [&](const std::vector<const cplx*>& a, const std::vector<int>& bd) -> cplx* {
+      auto mk2 = [&](int tag, const std::vector<const cplx*>& a, const std::vector<int>& bd) -> cplx* {
         if (k < 0) return const_cast<cplx*>(a[s]);
-        cplx* o = pool.c((int64_t)16 * bd[s] * bd[e]);
-        pair(st, o, a[s], 0, a[s + 1], 0, bd[s], bd[s + 1], bd[e], 1);
-        return o;
+        return memo(st, pool, ell, s, tag, (int64_t)16 * bd[s] * bd[e],
+                    [&](cplx* o) { pair(st, o, a[s], 0, a[s + 1], 0, bd[s], bd[s + 1], bd[e], 1); });
       };
-      auto gated = [&](const cplx* x, int X, int Y) -> cplx* {
+      auto gated = [&](int tag, const cplx* x, int X, int Y) -> cplx* {
         if (k < 0) return const_cast<cplx*>(x);
-        cplx* o = pool.c((int64_t)16 * X * Y);
-        apply_gate(st, o, 0, x, 0, at(o_gdag) + (int64_t)k * 16, 0, X, Y, 1, ONE, false);
-        return o;
+        return memo(st, pool, ell, s, tag, (int64_t)16 * X * Y, [&](cplx* o) {
+          apply_gate(st, o, 0, x, 0, at(o_gdag) + (int64_t)k * 16, 0, X, Y, 1, ONE, false);
+        });
       };
-      q.TT = mk2(tpv, tb);
-      q.TTg = gated(q.TT, tb[s], tb[e]);
-      if (k >= 0) {
-        q.TTp = pool.c((int64_t)16 * tb[s] * tb[e]);
-        out_leg_split(st, q.TTp, q.TT, tb[s], tb[e]);
-      }
-      q.BB = mk2(bpv, bb);
+      q.TT = mk2(1, tpv, tb);
+      q.TTg = gated(2, q.TT, tb[s], tb[e]);
+      if (k >= 0)
+        q.TTp = memo(st, pool, ell, s, 3, (int64_t)16 * tb[s] * tb[e],
+                     [&](cplx* o) { out_leg_split(st, o, q.TT, tb[s], tb[e]); });
+      q.BB = mk2(4, bpv, bb);
       if (!skipB) {
-        q.BAaB = mk2(BAa, ya);
-        q.BAbB = mk2(BAb, xb);
+        q.BAaB = mk2(5, BAa, ya);
+        q.BAbB = mk2(6, BAb, xb);
         const int64_t sz = (int64_t)w * xb[s] * ya[e];
         q.BBd = pool.c(sz * nb);
         if (k < 0) {
@@ -1650,10 +1697,10 @@ struct Engine {
         }
       }
       if (!skipT) {
-        q.TAaB = mk2(TAa, va);
-        q.TAaG = gated(q.TAaB, va[s], va[e]);
-        q.TAbB = mk2(TAb, ub);
-        q.TAbG = gated(q.TAbB, ub[s], ub[e]);
+        q.TAaB = mk2(7, TAa, va);
+        q.TAaG = gated(8, q.TAaB, va[s], va[e]);
+        q.TAbB = mk2(9, TAb, ub);
+        q.TAbG = gated(10, q.TAbB, ub[s], ub[e]);
         const int64_t sz = (int64_t)w * ub[s] * va[e];
         q.TBd = pool.c(sz * nb);
         if (k < 0) {
@@ -1681,12 +1728,12 @@ struct Engine {
         TAaG[s] = bk[s].TAaG;
       }
       if (!skipB) {
-        shared_left(st, pool, ell, LBb, TTg, tb, BAbB, xb);
-        shared_right(st, pool, ell, RBa, TTg, tb, BAaB, ya);
+        shared_left(st, pool, ell, 20, LBb, TTg, tb, BAbB, xb);
+        shared_right(st, pool, ell, 21, RBa, TTg, tb, BAaB, ya);
       }
       if (!skipT) {
-        shared_left(st, pool, ell, LTb, TAbG, ub, BBs, bb);
-        shared_right(st, pool, ell, RTa, TAaG, va, BBs, bb);
+        shared_left(st, pool, ell, 22, LTb, TAbG, ub, BBs, bb);
+        shared_right(st, pool, ell, 23, RTa, TAaG, va, BBs, bb);
       }
     }
     const cplx* Vd = V;  // [nb][K][16]
@@ -1705,14 +1752,16 @@ struct Engine {
         dRV[s] = pool.c((int64_t)bb[s] * tb[s] * nb);
         nc(st, bb[s], tb[s], w * tb[e], Y, sY, q.TTg, 0, dRV[s], (int64_t)bb[s] * tb[s], nb);
         if (k >= 0) {  // (V Y0) TT^H = sum_ac V[a,c] Y0_c TT_a^H: 16 shared products, one K=16 GEMM
-          cplx* Y0 = rp.c(sY);
-          nn(st, w * bb[s], tb[e], bb[e], q.BB, 0, R0e, 0, Y0, 0, 1);
-          cplx* Y0p = rp.c(sY);
-          out_leg_split(st, Y0p, Y0, bb[s], tb[e]);
           const int64_t sq = (int64_t)bb[s] * tb[s], sy = (int64_t)bb[s] * 4 * tb[e], stt = (int64_t)tb[s] * 4 * tb[e];
-          cplx* Q = rp.c(16 * sq);
-          for (int a = 0; a < 4; ++a)  // Q[a*4+c] = Y0p[c] TTp[a]^H
-            nc(st, bb[s], tb[s], 4 * tb[e], Y0p, sy, q.TTp + a * stt, 0, Q + (int64_t)a * 4 * sq, sq, 4);
+          cplx* Q = memo(st, rp, ell, s, 60, 16 * sq, [&](cplx* o) {
+            Pool tmp(st);
+            cplx* Y0 = tmp.c(sY);
+            nn(st, w * bb[s], tb[e], bb[e], q.BB, 0, R0e, 0, Y0, 0, 1);
+            cplx* Y0p = tmp.c(sY);
+            out_leg_split(st, Y0p, Y0, bb[s], tb[e]);
+            for (int a = 0; a < 4; ++a)  // Q[a*4+c] = Y0p[c] TTp[a]^H
+              nc(st, bb[s], tb[s], 4 * tb[e], Y0p, sy, q.TTp + a * stt, 0, o + (int64_t)a * 4 * sq, sq, 4);
+          });
           mm(st, 'N', 'N', nb, (int)sq, 16, ONE, Vd + (int64_t)k * 16, KK, 0, Q, sq, 0, ONE, dRV[s], sq, 0, 1);
         }
       }
@@ -1731,8 +1780,8 @@ struct Engine {
         dRT[s] = pool.c((int64_t)bb[s] * ub[s] * nb);
         nc(st, bb[s], ub[s], w * ub[e], Y, sY, q.TAbG, 0, dRT[s], (int64_t)bb[s] * ub[s], nb);
         const int64_t sY2 = (int64_t)bb[s] * w * va[e];
-        cplx* Y2 = rp.c(sY2);
-        nn(st, w * bb[s], va[e], bb[e], q.BB, 0, RTa[e], 0, Y2, 0, 1);
+        cplx* Y2 = memo(st, rp, ell, s, 61, sY2,
+                        [&](cplx* o) { nn(st, w * bb[s], va[e], bb[e], q.BB, 0, RTa[e], 0, o, 0, 1); });
         nc(st, bb[s], ub[s], w * va[e], Y2, 0, q.TBdG, (int64_t)w * ub[s] * va[e], dRT[s], (int64_t)bb[s] * ub[s],
            nb, ONE, ONE);
       }
@@ -1757,10 +1806,8 @@ struct Engine {
       cplx* YV = bpool.c(sYV * nb);  // dLV BB
       nn(st, tb[s], w * bb[e], bb[s], dLV, (int64_t)tb[s] * bb[s], q.BB, 0, YV, sYV, nb);
       cplx* Y0 = nullptr;  // L0 BB (shared)
-      if (k >= 0) {
-        Y0 = bpool.c(sYV);
-        nn(st, tb[s], w * bb[e], bb[s], L0s, 0, q.BB, 0, Y0, 0, 1);
-      }
+      if (k >= 0)
+        Y0 = memo(st, bpool, ell, s, 70, sYV, [&](cplx* o) { nn(st, tb[s], w * bb[e], bb[s], L0s, 0, q.BB, 0, o, 0, 1); });
       cplx* YB = nullptr;
       int64_t sYB = 0;
       if (!skipB) {  // dLB BAaB + LBb BBd : (t x w x ya')
@@ -1776,16 +1823,16 @@ struct Engine {
         sYT = (int64_t)va[s] * w * bb[e];
         YT = bpool.c(sYT * nb);
         nn(st, va[s], w * bb[e], bb[s], dLT, (int64_t)va[s] * bb[s], q.BB, 0, YT, sYT, nb);
-        YT0 = bpool.c((int64_t)ub[s] * w * bb[e]);
-        nn(st, ub[s], w * bb[e], bb[s], LTb[s], 0, q.BB, 0, YT0, 0, 1);
+        YT0 = memo(st, bpool, ell, s, 71, (int64_t)ub[s] * w * bb[e],
+                   [&](cplx* o) { nn(st, ub[s], w * bb[e], bb[s], LTb[s], 0, q.BB, 0, o, 0, 1); });
       }
       if (k >= 0) {
         // ---- extraction.  Terms whose right environment R is shared across
         // directions use Wt = Theta_top R^H (once per block) so that
         // sum conj(top) (Y R) = sum conj(Wt) Y  -- no per-direction Y R product.
         {
-          cplx* Wt = bpool.c((int64_t)16 * tb[s] * bb[e]);                 // TT R0^H
-          nc(st, 16 * tb[s], bb[e], tb[e], q.TT, 0, R0e, 0, Wt, 0, 1);
+          cplx* Wt = memo(st, bpool, ell, s, 72, (int64_t)16 * tb[s] * bb[e],   // TT R0^H
+                          [&](cplx* o) { nc(st, 16 * tb[s], bb[e], tb[e], q.TT, 0, R0e, 0, o, 0, 1); });
           extract_env(st, HT + (int64_t)k * 16, KK, Wt, 0, YV, sYV, tb[s], bb[e], nb, ONE);
         }
         {  // per-direction right environments: Z = Y0 dRV (+ LBb BAbB dRB)
@@ -1793,27 +1840,27 @@ struct Engine {
           cplx* Z = bpool.c(sZ * nb);
           nn(st, 16 * tb[s], tb[e], bb[e], Y0, 0, dRV[e], (int64_t)bb[e] * tb[e], Z, sZ, nb);
           if (!skipB) {
-            cplx* LBA = bpool.c((int64_t)16 * tb[s] * xb[e]);
-            nn(st, tb[s], 16 * xb[e], xb[s], LBb[s], 0, q.BAbB, 0, LBA, 0, 1);
+            cplx* LBA = memo(st, bpool, ell, s, 73, (int64_t)16 * tb[s] * xb[e],
+                             [&](cplx* o) { nn(st, tb[s], 16 * xb[e], xb[s], LBb[s], 0, q.BAbB, 0, o, 0, 1); });
             nn(st, 16 * tb[s], tb[e], xb[e], LBA, 0, dRB[e], (int64_t)xb[e] * tb[e], Z, sZ, nb, ONE, ONE);
           }
           extract_env(st, HT + (int64_t)k * 16, KK, q.TT, 0, Z, sZ, tb[s], tb[e], nb, ONE);
         }
         if (!skipB) {  // (dLB BAaB + LBb BBd) RBa  ->  Wt = TT RBa^H
-          cplx* Wt = bpool.c((int64_t)16 * tb[s] * ya[e]);
-          nc(st, 16 * tb[s], ya[e], tb[e], q.TT, 0, RBa[e], 0, Wt, 0, 1);
+          cplx* Wt = memo(st, bpool, ell, s, 74, (int64_t)16 * tb[s] * ya[e],
+                          [&](cplx* o) { nc(st, 16 * tb[s], ya[e], tb[e], q.TT, 0, RBa[e], 0, o, 0, 1); });
           extract_env(st, HT + (int64_t)k * 16, KK, Wt, 0, YB, sYB, tb[s], ya[e], nb, ONE);
         }
         if (!skipT) {
           {  // top TAaB with (dLT BB) RTa  ->  Wt = TAaB RTa^H
-            cplx* Wt = bpool.c((int64_t)16 * va[s] * bb[e]);
-            nc(st, 16 * va[s], bb[e], va[e], q.TAaB, 0, RTa[e], 0, Wt, 0, 1);
+            cplx* Wt = memo(st, bpool, ell, s, 75, (int64_t)16 * va[s] * bb[e],
+                            [&](cplx* o) { nc(st, 16 * va[s], bb[e], va[e], q.TAaB, 0, RTa[e], 0, o, 0, 1); });
             extract_env(st, HT + (int64_t)k * 16, KK, Wt, 0, YT, sYT, va[s], bb[e], nb, ONE);
           }
           // per-dir top TBd with shared (LTb BB) RTa
           const int64_t sZ3 = (int64_t)16 * ub[s] * va[e];
-          cplx* Z3 = bpool.c(sZ3);
-          nn(st, 16 * ub[s], va[e], bb[e], YT0, 0, RTa[e], 0, Z3, 0, 1);
+          cplx* Z3 = memo(st, bpool, ell, s, 76, sZ3,
+                          [&](cplx* o) { nn(st, 16 * ub[s], va[e], bb[e], YT0, 0, RTa[e], 0, o, 0, 1); });
           extract_env(st, HT + (int64_t)k * 16, KK, q.TBd, sZ3, Z3, 0, ub[s], va[e], nb, ONE);
           // top TAbB with (LTb BB) dRT
           const int64_t sZ4 = (int64_t)16 * ub[s] * ub[e];
@@ -1827,12 +1874,14 @@ struct Engine {
         cplx* nL = dnew((int64_t)tb[e] * bb[e] * nb, st);
         cn(st, tb[e], bb[e], w * tb[s], q.TTg, 0, YV, sYV, nL, (int64_t)tb[e] * bb[e], nb);
         if (k >= 0) {  // TT^H (V Y0) = sum_ac V[a,c] TT_a^H Y0_c: 16 shared products, one K=16 GEMM
-          cplx* Y0p = bpool.c(sYV);
-          out_leg_split(st, Y0p, Y0, tb[s], bb[e]);
           const int64_t sp = (int64_t)tb[e] * bb[e], sy = (int64_t)tb[s] * 4 * bb[e], stt = (int64_t)tb[s] * 4 * tb[e];
-          cplx* Pm = bpool.c(16 * sp);
-          for (int a = 0; a < 4; ++a)  // P[a*4+c] = TTp[a]^H Y0p[c]
-            cn(st, tb[e], bb[e], 4 * tb[s], q.TTp + a * stt, 0, Y0p, sy, Pm + (int64_t)a * 4 * sp, sp, 4);
+          cplx* Pm = memo(st, bpool, ell, s, 77, 16 * sp, [&](cplx* o) {
+            Pool tmp(st);
+            cplx* Y0p = tmp.c(sYV);
+            out_leg_split(st, Y0p, Y0, tb[s], bb[e]);
+            for (int a = 0; a < 4; ++a)  // P[a*4+c] = TTp[a]^H Y0p[c]
+              cn(st, tb[e], bb[e], 4 * tb[s], q.TTp + a * stt, 0, Y0p, sy, o + (int64_t)a * 4 * sp, sp, 4);
+          });
           mm(st, 'N', 'N', nb, (int)sp, 16, ONE, Vd + (int64_t)k * 16, KK, 0, Pm, sp, 0, ONE, nL, sp, 0, 1);
         }
         dset(dLV, nL, st);
