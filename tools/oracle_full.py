@@ -24,11 +24,16 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=4)
 ap.add_argument("--dirs", type=int, default=1)
 ap.add_argument("--out", default=None)
+ap.add_argument("--save-ref", default=None, help="also np.save the reference sites (object array) here")
 a = ap.parse_args()
 cfg = C.CONFIGS[a.config]
 t0 = time.time()
 ref = [x.detach().resolve_conj().cpu().numpy() for x in C.reference_mpo(cfg, device="cpu")]
 t_ref = time.time() - t0
+if a.save_ref:
+    arr = np.empty(len(ref), dtype=object)
+    arr[:] = ref
+    np.save(a.save_ref, arr, allow_pickle=True)
 K = C.num_gates(cfg.n, cfg.depth)
 G = C.haar_gates(cfg.cid, K)
 V = C.tangent_directions(cfg.cid, G, a.dirs)

@@ -20,13 +20,17 @@ from tn_inputs import configs as C  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=4)
 ap.add_argument("--file", default=None)
+ap.add_argument("--ref", default=None, help="reference sites saved by oracle_full.py --save-ref (same CPU build)")
 a = ap.parse_args()
 cfg = C.CONFIGS[a.config]
 path = a.file or os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
                               f"r01_oracle_c{cfg.cid}.npz")
 o = np.load(path)
 t0 = time.time()
-ref_cpu = C.reference_mpo(cfg, device="cpu")
+if a.ref:
+    ref_cpu = [torch.from_numpy(x) for x in np.load(a.ref, allow_pickle=True)]
+else:
+    ref_cpu = C.reference_mpo(cfg, device="cpu")
 t_ref = time.time() - t0
 ref_sum = np.array([float(x.abs().sum()) for x in ref_cpu])
 dev = torch.device("cuda")
@@ -51,5 +55,5 @@ print(json.dumps({
     "reference_rebuild_rel_diff": float(np.abs(ref_sum - o["ref_sum"]).max() / np.abs(o["ref_sum"]).max()),
     "t_reference_cpu_s": t_ref, "oracle_f": float(o["f"]), "gpu_f": f,
     "f_rel": abs(f - float(o["f"])) / abs(float(o["f"])), "grad_R_rel": rel(gR, o["grad_R"]),
-    "hess_R_rel": [rel(H[b], o["HR"][b]) for b in range(nd)],
+    "hess_R_rel": [rel(H[b], o["HR"][b]) for b in range(nd)] if nd else None,
     "diag": sc[3:8].cpu().tolist()}))
