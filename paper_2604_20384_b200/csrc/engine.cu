@@ -825,17 +825,22 @@ struct Engine {
               return gap2 > 0 ? 2.2e-16 / gap2 : 1.0;
             };
             double delta = mixing(hS[0]);
-            if (delta > 1e-2) {
-              int n_hi = 0;
-              while (n_hi < R && hS[n_hi] >= 1e-4 * hS[0]) ++n_hi;
-              if (n_hi > 0 && n_hi < s.r) {
-                refine_kept(st, tmp, uhf, Sf, A, R, 4 * s.br, R, n_hi, 2);
-                deflate_low(st, so, tmp, uhf, Sf, A, R, 4 * s.br, n_hi, info + 1);
-                TN_CUDA(cudaMemcpyAsync(hS.data(), Sf, R * sizeof(double), cudaMemcpyDeviceToHost, st));
-                TN_CUDA(cudaStreamSynchronize(st));
-                delta = mixing(hS[n_hi]);
-                ++n_deflate;
-              }
+            // Deflation levels: while the cut is unresolved relative to the
+            // current level's top, refine the rows above 1e-4 of that top and
+            // re-solve the block below them with its own Gram matrix (each
+            // level resolves ~1e-4 further down the spectrum).
+            int top_i = 0;
+            for (int level = 0; level < 3 && delta > 1e-2; ++level) {
+              int n_hi = top_i;
+              while (n_hi < R && hS[n_hi] >= 1e-4 * hS[top_i]) ++n_hi;
+              if (!(n_hi > top_i && n_hi < s.r)) break;
+              refine_kept(st, tmp, uhf, Sf, A, R, 4 * s.br, R, n_hi, 2);
+              deflate_low(st, so, tmp, uhf, Sf, A, R, 4 * s.br, n_hi, info + 1);
+              TN_CUDA(cudaMemcpyAsync(hS.data(), Sf, R * sizeof(double), cudaMemcpyDeviceToHost, st));
+              TN_CUDA(cudaStreamSynchronize(st));
+              delta = mixing(hS[n_hi]);
+              top_i = n_hi;
+              ++n_deflate;
             }
             // A boundary inside the double-precision noise floor (after the second
             // level: sigma_{r-1} < 1e-12 sigma_1) is not determined by the data for
