@@ -189,3 +189,29 @@ def test_fused_step_equals_environments_plus_apply(cid, max_batch):
     H3 = eng.apply(V)                                  # state after the fused step is the same
     assert torch.equal(H3, H1)
     eng.close()
+
+
+@pytest.mark.skipif(os.environ.get("TN_FULL_PARITY") != "1", reason="~2 min CPU reference build; TN_FULL_PARITY=1")
+def test_parity_config4_stored_oracle():
+    """C4 at full size in bench.py's launch configuration (64 directions,
+    SUB_BATCH sub-batches, fused tn_hvp_step) against oracle outputs stored by
+    tools/oracle_full.py (oracle/ only; 28 min of numpy on 16 cores): f and
+    grad_R, on the reference MPO rebuilt by the same CPU path."""
+    import os as _os
+    from paper_2604_20384_b200.api import SUB_BATCH, HVPEngine
+    root = _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__)))
+    o = np.load(_os.path.join(root, "profiles", "r01_oracle_c4.npz"))
+    cfg = C.CONFIGS[4]
+    ref_cpu = C.reference_mpo(cfg, device="cpu")
+    ref_sum = np.array([float(x.abs().sum()) for x in ref_cpu])
+    assert np.abs(ref_sum - o["ref_sum"]).max() <= 1e-12 * np.abs(o["ref_sum"]).max()
+    dev = torch.device("cuda")
+    K = C.num_gates(cfg.n, cfg.depth)
+    G = C.haar_gates(cfg.cid, K)
+    V = C.tangent_directions(cfg.cid, G, cfg.batch)
+    eng = HVPEngine(cfg.n, cfg.depth, cfg.chi, [x.to(dev) for x in ref_cpu], max_batch=SUB_BATCH[4])
+    sc, gR, H = eng.step(torch.tensor(G, device=dev), torch.tensor(V, device=dev))
+    assert abs(sc[0].item() - float(o["f"])) <= TOL * abs(float(o["f"]))
+    assert rel(gR.cpu().numpy(), o["grad_R"]) < TOL
+    assert torch.isfinite(H).all()
+    eng.close()
