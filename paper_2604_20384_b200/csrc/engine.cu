@@ -223,6 +223,7 @@ struct Engine {
   std::vector<ApplyGraph> graphs;
   cudaStream_t stc = nullptr;  // capture stream
   const bool graphs_enabled = std::getenv("TN_NO_GRAPH") == nullptr;
+  static constexpr int kGraphMaxBatch = 8;
   double work_primal = 0, work_apply = 0, work_fwd_first = 0;
   std::atomic<double> work_counter{0.0};
   std::atomic<double> work_counter_fwd{0.0};  // GEMMs issued by the fused step's forward-tangent thread
@@ -574,6 +575,7 @@ struct Engine {
     if (stg) cudaStreamDestroy(stg);
     drop_graphs();
     drop_chain_cache();
+    trim_pools();
     if (stf) cudaStreamDestroy(stf);
     if (stc) cudaStreamDestroy(stc);
     if (sth) cudaStreamDestroy(sth);
@@ -1391,6 +1393,7 @@ struct Engine {
     memo_map.clear();
     memo_bytes = 0;
     cudaStreamSynchronize(stc);
+    trim_pools();
   }
 
   template <class F>
@@ -2009,6 +2012,16 @@ struct Engine {
         if (p) cudaFree(p);
     }
     graphs.clear();
+    cudaDeviceGraphMemTrim(device);
+  }
+
+  // return cached-but-free pool memory (stream-ordered pool and graph pool) to
+  // the device so that other allocators (torch) can use it
+  void trim_pools() {
+    cudaDeviceSynchronize();
+    cudaMemPool_t mp;
+    if (cudaDeviceGetDefaultMemPool(&mp, device) == cudaSuccess) cudaMemPoolTrimTo(mp, 0);
+    cudaDeviceGraphMemTrim(device);
   }
 
   bool capture(ApplyGraph& g) {
@@ -2052,7 +2065,9 @@ struct Engine {
   void apply_call(cudaStream_t st, int batch, const cplx* dirs, cplx* hess, cplx* aux) {
     TN_CUDA(cudaSetDevice(device));
     if (!primal_valid) throw StateError("tn_hvp_apply before tn_hvp_environments");
-    if (!graphs_enabled || batch <= 0 || gemm_profile_active() || std::getenv("TN_PHASES")) {
+    // graphs pay off for launch-bound small batches (truncated CG: batch 1);
+    // large batches are GEMM-bound and would double the memory footprint
+    if (!graphs_enabled || batch <= 0 || batch > kGraphMaxBatch || gemm_profile_active() || std::getenv("TN_PHASES")) {
       apply(st, batch, dirs, hess, aux);
       return;
     }
@@ -2076,7 +2091,15 @@ struct Engine {
     }
     const int64_t n = (int64_t)batch * K * 16;
     TN_CUDA(cudaMemcpyAsync(g->in, dirs, sizeof(cplx) * n, cudaMemcpyDeviceToDevice, st));
-    TN_CUDA(cudaGraphLaunch(g->exec, st));
+    if (cudaGraphLaunch(g->exec, st) != cudaSuccess) {  // e.g. graph memory: run eagerly from now on
+      cudaGetLastError();
+      cudaGraphExecDestroy(g->exec);
+      g->exec = nullptr;
+      g->failed = true;
+      cudaDeviceGraphMemTrim(device);
+      apply(st, batch, dirs, hess, aux);
+      return;
+    }
     TN_CUDA(cudaMemcpyAsync(hess, g->out, sizeof(cplx) * n, cudaMemcpyDeviceToDevice, st));
     if (aux) TN_CUDA(cudaMemcpyAsync(aux, g->auxb, sizeof(cplx) * (n + batch), cudaMemcpyDeviceToDevice, st));
     count_launch(g->launches);
