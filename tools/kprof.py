@@ -15,7 +15,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=3)
 ap.add_argument("--batch", type=int, default=64)
 ap.add_argument("--max-batch", type=int, default=64)
-ap.add_argument("--what", default="apply", choices=["apply", "env"])
+ap.add_argument("--what", default="apply", choices=["apply", "env", "step"])
 a = ap.parse_args()
 cfg = C.CONFIGS[a.config]
 dev = torch.device("cuda")
@@ -28,21 +28,30 @@ eng = HVPEngine(cfg.n, cfg.depth, cfg.chi, ref, max_batch=a.max_batch)
 eng.environments(G)
 eng.apply(V)
 torch.cuda.synchronize()
+import time  # noqa: E402
+t0 = time.time()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     if a.what == "env":
         eng.environments(G)
+    elif a.what == "step":       # bench.py's step: fused tn_hvp_step
+        eng.step(G, V)
     else:
         eng.apply(V)
     torch.cuda.synchronize()
+wall = time.time() - t0
 agg = collections.defaultdict(lambda: [0, 0.0])
 for ev in prof.events():
     if ev.device_type == torch.autograd.DeviceType.CUDA:
-        name = ev.name.split("(")[0]
-        if "zgemm_kernel" in ev.name:
-            name = "zgemm_kernel" + ev.name[ev.name.find("<"):ev.name.find(">") + 1]
+        full = ev.name.replace("(anonymous namespace)::", "").replace("void ", "")
+        name = full.split("(")[0]
+        if "zgemm3m_kernel" in full:
+            name = "tn::zgemm3m_kernel (DMMA complex GEMM)"
+        elif "<" in name:
+            name = name[:name.find("<")]
         agg[name][0] += 1
         agg[name][1] += ev.device_time_total if hasattr(ev, "device_time_total") else ev.cuda_time_total
 tot = sum(v[1] for v in agg.values())
-print(f"{a.what} config {cfg.name} batch {a.batch}: kernels {sum(v[0] for v in agg.values())}, busy {tot/1e3:.1f} ms")
+print(f"{a.what} config {cfg.name} batch {a.batch} (sub-batch {a.max_batch}): kernels {sum(v[0] for v in agg.values())}, "
+      f"summed kernel time {tot/1e3:.1f} ms, wall {wall*1e3:.1f} ms (streams overlap in the primal pass)")
 for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1])[:25]:
     print(f"{k[:70]:70s} {n:7d} {t/1e3:9.2f} ms {100*t/tot:5.1f}%")
