@@ -1393,7 +1393,8 @@ struct Engine {
     memo_map.clear();
     memo_bytes = 0;
     cudaStreamSynchronize(stc);
-    trim_pools();
+    // no pool trim here: this runs on every primal pass, and returning the
+    // pooled memory would make the next step re-map it (~3 s per C4 step)
   }
 
   template <class F>
