@@ -4,11 +4,18 @@ and the fraction of the FP64 roofline) on 1..N B200s.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
 
 A step is one pass of the whole hot path over one
-batch: tn_hvp_environments (primal sweeps, layer environments, f, grad_R) then
-tn_hvp_apply on the config's batch of tangent directions.  Multi-GPU: one
-process per GPU (torchrun), each rank runs the full per-GPU batch on its own
-directions with its own primal (weak scaling; the path has no exchange step
-inside the HVP).  value = directions of all ranks / max-over-ranks step time.
+batch of the config's B tangent directions (C4: 64): the primal pass
+(tn_hvp_environments: sweeps, layer environments, f, grad_R) and the Riemannian
+HVPs of all B directions.
+  * N = 1: the fused tn_hvp_step (the first sub-batch's forward tangents
+    overlap the primal pass).
+  * N > 1 (torchrun, one process per GPU): strong scaling as north_star and
+    SURVEY.md §8(e) describe -- the primal pass once on rank 0, its store
+    broadcast in place with NCCL, B/N directions applied per rank, Hess_R
+    all-gathered with NCCL (parallel.sharded_step).
+value = B / max-over-ranks step time.  Phase times (primal, broadcast,
+apply, gather), the apply-only HVPs/s of SURVEY.md §8(d) and the broadcast
+bytes are measured after the timed region and reported beside it.
 """
 from __future__ import annotations
 
@@ -156,6 +163,47 @@ def oracle_sample(cfg, ref_cpu, G, budget_s=20.0):
     return 1.0 / (t_gate * 2 * K), dt, done
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def oracle_baseline(cfg, ref_cpu, G, budget_s=10.0):
+    """cpu_baseline object: the oracle sample at 1 BLAS thread and at all
+    cores of this host (threadpoolctl), plus the full-size oracle timings
+    recorded when tests/golden/ was generated (tools/golden_full.py)."""
+    from threadpoolctl import threadpool_limits
+    ncores = os.cpu_count()
+    with threadpool_limits(limits=1):
+        r1, dt1, n1 = oracle_sample(cfg, ref_cpu, G, budget_s)
+    with threadpool_limits(limits=ncores):
+        ra, dta, na = oracle_sample(cfg, ref_cpu, G, budget_s)
+    out = {"value": ra, "unit": "HVPs/s", "cores": ncores, "kind": "oracle",
+           "sample": (f"O3 numpy oracle sweep steps (SVD truncation + tangent update, 1 direction) on the first "
+                      f"top layer at full bonds: {na} gates in {dta:.1f} s at {ncores} threads, {n1} gates in "
+                      f"{dt1:.1f} s at 1 thread; HVPs/s = 1/(t_gate x 2K), an upper bound (excludes the layer "
+                      f"environment / extraction work)"),
+           "hvps_per_s_1thread": r1, "hvps_per_s_all_cores": ra, "nproc": ncores, "cpu_model": cpu_model(),
+           "s_per_hvp_1thread_upper_bound": 1 / r1, "s_per_hvp_all_cores_upper_bound": 1 / ra}
+    gpath = os.path.join(ROOT, "tests", "golden", f"full_c{cfg.cid}.json")
+    if os.path.exists(gpath):
+        with open(gpath) as f:
+            g = json.load(f)
+        td = g.get("t_dir_s") or []
+        out["oracle_full_size"] = {
+            "what": "measured full oracle run that wrote tests/golden (tools/golden_full.py), on the build "
+                    "container, not this host", "primal_s": g.get("t_primal_s"), "primal_and_E_s": g.get("t_env_s"),
+            "per_hvp_s": (sum(td) / len(td)) if td else None, "threads": g.get("threads"), "nproc": g.get("nproc"),
+            "hvps_per_s": (len(td) / sum(td)) if td else None}
+    return out
+
+
 def run_reference(args, cfg, rank, world):
     if rank != 0:
         return
@@ -163,23 +211,38 @@ def run_reference(args, cfg, rank, world):
     ref_cpu = [a.detach().resolve_conj().cpu().numpy() for a in ref]
     G = C.haar_gates(cfg.cid, C.num_gates(cfg.n, cfg.depth, cfg.first_offset))
     rates, times = [], []
+    done = 0
     for _ in range(args.steps):
         r, dt, done = oracle_sample(cfg, ref_cpu, G)
         rates.append(r)
         times.append(dt)
     v = statistics.median(rates)
-    cores = torch.get_num_threads()
+    cores = os.cpu_count()
     sample = (f"O3 numpy oracle sweep steps (SVD truncation + tangent update, 1 direction) on {done} gates of the "
-              f"first top layer at full bonds, ~20 s; HVPs/s = 1/(t_gate x 2K): upper bound, excludes the layer "
-              f"environment/extraction work")
+              f"first top layer at full bonds, ~20 s, {cores} cores ({cpu_model()}); HVPs/s = 1/(t_gate x 2K): upper "
+              f"bound, excludes the layer environment/extraction work")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "HVPs/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": cfg.name, "n": cfg.n, "depth": cfg.depth, "chi": cfg.chi},
         "cpu_baseline": {"value": v, "unit": "HVPs/s", "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": v, "unit": "HVPs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
+
+
+class Phase:
+    """CUDA-event interval on the current stream (synchronised on exit)."""
+
+    def __enter__(self):
+        self.e0, self.e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        self.e0.record()
+        return self
+
+    def __exit__(self, *a):
+        self.e1.record()
+        self.e1.synchronize()
+        self.ms = self.e0.elapsed_time(self.e1)
 
 
 # ----------------------------------------------------------------- ours --
@@ -195,25 +258,31 @@ def main():
         return
     from paper_2604_20384_b200 import _native as N
     from paper_2604_20384_b200.api import SUB_BATCH, HVPEngine
+    from paper_2604_20384_b200.parallel import broadcast_primal, gather_rows, shard, sharded_step
 
     dev = torch.device("cuda", torch.cuda.current_device())
-    B = args.batch or cfg.batch
+    B = args.batch or cfg.batch                       # directions per step (all ranks together)
     mb = args.max_batch or SUB_BATCH[cfg.cid]
     K = C.num_gates(cfg.n, cfg.depth, cfg.first_offset)
     ref = C.reference_mpo(cfg, device=dev)
     Gnp = C.haar_gates(cfg.cid, K)
-    Vnp = C.tangent_directions(cfg.cid, Gnp, B, offset=rank * B)   # each rank: its own directions
+    Vnp = C.tangent_directions(cfg.cid, Gnp, B)
     G = torch.tensor(Gnp, device=dev)
     V = torch.tensor(Vnp, device=dev)
     eng = HVPEngine(cfg.n, cfg.depth, cfg.chi, ref, cfg.first_offset, max_batch=mb)
     out = torch.empty_like(V)
+    s0, cnt = shard(B, rank, world)
+    Vmine = V[s0:s0 + cnt].contiguous()
 
-    def step():
+    def step(Gd=G, Vd=V):
+        if world > 1:
+            return sharded_step(eng, Gd, Vd, out=out)
         if args.unfused:
-            eng.environments(G)
-            eng.apply(V, out=out)
-        else:
-            eng.step(G, V, out=out)
+            sc, _ = eng.environments(Gd)
+            eng.apply(Vd, out=out)
+            return sc, out
+        sc, _, _ = eng.step(Gd, Vd, out=out)
+        return sc, out
 
     for _ in range(max(args.warmup - 1, 0)):
         step()
@@ -221,15 +290,23 @@ def main():
     # the last warm-up step is instrumented (untimed) and unfused, so that the
     # apply phase's GEMMs run alone on one stream: per-launch GEMM time (CUDA
     # events around every GEMM) and exact complex MACs of each phase
+    barrier(world)
+    env_gemm_ms = env_gemm_cmac = 0.0
+    if rank == 0:
+        N.tn_gemm_profile(1)
+        eng.environments(G)
+        torch.cuda.synchronize()
+        env_gemm_ms, env_gemm_cmac = N.tn_gemm_profile(0)
+    if world > 1:
+        broadcast_primal(eng, G)
     N.tn_gemm_profile(1)
-    eng.environments(G)
-    torch.cuda.synchronize()
-    env_gemm_ms, env_gemm_cmac = N.tn_gemm_profile(0)
-    N.tn_gemm_profile(1)
-    eng.apply(V, out=out)
+    if cnt:
+        eng.apply(Vmine)
     torch.cuda.synchronize()
     gemm_ms, gemm_cmac = N.tn_gemm_profile(0)
     cmac_dir, cmac_primal = eng.work()
+    if rank != 0:
+        cmac_primal = 0.0
 
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -245,7 +322,7 @@ def main():
         launches = N.tn_hvp_launch_count() - l0
     barrier(world)
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
-    value = world * B / (ms / 1e3)
+    value = B / (ms / 1e3)
 
     # end-to-end through the public API with host buffers (pinned), copies inside the timed region
     e2e = None
@@ -259,12 +336,8 @@ def main():
         def step_e2e():
             Gd.copy_(Gh, non_blocking=True)
             Vd.copy_(Vh, non_blocking=True)
-            if args.unfused:
-                sc, _ = eng.environments(Gd)
-                eng.apply(Vd, out=out)
-            else:
-                sc, _, _ = eng.step(Gd, Vd, out=out)
-            Hh.copy_(out, non_blocking=True)
+            sc, H = step(Gd, Vd)
+            Hh.copy_(H, non_blocking=True)
             Sh.copy_(sc, non_blocking=True)
 
         torch.cuda.synchronize()
@@ -276,28 +349,68 @@ def main():
         torch.cuda.synchronize()
         barrier(world)
         ms_e2e = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
-        e2e = {"value": world * B / (ms_e2e / 1e3), "unit": "HVPs/s",
+        e2e = {"value": B / (ms_e2e / 1e3), "unit": "HVPs/s",
                "h2d_bytes_per_step": int(Gh.numel() * 16 + Vh.numel() * 16),
                "d2h_bytes_per_step": int(Hh.numel() * 16 + 8 * 8)}
 
+    # phases of one (untimed) step, each bracketed by a barrier: primal pass on
+    # rank 0, broadcast of the store, apply of this rank's share, all_gather
+    barrier(world)
+    with Phase() as p_env:
+        if rank == 0:
+            eng.environments(G)
+    t_env = max_over_ranks(p_env.ms, world)
+    barrier(world)
+    with Phase() as p_bc:
+        if world > 1:
+            broadcast_primal(eng, G)
+    t_bc = max_over_ranks(p_bc.ms, world)
+    barrier(world)
+    with Phase() as p_ap:
+        local_H = eng.apply(Vmine) if cnt else V[:0]
+    t_ap = max_over_ranks(p_ap.ms, world)
+    barrier(world)
+    with Phase() as p_ga:
+        if world > 1:
+            gather_rows(local_H, B)
+    t_ga = max_over_ranks(p_ga.ms, world)
+    phases = {"primal_ms": t_env, "broadcast_ms": t_bc if world > 1 else 0.0,
+              "broadcast_bytes": int(eng.primal_bytes) if world > 1 else 0, "apply_ms": t_ap,
+              "gather_ms": t_ga if world > 1 else 0.0, "directions_per_rank": cnt,
+              "apply_only_hvps_per_s": B / (t_ap / 1e3),
+              "apply_only": "SURVEY.md §8(d) HVPs/s: B directions / max-over-ranks apply time of the rank shares, "
+                            "primal built once and excluded",
+              "apply_plus_broadcast_hvps_per_s": B / ((t_ap + (t_bc if world > 1 else 0.0)) / 1e3)}
+
     peak, peak_src = fp64_peak()
     achieved = 8 * gemm_cmac / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
-    traffic = None
+    traffic = traffic_alg = None
     tpath = os.path.join(ROOT, "profiles", f"traffic_c{cfg.cid}.json")  # ncu dram bytes/launch (committed)
     if os.path.exists(tpath):
         with open(tpath) as f:
-            traffic = json.load(f).get("bytes_per_launch")
+            tj = json.load(f)
+        traffic = tj.get("dram_bytes_per_launch")
+        traffic_alg = tj.get("algorithmic_bytes_per_launch")
+    flops_step = 8 * (cmac_dir * B + max_over_ranks(cmac_primal, world))
     line = {
         "metric": METRIC, "value": value, "unit": "HVPs/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": cfg.name, "n": cfg.n, "depth": cfg.depth, "chi": cfg.chi, "gates": K,
-                   "directions_per_gpu": B, "sub_batch": mb, "parallelism": f"weak x{world} (directions)",
-                   "step": "tn_hvp_environments + tn_hvp_apply" if args.unfused else
-                           "tn_hvp_step (fused: first sub-batch's forward tangents overlap the primal pass)",
+                   "directions_per_step": B, "sub_batch": mb,
+                   "parallelism": ("strong: primal once on rank 0 + NCCL broadcast of the store, "
+                                   f"{B}/{world} directions per rank, NCCL all_gather of Hess_R") if world > 1
+                                  else "1 GPU",
+                   "step": ("parallel.sharded_step" if world > 1 else
+                            "tn_hvp_environments + tn_hvp_apply" if args.unfused else
+                            "tn_hvp_step (fused: first sub-batch's forward tangents overlap the primal pass)"),
                    "l2": "working set (primal store, tangent caches: GBs) > 126 MB L2; no flush"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "traffic_algorithmic_bytes_per_launch": traffic_alg,
+                     "traffic_source": f"profiles/traffic_c{cfg.cid}.json (ncu dram__bytes_read+write per "
+                                       f"zgemm3m launch over a sample of APPLY launches, same population as "
+                                       f"'achieved')",
                      "kernel": "tn::zgemm3m_kernel (DMMA m8n8k4 f64, 3M: 3 real DMMA per complex k-step; "
                                "algorithmic 8 flop per complex MAC, so frac can exceed 1 up to 4/3)",
                      "peak_source": peak_src,
@@ -305,22 +418,20 @@ def main():
                                     "one stream; CUDA events around every GEMM launch)",
                      "apply_gemm_ms": gemm_ms, "primal_gemm_ms": env_gemm_ms,
                      "gemm_share_of_step": gemm_ms / ms if ms else None,   # apply-phase GEMM time / step
-                     "flops_per_step": 8 * (gemm_cmac + env_gemm_cmac), "apply_cmac_per_direction": cmac_dir,
-                     "primal_cmac": cmac_primal},
+                     "flops_per_step": flops_step, "apply_cmac_per_direction": cmac_dir,
+                     "primal_cmac": cmac_primal,
+                     "step_frac": flops_step / (ms / 1e3) / 1e12 / peak / world},
+        "phases": phases,
         "clocks": clk.summary(),
         "gpu_launches": int(launches),      # library kernel launches inside the timed region (all steps)
         "e2e": e2e,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ref_cpu = [a.detach().resolve_conj().cpu().numpy() for a in ref]
-        v, dt, done = oracle_sample(cfg, ref_cpu, Gnp)
-        line["cpu_baseline"] = {"value": v, "unit": "HVPs/s", "cores": torch.get_num_threads(), "kind": "oracle",
-                                "sample": f"O3 numpy oracle sweep steps (SVD truncation + tangent update, 1 "
-                                          f"direction) on {done} gates of the first top layer at full bonds, "
-                                          f"{dt:.1f} s; HVPs/s = 1/(t_gate x 2K): upper bound, excludes the layer "
-                                          f"environment/extraction work"}
+        line["cpu_baseline"] = oracle_baseline(cfg, ref_cpu, Gnp)
     if rank == 0:
         print(json.dumps(line))
+    eng.close()
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

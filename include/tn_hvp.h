@@ -21,13 +21,20 @@
  *   directions [B][K][4][4], outputs likewise.
  *
  * Ownership: every pointer argument is CALLER-owned.  Device pointers must
- * stay valid for the duration of the call (stream-ordered).  The context owns
- * its device arenas (primal store + workspace, cudaMalloc'd in
- * tn_hvp_setup, freed in tn_hvp_destroy) and its cuSOLVER handle.  The primal
- * store can be exported for a collective (tn_hvp_primal_blob).
+ * stay valid for the duration of the call (stream-ordered).  The primal store
+ * (tn_hvp_query's primal_bytes) is either caller-owned (primal_buf of
+ * tn_hvp_setup, kept until tn_hvp_destroy) or allocated by the context.  The
+ * context owns its cuSOLVER handles, internal streams and the transient
+ * buffers of a call; those come from a stream-ordered cudaMemPool private to
+ * this library (never the device's default pool), whose cached blocks are
+ * returned by tn_hvp_trim_memory and tn_hvp_destroy.  The primal store is one
+ * flat byte range (tn_hvp_primal_blob) so a collective can move it.
  *
  * Streams: `stream` is a cudaStream_t passed as void*; all device work is
- * enqueued on it.  Calls that must read a device value on the host say so.
+ * enqueued on it (the primal pass forks internal streams and joins them back
+ * into it).  Calls on one context must be stream-ordered: the same stream, or
+ * the caller orders them.  No call synchronises the device; calls that must
+ * read a device value on the host synchronise `stream` and say so.
  *
  * Errors: every call returns tn_status and never throws across the ABI.
  *   TN_EINVAL  argument error, detected before any launch;
@@ -50,6 +57,19 @@ extern "C" {
 
 typedef enum { TN_OK = 0, TN_EINVAL = 1, TN_ENOMEM = 2, TN_ECUDA = 3, TN_ENUMERIC = 4, TN_ESTATE = 5 } tn_status;
 
+/* Arithmetic type.  Only complex128 is built (north_star's complex64 mode is
+ * optional and not implemented: TN_C64 returns TN_EINVAL). */
+typedef enum { TN_C128 = 0, TN_C64 = 1 } tn_dtype;
+
+/* Argument checks, each costs one small kernel and a
+ * stream synchronisation per call:
+ *   TN_CHECK_UNITARY: every gate of environments / step / cost has
+ *     ||G^dag G - I||_F <= 1e-10, else TN_EINVAL before any other work;
+ *   TN_CHECK_TANGENT: every direction of apply / step has
+ *     ||V - P_G V|| <= 1e-8 ||V|| (norms over all K gates), else TN_EINVAL. */
+#define TN_CHECK_UNITARY 1u
+#define TN_CHECK_TANGENT 2u
+
 typedef struct tn_hvp_ctx tn_hvp_ctx;
 
 typedef struct {
@@ -57,20 +77,35 @@ typedef struct {
   int32_t depth;        /* D >= 1 brickwall layers                              */
   int32_t first_offset; /* 0 | 1: first layer on (0,1),(2,3).. or (1,2),(3,4).. */
   int32_t chi;          /* primal bond cap; tangent bonds <= 2*chi              */
+  int32_t dtype;        /* tn_dtype; TN_C128                                    */
   int32_t max_batch;    /* directions per internal sub-batch of tn_hvp_apply    */
   int32_t device;       /* CUDA device ordinal                                  */
-  uint32_t flags;       /* reserved, 0                                          */
+  uint32_t flags;       /* TN_CHECK_UNITARY | TN_CHECK_TANGENT, or 0            */
 } tn_hvp_config;
+
+typedef struct {
+  size_t primal_bytes;        /* the primal store (tn_hvp_primal_blob's size)          */
+  size_t workspace_bytes;     /* direction-independent tangent chains, recorded by the */
+                              /* first apply at a point (from the library pool)        */
+  size_t per_direction_bytes; /* one direction's tangent state (cached forward tangent */
+                              /* + live backward tangent); x max_batch per sub-batch   */
+} tn_hvp_sizes;
 
 /* Number of gates K implied by (n_sites, depth, first_offset). */
 int32_t tn_hvp_num_gates(int32_t n_sites, int32_t depth, int32_t first_offset);
 
-/* Create a context.  ref_bonds: HOST int32[n+1] (b_0 = b_n = 1);
- * ref_mpo: DEVICE, the n site tensors packed back to back in site order,
- * sum_s b_s*4*b_{s+1} complex128 (copied into the context).  Allocates the
- * arenas for the whole (n, D, chi, max_batch) problem. */
-tn_status tn_hvp_setup(const tn_hvp_config* cfg, const int32_t* ref_bonds, const void* ref_mpo,
-                       void* stream, tn_hvp_ctx** out);
+/* Sizes of a context for (cfg, ref_bonds) without creating it (host only, no
+ * CUDA call).  ref_bonds: HOST int32[n+1].  TN_EINVAL as tn_hvp_setup. */
+tn_status tn_hvp_query(const tn_hvp_config* cfg, const int32_t* ref_bonds, tn_hvp_sizes* out);
+
+/* Create a context.  ref_bonds: HOST int32[n+1] (b_0 = b_n = 1, neighbouring
+ * bonds within a factor 4); ref_mpo: DEVICE, the n site tensors packed back to
+ * back in site order, sum_s b_s*4*b_{s+1} complex128 (copied into the context).
+ * primal_buf: DEVICE, 256-byte aligned, >= tn_hvp_query's primal_bytes
+ * (primal_bytes_avail), caller-owned and kept until tn_hvp_destroy; or NULL:
+ * the context allocates the store itself.  Synchronises the stream. */
+tn_status tn_hvp_setup(const tn_hvp_config* cfg, const int32_t* ref_bonds, const void* ref_mpo, void* primal_buf,
+                       size_t primal_bytes_avail, void* stream, tn_hvp_ctx** out);
 
 /* Primal pass (a2-a5): bottom and top sweeps with truncation, per-layer
  * left/right environments, E_k = dT/dG_k (eq:environment),
@@ -89,7 +124,7 @@ tn_status tn_hvp_environments(tn_hvp_ctx* ctx, const void* gates, void* scalars_
  * tangent propagation fused with the layer environments (eq:dbis,
  * eq:overlap-hvp), then Omega, H_f and the Riemannian Hessian
  * (PAPER.md:501-505, :1152-1157).
- * dirs: DEVICE [batch][K][4][4] tangent at G (not checked unless flags).
+ * dirs: DEVICE [batch][K][4][4] tangent at G (checked with TN_CHECK_TANGENT).
  * hess_R_out: DEVICE [batch][K][4][4].
  * aux_out: DEVICE, nullable: [batch][K][4][4] H_T (Wirtinger HVP of T)
  *   followed by [batch] complex Omega.
@@ -137,15 +172,27 @@ tn_status tn_hvp_ti_environments(tn_hvp_ctx* ctx, const void* layer_gates, void*
 tn_status tn_hvp_ti_apply(tn_hvp_ctx* ctx, int32_t batch, const void* layer_dirs, void* hess_R_out, void* stream);
 
 /* Cost only (a3, top sweep): T and f at the given gates without touching the
- * stored primal (for the trust-region rho test).  scalars_out as above. */
+ * stored primal (for the trust-region rho test).  scalars_out as above.  The
+ * stored point's primal store, caches and graphs are never written, so later
+ * tn_hvp_apply calls are unaffected even when this call fails.  TN_ENUMERIC on
+ * a solver failure or a non-finite T.  Synchronises the stream. */
 tn_status tn_hvp_cost(tn_hvp_ctx* ctx, const void* gates, void* scalars_out, void* stream);
 
 /* Primal store as one flat device byte range (for an NCCL broadcast). */
 tn_status tn_hvp_primal_blob(tn_hvp_ctx* ctx, void** ptr, size_t* bytes);
 
-/* Mark the primal store as valid for `gates` after it was filled by a
- * collective instead of tn_hvp_environments (same shapes, same gates). */
+/* Mark the primal store as valid after a collective filled it (through
+ * tn_hvp_primal_copy into the context, or the blob pointer) instead of
+ * tn_hvp_environments.  gates: DEVICE [K][4][4], the point the store was built
+ * at; the store carries its own copy and the two must agree bit for bit, else
+ * TN_EINVAL and the store stays invalid.  Drops the per-point caches and the
+ * translation-invariant state.  Synchronises the stream. */
 tn_status tn_hvp_primal_imported(tn_hvp_ctx* ctx, const void* gates, void* stream);
+
+/* Release the per-point caches and CUDA graphs (the next apply rebuilds them)
+ * and return the library pool's unused device memory to the device, e.g.
+ * before the caller allocates large buffers of its own.  Synchronises. */
+tn_status tn_hvp_trim_memory(tn_hvp_ctx* ctx, void* stream);
 
 /* out = P_G(in) = 1/2 (in - G in^dag G), gate-wise, batched (eq:projec,
  * PAPER.md:1113-1115).  gates [K][4][4], in/out [batch][K][4][4], DEVICE. */
@@ -188,8 +235,10 @@ tn_status tn_pauli_basis(int32_t K, int64_t first, int32_t count, const void* ga
 tn_status tn_pauli_coords(int32_t K, int32_t count, const void* gates, const void* X, void* out, void* stream);
 tn_status tn_sym_eig(int32_t n, void* A, void* w, void* asym, int32_t vectors, void* stream);
 
-/* Copy the primal store to (into_ctx = 0) or from (into_ctx = 1) a caller
- * DEVICE buffer of exactly tn_hvp_primal_blob's size (broadcast support). */
+/* Copy the primal store to (into_ctx = 0; TN_ESTATE without a valid primal
+ * pass) or from (into_ctx = 1) a caller DEVICE buffer of exactly
+ * tn_hvp_primal_blob's size (broadcast support).  into_ctx = 1 invalidates the
+ * context's point until tn_hvp_primal_imported. */
 tn_status tn_hvp_primal_copy(tn_hvp_ctx* ctx, void* buf, size_t bytes, int32_t into_ctx, void* stream);
 
 /* Building block exposed for tests: batched complex128 GEMM on the FP64
@@ -214,6 +263,7 @@ int64_t tn_hvp_launch_count(void);
  * MACs (HOST outputs, may be NULL when mode = 1). */
 tn_status tn_gemm_profile(int32_t mode, double* ms, double* cmac);
 
+/* Destroy a context.  The caller has synchronised the streams it used with it. */
 void tn_hvp_destroy(tn_hvp_ctx* ctx);
 
 /* Last error text of ctx (or of the calling thread when ctx is NULL). */

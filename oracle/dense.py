@@ -168,6 +168,15 @@ def vec_env(top: np.ndarray, bot: np.ndarray, n: int, s: int) -> np.ndarray:
     return np.einsum("xaibjy,xcidjy->abcd", np.conj(t), b).reshape(4, 4)
 
 
+def tangent_project(D: np.ndarray, Ur: np.ndarray, Vr: np.ndarray) -> np.ndarray:
+    """P_T D = (P^L (x) I + I (x) P^R - P^L (x) P^R) D for the matricised state D
+    (rows: sites left of the cut), P^L = Ur Ur^dag, P^R = Vr^dag Vr: the orthogonal
+    projection onto the tangent space of the bond-r manifold at the kept
+    Schmidt spaces (PAPER.md:1019-1023 fixed projectors; reading X8)."""
+    PLD = Ur @ (Ur.conj().T @ D)
+    return PLD + (D @ Vr.conj().T) @ Vr - (PLD @ Vr.conj().T) @ Vr
+
+
 class DenseTruncated:
     """O2: the truncated definition of SURVEY.md §8(c.2), written out densely.
 
@@ -231,11 +240,7 @@ class DenseTruncated:
         Ur, Vr = U[:, :r], Vh[:r]
         y = Ur @ (Ur.conj().T @ mat)
         sc = np.linalg.norm(mat) / np.linalg.norm(y)
-        out = []
-        for d in dxp:
-            D = d.reshape(mat.shape)
-            PLD = Ur @ (Ur.conj().T @ D)
-            out.append((sc * (PLD + (D @ Vr.conj().T) @ Vr - (PLD @ Vr.conj().T) @ Vr)).reshape(x.shape))
+        out = [(sc * tangent_project(d.reshape(mat.shape), Ur, Vr)).reshape(x.shape) for d in dxp]
         bonds[c] = r
         self.diag.append({"cut": c, "r": r, "sigma": S, "s": sc})
         return (sc * y).reshape(x.shape), out

@@ -18,8 +18,10 @@ EXPORTS = ["tn_hvp_num_gates", "tn_hvp_setup", "tn_hvp_environments", "tn_hvp_ap
            "tn_hvp_cost", "tn_hvp_primal_blob", "tn_hvp_primal_imported", "tn_riemannian_project", "tn_zgemm",
            "tn_hvp_work", "tn_retract", "tn_tangent_dot", "tn_tangent_axpby", "tn_hvp_primal_copy",
            "tn_hvp_launch_count", "tn_gemm_profile", "tn_pauli_basis", "tn_pauli_coords", "tn_sym_eig",
-           "tn_hvp_ti_environments", "tn_hvp_ti_apply", "tn_hvp_step",
+           "tn_hvp_ti_environments", "tn_hvp_ti_apply", "tn_hvp_step", "tn_hvp_query", "tn_hvp_trim_memory",
            "tn_hvp_destroy", "tn_hvp_last_error"]
+TN_C128, TN_C64 = 0, 1
+TN_CHECK_UNITARY, TN_CHECK_TANGENT = 1, 2
 
 
 class TNError(RuntimeError):
@@ -30,7 +32,11 @@ class TNError(RuntimeError):
 
 class Config(C.Structure):
     _fields_ = [("n_sites", C.c_int32), ("depth", C.c_int32), ("first_offset", C.c_int32), ("chi", C.c_int32),
-                ("max_batch", C.c_int32), ("device", C.c_int32), ("flags", C.c_uint32)]
+                ("dtype", C.c_int32), ("max_batch", C.c_int32), ("device", C.c_int32), ("flags", C.c_uint32)]
+
+
+class Sizes(C.Structure):
+    _fields_ = [("primal_bytes", C.c_size_t), ("workspace_bytes", C.c_size_t), ("per_direction_bytes", C.c_size_t)]
 
 
 _lib = None
@@ -45,7 +51,9 @@ def lib():
         vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
         L.tn_hvp_num_gates.argtypes = [i32, i32, i32]
         L.tn_hvp_num_gates.restype = i32
-        L.tn_hvp_setup.argtypes = [C.POINTER(Config), C.POINTER(i32), vp, vp, C.POINTER(vp)]
+        L.tn_hvp_setup.argtypes = [C.POINTER(Config), C.POINTER(i32), vp, vp, C.c_size_t, vp, C.POINTER(vp)]
+        L.tn_hvp_query.argtypes = [C.POINTER(Config), C.POINTER(i32), C.POINTER(Sizes)]
+        L.tn_hvp_trim_memory.argtypes = [vp, vp]
         L.tn_hvp_environments.argtypes = [vp, vp, vp, vp, vp]
         L.tn_hvp_apply.argtypes = [vp, i32, vp, vp, vp, vp]
         L.tn_hvp_gradient_T.argtypes = [vp, vp, vp]
@@ -68,7 +76,7 @@ def lib():
         L.tn_sym_eig.argtypes = [i32, vp, vp, vp, i32, vp]
         for name in ("tn_retract", "tn_tangent_dot", "tn_tangent_axpby", "tn_hvp_primal_copy", "tn_pauli_basis",
                      "tn_pauli_coords", "tn_sym_eig", "tn_hvp_ti_environments", "tn_hvp_ti_apply",
-                     "tn_hvp_step"):
+                     "tn_hvp_step", "tn_hvp_query", "tn_hvp_trim_memory"):
             getattr(L, name).restype = C.c_int
         L.tn_hvp_launch_count.argtypes = []
         L.tn_hvp_launch_count.restype = C.c_int64
@@ -96,11 +104,24 @@ def tn_hvp_num_gates(n, depth, first_offset=0):
     return lib().tn_hvp_num_gates(n, depth, first_offset)
 
 
-def tn_hvp_setup(cfg: Config, ref_bonds, ref_mpo_ptr, stream):
+def tn_hvp_query(cfg: Config, ref_bonds):
+    """-> (primal_bytes, workspace_bytes, per_direction_bytes)."""
+    arr = (C.c_int32 * len(ref_bonds))(*ref_bonds)
+    out = Sizes()
+    check(lib().tn_hvp_query(C.byref(cfg), arr, C.byref(out)))
+    return out.primal_bytes, out.workspace_bytes, out.per_direction_bytes
+
+
+def tn_hvp_setup(cfg: Config, ref_bonds, ref_mpo_ptr, stream, primal_ptr=0, primal_bytes=0):
     arr = (C.c_int32 * len(ref_bonds))(*ref_bonds)
     out = C.c_void_p()
-    check(lib().tn_hvp_setup(C.byref(cfg), arr, C.c_void_p(ref_mpo_ptr), C.c_void_p(stream), C.byref(out)))
+    check(lib().tn_hvp_setup(C.byref(cfg), arr, C.c_void_p(ref_mpo_ptr), C.c_void_p(primal_ptr or None),
+                             C.c_size_t(primal_bytes), C.c_void_p(stream), C.byref(out)))
     return out
+
+
+def tn_hvp_trim_memory(ctx, stream):
+    check(lib().tn_hvp_trim_memory(ctx, C.c_void_p(stream)), ctx)
 
 
 def tn_hvp_environments(ctx, gates_ptr, scalars_ptr, grad_R_ptr, stream):

@@ -31,7 +31,7 @@ class HVPEngine:
     U_ref/2^{n/2} (right-canonical, centre at site 0).
     """
 
-    def __init__(self, n, depth, chi, ref_sites, first_offset=0, max_batch=64, device=None):
+    def __init__(self, n, depth, chi, ref_sites, first_offset=0, max_batch=64, device=None, flags=0):
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2604_20384_b200 needs a CUDA device (no CPU fallback)")
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
@@ -39,16 +39,27 @@ class HVPEngine:
         self.K = N.tn_hvp_num_gates(n, depth, first_offset)
         self.ref_bonds = [1] + [int(a.shape[2]) for a in ref_sites]
         packed = torch.cat([a.to(self.device, torch.complex128).contiguous().reshape(-1) for a in ref_sites])
-        cfg = N.Config(n, depth, first_offset, chi, max_batch, self.device.index, 0)
+        cfg = N.Config(n, depth, first_offset, chi, N.TN_C128, max_batch, self.device.index, flags)
+        # the primal store is a caller-owned torch buffer (tn_hvp_query's size):
+        # visible to torch's allocator and broadcastable in place (parallel.py)
+        self.primal_bytes, self.workspace_bytes, self.per_direction_bytes = N.tn_hvp_query(cfg, self.ref_bonds)
+        self.primal = torch.empty(max(self.primal_bytes, 256), dtype=torch.uint8, device=self.device)
         with torch.cuda.device(self.device):
-            self.ctx = N.tn_hvp_setup(cfg, self.ref_bonds, packed.data_ptr(), _stream())
+            self.ctx = N.tn_hvp_setup(cfg, self.ref_bonds, packed.data_ptr(), _stream(), self.primal.data_ptr(),
+                                      self.primal.numel())
         self.max_batch = max_batch
         self.scalars = torch.zeros(8, dtype=torch.float64, device=self.device)
 
     def close(self):
         if getattr(self, "ctx", None):
+            torch.cuda.synchronize(self.device)
             N.tn_hvp_destroy(self.ctx)
             self.ctx = None
+            self.primal = None
+
+    def trim_memory(self):
+        """Drop per-point caches / graphs and return the library pool's unused memory."""
+        N.tn_hvp_trim_memory(self.ctx, _stream())
 
     def __del__(self):
         try:
@@ -113,7 +124,17 @@ class HVPEngine:
     def primal_blob(self):
         return N.tn_hvp_primal_blob(self.ctx)
 
+    def primal_store(self) -> torch.Tensor:
+        """The primal store itself (uint8, tn_hvp_primal_blob's bytes; no copy)."""
+        return self.primal[: self.primal_bytes]
+
+    def invalidate_primal(self):
+        """Before the store is overwritten by a collective: drop the old point."""
+        st = self.primal_store()
+        N.tn_hvp_primal_copy(self.ctx, st.data_ptr(), st.numel(), 1, _stream())
+
     def primal_imported(self, gates: torch.Tensor):
+        _require_cuda(gates, "gates")
         N.tn_hvp_primal_imported(self.ctx, gates.data_ptr(), _stream())
 
     def work(self):
@@ -179,16 +200,17 @@ def axpby(a, x: torch.Tensor, b, y: torch.Tensor) -> torch.Tensor:
 
 
 def primal_export(eng: "HVPEngine") -> torch.Tensor:
-    """Copy the context's primal store into a uint8 torch tensor (for a broadcast)."""
-    _, n = eng.primal_blob()
-    buf = torch.empty(n, dtype=torch.uint8, device=eng.device)
-    N.tn_hvp_primal_copy(eng.ctx, buf.data_ptr(), n, 0, _stream())
-    return buf
+    """The context's primal store (caller-owned uint8 tensor, tn_hvp_primal_blob's
+    bytes); valid after environments / step.  No copy."""
+    return eng.primal_store()
 
 
 def primal_import(eng: "HVPEngine", buf: torch.Tensor, gates: torch.Tensor):
-    """Fill the primal store from a buffer produced by primal_export (same shapes)."""
-    N.tn_hvp_primal_copy(eng.ctx, buf.data_ptr(), buf.numel(), 1, _stream())
+    """Fill the primal store from a buffer produced by primal_export at `gates`
+    (same shapes) and mark it valid; a buffer that IS the store (in-place
+    broadcast) is only marked.  TN_EINVAL if the store's point is not `gates`."""
+    if buf.data_ptr() != eng.primal.data_ptr():
+        N.tn_hvp_primal_copy(eng.ctx, buf.data_ptr(), buf.numel(), 1, _stream())
     eng.primal_imported(gates)
 
 

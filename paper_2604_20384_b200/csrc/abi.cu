@@ -73,21 +73,48 @@ tn_status tn_riemannian_project(int32_t K, int32_t batch, const void* gates, con
   });
 }
 
-tn_status tn_hvp_setup(const tn_hvp_config* cfg, const int32_t* ref_bonds, const void* ref_mpo, void* stream,
-                       tn_hvp_ctx** out) {
-  if (!cfg || !ref_bonds || !ref_mpo || !out) return fail(nullptr, TN_EINVAL, "tn_hvp_setup: null argument");
+namespace {
+tn_status check_config(const tn_hvp_config* cfg, const int32_t* ref_bonds, const char* who) {
+  const std::string w(who);
   if (cfg->n_sites < 2 || cfg->depth < 1 || (cfg->first_offset != 0 && cfg->first_offset != 1) || cfg->chi < 1 ||
-      cfg->max_batch < 1)
-    return fail(nullptr, TN_EINVAL, "tn_hvp_setup: n>=2, depth>=1, offset in {0,1}, chi>=1, max_batch>=1");
+      cfg->max_batch < 1 || cfg->device < 0)
+    return fail(nullptr, TN_EINVAL, w + ": n>=2, depth>=1, offset in {0,1}, chi>=1, max_batch>=1, device>=0");
+  if (cfg->dtype != TN_C128)
+    return fail(nullptr, TN_EINVAL, w + ": only dtype TN_C128 is built (the complex64 mode is not implemented)");
+  if (cfg->flags & ~(TN_CHECK_UNITARY | TN_CHECK_TANGENT))
+    return fail(nullptr, TN_EINVAL, w + ": unknown flag bits");
   if (ref_bonds[0] != 1 || ref_bonds[cfg->n_sites] != 1)
-    return fail(nullptr, TN_EINVAL, "tn_hvp_setup: boundary bonds must be 1");
+    return fail(nullptr, TN_EINVAL, w + ": boundary bonds must be 1");
   for (int s = 0; s < cfg->n_sites; ++s) {
     const int64_t bl = ref_bonds[s], br = ref_bonds[s + 1];
     if (bl < 1 || br < 1 || br > 4 * bl || bl > 4 * br)
-      return fail(nullptr, TN_EINVAL, "tn_hvp_setup: reference bonds must satisfy 1 <= b_{s+1} <= 4 b_s and vice versa");
+      return fail(nullptr, TN_EINVAL, w + ": reference bonds must satisfy 1 <= b_{s+1} <= 4 b_s and vice versa");
   }
+  return TN_OK;
+}
+}  // namespace
+
+tn_status tn_hvp_query(const tn_hvp_config* cfg, const int32_t* ref_bonds, tn_hvp_sizes* out) {
+  if (!cfg || !ref_bonds || !out) return fail(nullptr, TN_EINVAL, "tn_hvp_query: null argument");
+  if (tn_status st = check_config(cfg, ref_bonds, "tn_hvp_query")) return st;
+  return guarded(nullptr, [&] {
+    tn::engine_query(*cfg, ref_bonds, &out->primal_bytes, &out->workspace_bytes, &out->per_direction_bytes);
+  });
+}
+
+tn_status tn_hvp_setup(const tn_hvp_config* cfg, const int32_t* ref_bonds, const void* ref_mpo, void* primal_buf,
+                       size_t primal_bytes_avail, void* stream, tn_hvp_ctx** out) {
+  if (!cfg || !ref_bonds || !ref_mpo || !out) return fail(nullptr, TN_EINVAL, "tn_hvp_setup: null argument");
+  if (tn_status st = check_config(cfg, ref_bonds, "tn_hvp_setup")) return st;
   *out = nullptr;
-  return guarded(nullptr, [&] { *out = tn::engine_create(*cfg, ref_bonds, ref_mpo, (cudaStream_t)stream); });
+  return guarded(nullptr, [&] {
+    *out = tn::engine_create(*cfg, ref_bonds, ref_mpo, primal_buf, primal_bytes_avail, (cudaStream_t)stream);
+  });
+}
+
+tn_status tn_hvp_trim_memory(tn_hvp_ctx* ctx, void* stream) {
+  if (!ctx) return fail(nullptr, TN_EINVAL, "tn_hvp_trim_memory: null context");
+  return guarded(ctx, [&] { tn::engine_trim_memory(ctx, (cudaStream_t)stream); });
 }
 
 tn_status tn_hvp_environments(tn_hvp_ctx* ctx, const void* gates, void* scalars_out, void* grad_R_out, void* stream) {
@@ -167,13 +194,12 @@ tn_status tn_retract(int32_t K, const void* gates, const void* xi, double alpha,
   if (K < 0 || (K && (!gates || !xi || !out))) return fail(nullptr, TN_EINVAL, "tn_retract: bad argument");
   return guarded(nullptr, [&] {
     if (!K) return;
-    int* st = nullptr;
-    TN_CUDA(cudaMallocAsync((void**)&st, sizeof(int), (cudaStream_t)stream));
+    int* st = (int*)tn::dalloc(sizeof(int), (cudaStream_t)stream);
     TN_CUDA(cudaMemsetAsync(st, 0, sizeof(int), (cudaStream_t)stream));
     tn::retract((cudaStream_t)stream, K, (const tn::cplx*)gates, (const tn::cplx*)xi, alpha, (tn::cplx*)out, st);
     int h = 0;
     TN_CUDA(cudaMemcpyAsync(&h, st, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
-    TN_CUDA(cudaFreeAsync(st, (cudaStream_t)stream));
+    tn::dfree(st, (cudaStream_t)stream);
     TN_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
     if (h) throw tn::NumericError("tn_retract: singular iterate");
   });
@@ -221,16 +247,7 @@ tn_status tn_sym_eig(int32_t n, void* A, void* w, void* asym, int32_t vectors, v
 
 tn_status tn_hvp_primal_copy(tn_hvp_ctx* ctx, void* buf, size_t bytes, int32_t into_ctx, void* stream) {
   if (!ctx || !buf || (into_ctx != 0 && into_ctx != 1)) return fail(ctx, TN_EINVAL, "tn_hvp_primal_copy: bad argument");
-  return guarded(ctx, [&] {
-    void* p = nullptr;
-    size_t n = 0;
-    tn::engine_primal_blob(ctx, &p, &n);
-    if (bytes != n) throw std::invalid_argument("tn_hvp_primal_copy: size mismatch");
-    if (into_ctx)
-      TN_CUDA(cudaMemcpyAsync(p, buf, n, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
-    else
-      TN_CUDA(cudaMemcpyAsync(buf, p, n, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
-  });
+  return guarded(ctx, [&] { tn::engine_primal_copy(ctx, buf, bytes, into_ctx, (cudaStream_t)stream); });
 }
 
 int64_t tn_hvp_launch_count(void) { return tn::launch_count(); }

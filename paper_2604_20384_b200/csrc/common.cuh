@@ -44,6 +44,13 @@ void gemm_profile_begin();                      // enable + reset (host side)
 void gemm_profile_end(double* ms, double* cmac);  // sync, disable, read totals
 bool gemm_profile_active();
 
+// Library-private stream-ordered device memory (zgemm.cu): a cudaMemPool per
+// device owned by this library (the device's default pool is left untouched).
+// pool_trim returns the pool's unused blocks to the device.
+void* dalloc(size_t bytes, cudaStream_t st);
+void dfree(void* p, cudaStream_t st);
+void pool_trim(int device);
+
 // Batched row-major complex GEMM on DMMA (zgemm.cu).
 // C[b] = alpha * op(A[b]) * op(B[b]) + beta * C[b]; op(A): M x K, op(B): K x N.
 // opa/opb in {'N','T','C'}; strides in elements, 0 = operand shared.

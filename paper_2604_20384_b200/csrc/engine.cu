@@ -89,14 +89,13 @@ void poison(void* p, size_t bytes, cudaStream_t st) {
 }
 
 cplx* dnew(int64_t n, cudaStream_t st) {
-  void* p = nullptr;
   const size_t bytes = (size_t)std::max<int64_t>(n, 1) * sizeof(cplx);
-  TN_CUDA(cudaMallocAsync(&p, bytes, st));
+  void* p = dalloc(bytes, st);
   poison(p, bytes, st);
   return (cplx*)p;
 }
 void ddel(cplx*& p, cudaStream_t st) {
-  if (p) cudaFreeAsync(p, st);
+  dfree(p, st);
   p = nullptr;
 }
 void dset(cplx*& slot, cplx* nw, cudaStream_t st) {
@@ -109,22 +108,20 @@ struct Pool {  // stream-ordered transient device buffers
   std::vector<void*> ptrs;
   explicit Pool(cudaStream_t s) : st(s) {}
   cplx* c(int64_t n) {
-    void* p = nullptr;
     if (n <= 0) n = 1;
-    TN_CUDA(cudaMallocAsync(&p, (size_t)n * sizeof(cplx), st));
+    void* p = dalloc((size_t)n * sizeof(cplx), st);
     poison(p, (size_t)n * sizeof(cplx), st);
     ptrs.push_back(p);
     return (cplx*)p;
   }
   void* raw(size_t bytes) {
-    void* p = nullptr;
-    TN_CUDA(cudaMallocAsync(&p, std::max<size_t>(bytes, 16), st));
+    void* p = dalloc(std::max<size_t>(bytes, 16), st);
     poison(p, std::max<size_t>(bytes, 16), st);
     ptrs.push_back(p);
     return p;
   }
   ~Pool() {
-    for (void* p : ptrs) cudaFreeAsync(p, st);
+    for (void* p : ptrs) dfree(p, st);
   }
 };
 
@@ -143,6 +140,7 @@ struct Engine {
   // primal arena
   char* arena = nullptr;
   size_t arena_bytes = 0;
+  bool own_arena = true;  // false: caller-owned primal_buf (tn_hvp_setup)
   size_t o_gates = 0, o_gdag = 0, o_E = 0, o_gradf = 0, o_scal = 0, o_diag = 0;
   std::vector<std::vector<size_t>> o_L, o_R;  // per layer, per cut
   std::vector<double> h_s;                    // host copy of the frozen factors
@@ -153,13 +151,10 @@ struct Engine {
   struct Solver {
     cusolverDnHandle_t h = nullptr;
     cusolverDnParams_t prm = nullptr;
-    gesvdjInfo_t svdj = nullptr;
     std::vector<char> host_ws;
   };
   Solver sol[2];
-  int svd_method = 3;  // 0 gesvdj, 1 Xgesvdp, 2 Xgesvd, 3 Gram heevd (default)
   int lwork_heevd = 0;
-  int fallback_method = 2;  // TN_SVD_FALLBACK: gesvd (QR iteration, default) | gesvdj
   std::atomic<int> n_fallback{0}, n_deflate{0}, n_noise{0};
   size_t svd_dws = 0, svd_hws = 0;
   int lwork_geqrf = 0, lwork_ungqr = 0;
@@ -418,15 +413,54 @@ struct Engine {
   }
 
   // ------------------------------------------------------------ setup --
-  void setup(const tn_hvp_config& c, const int32_t* rb, const void* ref_mpo, cudaStream_t st) {
+  // Host-only plan: layers, both sides' step lists with their static bond
+  // profiles (a2/a3 keep rule, X7), and the primal-arena layout.
+  void plan(const tn_hvp_config& c, const int32_t* rb) {
     cfg = c;
     n = c.n_sites;
     D = c.depth;
     off = c.first_offset;
     chi = c.chi;
     device = c.device;
-    TN_CUDA(cudaSetDevice(device));
     build_layers();
+    ref_bonds.assign(rb, rb + n + 1);
+    std::vector<int> ones(n + 1, 1);
+    n_pair_steps = 0;
+    plan_side(bot, ones, false);
+    plan_side(top, ref_bonds, true);
+    layout_arena();
+  }
+
+  // Bytes of one direction's tangent state: the cached forward tangent blocks
+  // of every bottom snapshot plus the live backward tangent's blocks.
+  size_t per_direction_bytes() const {
+    size_t e = 0;
+    for (size_t li = 0; li + 1 < bot.snap.size(); ++li)
+      for (int s = 0; s < n; ++s) e += (size_t)bsize(bot.snap[li], s);
+    size_t mx = 0;
+    for (const Bonds& b : top.snap) {
+      size_t t = 0;
+      for (int s = 0; s < n; ++s) t += (size_t)bsize(b, s);
+      mx = std::max(mx, t);
+    }
+    return (e + mx) * sizeof(cplx);
+  }
+
+  size_t chain_cache_bytes() const {
+    return sizeof(cplx) * (size_t)(chain_cache_elems(bot) + chain_cache_elems(top));
+  }
+
+  // primal_buf: caller-owned DEVICE buffer of at least arena_bytes (nullptr:
+  // the context allocates and owns it).
+  void setup(const tn_hvp_config& c, const int32_t* rb, const void* ref_mpo, void* primal_buf, size_t primal_bytes,
+             cudaStream_t st) {
+    plan(c, rb);
+    if (primal_buf && primal_bytes < arena_bytes)
+      throw std::invalid_argument("tn_hvp_setup: primal_buf smaller than tn_hvp_query's primal_bytes (" +
+                                  std::to_string(primal_bytes) + " < " + std::to_string(arena_bytes) + ")");
+    if (reinterpret_cast<uintptr_t>(primal_buf) % 256 != 0)
+      throw std::invalid_argument("tn_hvp_setup: primal_buf must be 256-byte aligned");
+    TN_CUDA(cudaSetDevice(device));
     {
       std::vector<int> lo, ls(1, 0);
       for (int ell = 1; ell <= D; ++ell) {
@@ -439,13 +473,14 @@ struct Engine {
       if (!lo.empty()) TN_CUDA(cudaMemcpy(d_layer_of, lo.data(), sizeof(int) * lo.size(), cudaMemcpyHostToDevice));
       TN_CUDA(cudaMemcpy(d_layer_start, ls.data(), sizeof(int) * ls.size(), cudaMemcpyHostToDevice));
     }
-    ref_bonds.assign(rb, rb + n + 1);
-    std::vector<int> ones(n + 1, 1);
-    plan_side(bot, ones, false);
-    plan_side(top, ref_bonds, true);
-    layout_arena();
-    TN_CUDA(cudaMalloc(&arena, std::max<size_t>(arena_bytes, 256)));
-    if (g_poison) TN_CUDA(cudaMemset(arena, 0xFF, std::max<size_t>(arena_bytes, 256)));
+    if (primal_buf) {
+      arena = static_cast<char*>(primal_buf);
+      own_arena = false;
+    } else {
+      TN_CUDA(cudaMalloc(&arena, std::max<size_t>(arena_bytes, 256)));
+      own_arena = true;
+    }
+    if (g_poison) TN_CUDA(cudaMemsetAsync(arena, 0xFF, std::max<size_t>(arena_bytes, 256), st));
     // reference copy
     ref_off.assign(n, 0);
     size_t e = 0;
@@ -455,22 +490,6 @@ struct Engine {
     }
     TN_CUDA(cudaMalloc(&ref, e * sizeof(cplx)));
     TN_CUDA(cudaMemcpyAsync(ref, ref_mpo, e * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-    // memory pool keeps transient buffers cached
-    cudaMemPool_t pool;
-    TN_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
-    uint64_t thr = UINT64_MAX;
-    TN_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-    // no cross-stream reuse dependencies: the bottom and top sweeps run on two
-    // streams and must not be serialised through recycled pool blocks
-    int off = 0;
-    TN_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseFollowEventDependencies, &off));
-    TN_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowOpportunistic, &off));
-    TN_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &off));
-    if (const char* f = std::getenv("TN_SVD_FALLBACK")) fallback_method = std::string(f) == "gesvdj" ? 0 : 2;
-    if (const char* m = std::getenv("TN_SVD")) {
-      const std::string v(m);
-      svd_method = v == "gesvdj" ? 0 : v == "gesvd" ? 2 : v == "gesvdp" ? 1 : 3;
-    }
     TN_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
     TN_CUDA(cudaStreamCreateWithFlags(&st1, cudaStreamNonBlocking));
     TN_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
@@ -489,9 +508,6 @@ struct Engine {
     for (Solver& so : sol) {
       TN_SOLVER(cusolverDnCreate(&so.h));
       TN_SOLVER(cusolverDnCreateParams(&so.prm));
-      TN_SOLVER(cusolverDnCreateGesvdjInfo(&so.svdj));
-      TN_SOLVER(cusolverDnXgesvdjSetTolerance(so.svdj, 1e-15));
-      TN_SOLVER(cusolverDnXgesvdjSetMaxSweeps(so.svdj, 100));
     }
     Solver& so = sol[0];
     TN_SOLVER(cusolverDnSetStream(so.h, st));
@@ -500,44 +516,20 @@ struct Engine {
         for (Step& s : ls) {
           if (s.type == PAIR) {
             const int mr = std::max(4 * s.bl, 4 * s.br), nc_ = std::min(4 * s.bl, 4 * s.br);
-            size_t dws = 0, hws = 0;
             {
               int lw = 0;
               TN_SOLVER(cusolverDnZheevd_bufferSize(so.h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, 4 * s.bl,
                                                     nullptr, 4 * s.bl, nullptr, &lw));
               lwork_heevd = std::max(lwork_heevd, lw);
             }
-            {  // Jacobi workspace always (fallback of the Gram split)
-              int lw = 0;
-              TN_SOLVER(cusolverDnZgesvdj_bufferSize(so.h, CUSOLVER_EIG_MODE_VECTOR, 1, mr, nc_, nullptr, mr, nullptr,
-                                                     nullptr, mr, nullptr, nc_, &lw, so.svdj));
-              dws = std::max(dws, (size_t)lw * sizeof(cplx));
-            }
-            {  // QR-iteration workspace always (fallback of the Gram split)
+            {  // QR-iteration SVD workspace (fallback of the Gram split)
               size_t d2 = 0, h2 = 0;
               TN_SOLVER(cusolverDnXgesvd_bufferSize(so.h, so.prm, 'S', 'S', mr, nc_, CUDA_C_64F, nullptr, mr,
                                                     CUDA_R_64F, nullptr, CUDA_C_64F, nullptr, mr, CUDA_C_64F, nullptr,
                                                     nc_, CUDA_C_64F, &d2, &h2));
-              dws = std::max(dws, d2);
-              hws = std::max(hws, h2);
+              svd_dws = std::max(svd_dws, d2);
+              svd_hws = std::max(svd_hws, h2);
             }
-            if (svd_method == 3 || svd_method == 0) {
-            } else if (svd_method == 0) {
-              int lw = 0;
-              TN_SOLVER(cusolverDnZgesvdj_bufferSize(so.h, CUSOLVER_EIG_MODE_VECTOR, 1, mr, nc_, nullptr, mr, nullptr,
-                                                     nullptr, mr, nullptr, nc_, &lw, so.svdj));
-              dws = (size_t)lw * sizeof(cplx);
-            } else if (svd_method == 1) {
-              TN_SOLVER(cusolverDnXgesvdp_bufferSize(so.h, so.prm, CUSOLVER_EIG_MODE_VECTOR, 1, mr, nc_, CUDA_C_64F,
-                                                     nullptr, mr, CUDA_R_64F, nullptr, CUDA_C_64F, nullptr, mr,
-                                                     CUDA_C_64F, nullptr, nc_, CUDA_C_64F, &dws, &hws));
-            } else {
-              TN_SOLVER(cusolverDnXgesvd_bufferSize(so.h, so.prm, 'S', 'S', mr, nc_, CUDA_C_64F, nullptr, mr,
-                                                    CUDA_R_64F, nullptr, CUDA_C_64F, nullptr, mr, CUDA_C_64F, nullptr,
-                                                    nc_, CUDA_C_64F, &dws, &hws));
-            }
-            svd_dws = std::max(svd_dws, dws);
-            svd_hws = std::max(svd_hws, hws);
             int lw = 0;  // LQ of Y (r x 4br): geqrf on the column-major (4br x r) view
             TN_SOLVER(cusolverDnZgeqrf_bufferSize(so.h, 4 * s.br, s.r, nullptr, 4 * s.br, &lw));
             lwork_geqrf = std::max(lwork_geqrf, lw);
@@ -556,34 +548,40 @@ struct Engine {
     for (Solver& x : sol) x.host_ws.assign(svd_hws + 64, 0);
   }
 
+  // The caller has synchronised the streams it used with this context
+  // (tn_hvp_destroy contract); the engine drains its own streams.
   ~Engine() {
+    if (!st1) {  // never set up (tn_hvp_query, or setup failed early)
+      if (d_layer_of) cudaFree(d_layer_of);
+      if (d_layer_start) cudaFree(d_layer_start);
+      if (ti_buf) cudaFree(ti_buf);
+      if (arena && own_arena) cudaFree(arena);
+      if (ref) cudaFree(ref);
+      return;
+    }
+    for (cudaStream_t x : {st1, st2, stg, stf, sth, stc})
+      if (x) cudaStreamSynchronize(x);
+    drop_graphs(stc);
+    drop_chain_cache(stc);
+    cudaStreamSynchronize(stc);
     if (d_layer_of) cudaFree(d_layer_of);
     if (d_layer_start) cudaFree(d_layer_start);
     if (ti_buf) cudaFree(ti_buf);
     for (Solver& so : sol) {
-      if (so.svdj) cusolverDnDestroyGesvdjInfo(so.svdj);
       if (so.prm) cusolverDnDestroyParams(so.prm);
       if (so.h) cusolverDnDestroy(so.h);
     }
-    if (ev_fork) cudaEventDestroy(ev_fork);
-    if (ev_join) cudaEventDestroy(ev_join);
-    if (ev_join1) cudaEventDestroy(ev_join1);
-    if (ev_joing) cudaEventDestroy(ev_joing);
+    for (cudaEvent_t e : {ev_fork, ev_join, ev_join1, ev_joing, ev_joinf})
+      if (e) cudaEventDestroy(e);
     for (auto& v : ev_snap)
       for (auto& e : v)
         if (e) cudaEventDestroy(e);
-    if (stg) cudaStreamDestroy(stg);
-    drop_graphs();
-    drop_chain_cache();
-    trim_pools();
-    if (stf) cudaStreamDestroy(stf);
-    if (stc) cudaStreamDestroy(stc);
-    if (sth) cudaStreamDestroy(sth);
-    if (ev_joinf) cudaEventDestroy(ev_joinf);
-    if (st2) cudaStreamDestroy(st2);
-    if (st1) cudaStreamDestroy(st1);
-    if (arena) cudaFree(arena);
+    for (cudaStream_t x : {st1, st2, stg, stf, sth, stc})
+      if (x) cudaStreamDestroy(x);
+    if (arena && own_arena) cudaFree(arena);
     if (ref) cudaFree(ref);
+    pool_trim(device);
+    cudaDeviceGraphMemTrim(device);
   }
 
   // ------------------------------------------------------ primal pass --
@@ -631,9 +629,12 @@ struct Engine {
 
   // SVD of a row-major (R x Cc) matrix A (destroyed): singular values S (mn =
   // min(R, Cc), descending) and the full left basis uhf = U^H (mn x R row-major).
+  // method kGram: eigendecomposition of A A^H (R x R, all R left vectors);
+  // kQRIter: QR-iteration SVD (the fallback for unresolved cuts).
+  static constexpr int kQRIter = 2, kGram = 3;
   void svd_rowmajor(cudaStream_t st, Solver& so, Pool& pool, cplx* A, int R, int Cc, double* S, cplx* uhf,
                     int* info, int method) {
-    if (method == 3) {
+    if (method == kGram) {
       // Gram split: G = A A^H (R x R), heevd -> all R left vectors (zeros beyond min(R, Cc))
       cplx* Gm = pool.c((int64_t)R * R);
       nc(st, R, R, Cc, A, 0, A, 0, Gm, 0, 1);
@@ -662,17 +663,7 @@ struct Engine {
     void* dws = pool.raw(svd_dws + 64);
     TN_SOLVER(cusolverDnSetStream(so.h, st));
     int* ci = call_info(pool, st);
-    if (method == 0) {
-      TN_SOLVER(cusolverDnZgesvdj(so.h, CUSOLVER_EIG_MODE_VECTOR, 1, m, nn_, (cuDoubleComplex*)M, m, S,
-                                  (cuDoubleComplex*)Up, m, (cuDoubleComplex*)Vp, nn_, (cuDoubleComplex*)dws,
-                                  (int)(svd_dws / sizeof(cplx)), ci, so.svdj));
-    } else if (method == 1) {
-      double herr = 0;
-      TN_SOLVER(cusolverDnXgesvdp(so.h, so.prm, CUSOLVER_EIG_MODE_VECTOR, 1, m, nn_, CUDA_C_64F, M, m, CUDA_R_64F, S,
-                                  CUDA_C_64F, Up, m, CUDA_C_64F, Vp, nn_, CUDA_C_64F, dws, svd_dws,
-                                  so.host_ws.data(), svd_hws, ci, &herr));
-    } else {
-      // Xgesvd returns V^H (mn x nn_, ldvt = mn) in Vp
+    {  // QR-iteration SVD (LAPACK-like accuracy); Xgesvd returns V^H (mn x nn_, ldvt = mn) in Vp
       TN_SOLVER(cusolverDnXgesvd(so.h, so.prm, 'S', 'S', m, nn_, CUDA_C_64F, M, m, CUDA_R_64F, S, CUDA_C_64F, Up, m,
                                  CUDA_C_64F, Vp, mn, CUDA_C_64F, dws, svd_dws, so.host_ws.data(), svd_hws, ci));
       cplx* V = pool.c((int64_t)nn_ * mn);
@@ -744,10 +735,12 @@ struct Engine {
   // Runs one side's primal sweep.  store: write snapshots / replay data to the arena.
   // Returns the final MPS (pool-owned) -- the top side's T_0.
   // on_snap(idx): called after layer snapshot idx has been enqueued on st
+  // gmat (optional): the side's gate array (G, or G^dag for the top side) to
+  // use instead of the stored point's (tn_hvp_cost: trial gates, arena untouched).
   Mps primal_side(cudaStream_t st, Solver& so, Pool& pool, bool is_top, bool store, int* info, double* diag,
-                  const std::function<void(int)>& on_snap = nullptr) {
+                  const std::function<void(int)>& on_snap = nullptr, const cplx* gmat = nullptr) {
     SidePlan& sp = is_top ? top : bot;
-    const cplx* G = is_top ? at(o_gdag) : at(o_gates);
+    const cplx* G = gmat ? gmat : is_top ? at(o_gdag) : at(o_gates);
     Mps P;
     P.a.assign(n, nullptr);
     P.b = sp.init.p;
@@ -804,15 +797,15 @@ struct Engine {
           // Split: Gram heevd (fast) when the cut lies where it resolves the
           // spectrum (smallest kept sigma >= 1e-6 sigma_1 and a boundary gap in
           // sigma^2 >= 1e-12 sigma_1^2), else one-sided Jacobi (relative accuracy).
-          int method = svd_method;
-          int nbas = method == 3 ? 4 * s.bl : s.mn;
+          int method = kGram;
+          int nbas = 4 * s.bl;
           cplx* Acp = tmp.c(nth);
           TN_CUDA(cudaMemcpyAsync(Acp, A, nth * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
           cplx* uhf = tmp.c((int64_t)4 * s.bl * 4 * s.bl);
           double* Sf = (double*)tmp.raw((size_t)4 * s.bl * sizeof(double));
           svd_rowmajor(st, so, tmp, Acp, 4 * s.bl, 4 * s.br, Sf, uhf, info + 1, method);
-          int iters = method == 3 ? 0 : 2;
-          if (method == 3 && s.r < 4 * s.bl) {  // something (discarded or null) is excluded
+          int iters = 0;
+          if (s.r < 4 * s.bl) {  // something (discarded or null) is excluded
             // kept/excluded mixing of a Gram basis ~ eps sigma_top^2 / (sigma_{r-1}^2 - sigma_r^2)
             // (sigma_r = 0 for a null direction); first-order refinement converges
             // quadratically from delta <~ 1e-2.  Otherwise a second Gram level on the
@@ -853,7 +846,7 @@ struct Engine {
               ++n_noise;
             }
             if (delta > 1e-2) {
-              method = fallback_method;
+              method = kQRIter;
               nbas = s.mn;
               iters = 2;
               TN_CUDA(cudaMemcpyAsync(Acp, A, nth * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
@@ -979,15 +972,55 @@ struct Engine {
     TN_CUDA(cudaStreamSynchronize(st));  // pool temporaries are freed on return
   }
 
+  // ABI flag checks, before any work of the call: each gate
+  // ||G^dag G - I||_F <= 1e-10 (TN_CHECK_UNITARY); each direction
+  // ||V - P_G V|| <= 1e-8 ||V|| (TN_CHECK_TANGENT).  TN_EINVAL otherwise.
+  void check_gates(cudaStream_t st, const cplx* G, int Kg) {
+    if (!(cfg.flags & TN_CHECK_UNITARY) || Kg <= 0) return;
+    Pool pool(st);
+    double* res = (double*)pool.raw(sizeof(double) * Kg);
+    check_unitary(st, Kg, G, res);
+    std::vector<double> h(Kg);
+    TN_CUDA(cudaMemcpyAsync(h.data(), res, sizeof(double) * Kg, cudaMemcpyDeviceToHost, st));
+    TN_CUDA(cudaStreamSynchronize(st));
+    for (int k = 0; k < Kg; ++k)
+      if (!(h[k] <= 1e-10))
+        throw std::invalid_argument("gate " + std::to_string(k) + " is not unitary: ||G^dag G - I||_F = " +
+                                    std::to_string(h[k]) + " > 1e-10 (TN_CHECK_UNITARY)");
+  }
+  void check_dirs(cudaStream_t st, const cplx* G, const cplx* V, int batch) {
+    if (!(cfg.flags & TN_CHECK_TANGENT) || batch <= 0) return;
+    Pool pool(st);
+    const int64_t m = (int64_t)K * batch;
+    double* res = (double*)pool.raw(sizeof(double) * 2 * m);
+    check_tangent(st, K, batch, G, V, res);
+    std::vector<double> h(2 * m);
+    TN_CUDA(cudaMemcpyAsync(h.data(), res, sizeof(double) * 2 * m, cudaMemcpyDeviceToHost, st));
+    TN_CUDA(cudaStreamSynchronize(st));
+    for (int b = 0; b < batch; ++b) {
+      double r2 = 0, n2 = 0;
+      for (int k = 0; k < K; ++k) {
+        r2 += h[2 * ((int64_t)b * K + k)];
+        n2 += h[2 * ((int64_t)b * K + k) + 1];
+      }
+      if (!(std::sqrt(r2) <= 1e-8 * std::sqrt(n2)))
+        throw std::invalid_argument("direction " + std::to_string(b) + " is not tangent at G: ||V - P_G V|| = " +
+                                    std::to_string(std::sqrt(r2)) + " > 1e-8 ||V|| = " +
+                                    std::to_string(1e-8 * std::sqrt(n2)) + " (TN_CHECK_TANGENT)");
+    }
+  }
+
   // fwd_out (fused step): also replay the forward tangents of fwd_nb directions
   // fwd_V on stream stf while the sweeps run (see step()).
   void environments(cudaStream_t st, const cplx* gates, double* scalars, cplx* grad_R, int fwd_nb = 0,
                     const cplx* fwd_V = nullptr, std::vector<TanSnap>* fwd_out = nullptr) {
     TN_CUDA(cudaSetDevice(device));
+    check_gates(st, gates, K);
+    if (fwd_out) check_dirs(st, gates, fwd_V, fwd_nb);
     primal_valid = false;
     ti_valid = false;
-    drop_graphs();
-    drop_chain_cache();
+    drop_graphs(st);
+    drop_chain_cache(st);
     n_fallback = 0;
     n_deflate = 0;
     n_noise = 0;
@@ -1246,28 +1279,24 @@ struct Engine {
     }
   }
 
+  // T and f at trial gates (a3 top sweep only, the TR rho test).  The stored
+  // point (arena, caches, graphs) is never touched, so a failure here leaves
+  // the primal store valid for later applies.
   void cost(cudaStream_t st, const cplx* gates, double* scalars) {
     TN_CUDA(cudaSetDevice(device));
+    check_gates(st, gates, K);
     Pool pool(st);
-    cplx* G = pool.c((int64_t)K * 16);
     cplx* Gd = pool.c((int64_t)K * 16);
-    TN_CUDA(cudaMemcpyAsync(G, gates, (size_t)K * 16 * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-    dagger4(st, Gd, G, K);
-    // primal_side reads gates from the arena: swap in temporaries
-    cplx* saved = pool.c((int64_t)K * 16);
-    TN_CUDA(cudaMemcpyAsync(saved, at(o_gdag), (size_t)K * 16 * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-    TN_CUDA(cudaMemcpyAsync(at(o_gdag), Gd, (size_t)K * 16 * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+    dagger4(st, Gd, gates, K);
     int* info = (int*)pool.raw(2 * sizeof(int));
     TN_CUDA(cudaMemsetAsync(info, 0, 2 * sizeof(int), st));
-    Mps T0 = primal_side(st, sol[0], pool, true, false, info, nullptr);
-    TN_CUDA(cudaMemcpyAsync(at(o_gdag), saved, (size_t)K * 16 * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+    Mps T0 = primal_side(st, sol[0], pool, true, false, info, nullptr, nullptr, Gd);
     std::vector<const cplx*> tp(T0.a.begin(), T0.a.end());
     std::vector<int> ones(n + 1, 1);
     std::vector<const cplx*> bp(n);
     cplx* id = pool.c(4);
     const double h = 1.0 / std::sqrt(2.0);
-    cplx idh[4] = {{h, 0}, {0, 0}, {0, 0}, {h, 0}};
-    TN_CUDA(cudaMemcpyAsync(id, idh, sizeof(idh), cudaMemcpyHostToDevice, st));
+    set_small(st, id, 4, {h, 0.0}, ZERO, ZERO, {h, 0.0});
     for (int s = 0; s < n; ++s) bp[s] = id;
     cplx* T11 = overlap(st, pool, tp, T0.b, bp, ones);
     for (cplx*& p : T0.a) ddel(p, st);
@@ -1276,9 +1305,13 @@ struct Engine {
     finish_cost(st, sc, T11);
     TN_CUDA(cudaMemcpyAsync(scalars, sc, 8 * sizeof(double), cudaMemcpyDeviceToDevice, st));
     int hinfo[2];
+    double hsc[3];
     TN_CUDA(cudaMemcpyAsync(hinfo, info, sizeof(hinfo), cudaMemcpyDeviceToHost, st));
+    TN_CUDA(cudaMemcpyAsync(hsc, sc, sizeof(hsc), cudaMemcpyDeviceToHost, st));
     TN_CUDA(cudaStreamSynchronize(st));
     if (hinfo[0] != 0 || hinfo[1] != 0) throw NumericError("cuSOLVER info nonzero in tn_hvp_cost");
+    if (!std::isfinite(hsc[0]) || !std::isfinite(hsc[1]) || !std::isfinite(hsc[2]))
+      throw NumericError("tn_hvp_cost: non-finite T");
   }
 
   // ---------------------------------------------------- tangent pass --
@@ -1368,33 +1401,35 @@ struct Engine {
       }
     return e;
   }
-  // the side's cache if enabled and it fits (keeping half the free memory)
-  ChainCache* chain_cache_for(int side) {
+  // The side's cache if enabled and it fits (keeping half the free memory).
+  // Inside a stream capture only an already-built cache is used: recording
+  // there would store graph-owned allocations in it.
+  ChainCache* chain_cache_for(int side, cudaStream_t st) {
     if (!chain_cache_enabled) return nullptr;
     ChainCache& c = chain_cache[side];
     if (c.built) return &c;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    TN_CUDA(cudaStreamIsCapturing(st, &cs));
+    if (cs != cudaStreamCaptureStatusNone) return nullptr;
     size_t fr = 0, tot = 0;
     TN_CUDA(cudaMemGetInfo(&fr, &tot));
     const size_t need = sizeof(cplx) * (size_t)chain_cache_elems(side ? top : bot);
     return need < fr / 2 ? &c : nullptr;
   }
-  void drop_chain_cache() {
+  // Release the per-point caches, stream-ordered on st: every use of them was
+  // enqueued on st or joined into it (calls on one context are stream-ordered,
+  // tn_hvp.h), so no host or device-wide synchronisation is needed.  Blocks go
+  // back to the library pool (not trimmed: the next pass reuses them).
+  void drop_chain_cache(cudaStream_t st) {
     memo_budget_set = false;
-    bool any = !memo_owned.empty();
-    for (ChainCache& c : chain_cache) any = any || !c.owned.empty();
-    if (!any) return;
-    cudaDeviceSynchronize();
     for (ChainCache& c : chain_cache) {
-      for (cplx* p : c.owned) cudaFreeAsync(p, stc);
+      for (cplx* p : c.owned) dfree(p, st);
       c = ChainCache{};
     }
-    for (cplx* p : memo_owned) cudaFreeAsync(p, stc);
+    for (cplx* p : memo_owned) dfree(p, st);
     memo_owned.clear();
     memo_map.clear();
     memo_bytes = 0;
-    cudaStreamSynchronize(stc);
-    // no pool trim here: this runs on every primal pass, and returning the
-    // pooled memory would make the next step re-map it (~3 s per C4 step)
   }
 
   template <class F>
@@ -1920,7 +1955,7 @@ struct Engine {
                                         const std::function<void(int)>& before_layer = nullptr) {
     std::vector<TanSnap> DB(D);
     Tangent t;
-    tangent_init(st, t, bot, false, nb, chain_cache_for(0));
+    tangent_init(st, t, bot, false, nb, chain_cache_for(0, st));
     for (size_t li = 0; li < bot.steps.size(); ++li) {
       DB[li] = take_snapshot(st, t, nb);
       if (before_layer) before_layer((int)li);
@@ -1961,7 +1996,7 @@ struct Engine {
       }
       // backward (top) tangent on the fly + layer HVP extraction
       Tangent t;
-      tangent_init(st, t, top, true, nb, chain_cache_for(1));
+      tangent_init(st, t, top, true, nb, chain_cache_for(1, st));
       for (size_t li = 0; li < top.steps.size(); ++li) {
         const int ell = top.ell[li];
         if (phases) TN_CUDA(cudaEventRecord(pe[2], st));
@@ -2004,33 +2039,37 @@ struct Engine {
     work_fwd_first = 0;
   }
 
-  void drop_graphs() {
+  // Replays run on the caller's stream: wait for that stream only (not the
+  // device) before the executable graphs and their I/O buffers go.
+  void drop_graphs(cudaStream_t st) {
     if (graphs.empty()) return;
-    cudaDeviceSynchronize();  // no replay may still read the buffers
+    TN_CUDA(cudaStreamSynchronize(st));
     for (ApplyGraph& g : graphs) {
       if (g.exec) cudaGraphExecDestroy(g.exec);
-      for (cplx* p : {g.in, g.out, g.auxb})
-        if (p) cudaFree(p);
+      for (cplx* p : {g.in, g.out, g.auxb}) dfree(p, st);
     }
     graphs.clear();
     cudaDeviceGraphMemTrim(device);
   }
 
-  // return cached-but-free pool memory (stream-ordered pool and graph pool) to
-  // the device so that other allocators (torch) can use it
-  void trim_pools() {
-    cudaDeviceSynchronize();
-    cudaMemPool_t mp;
-    if (cudaDeviceGetDefaultMemPool(&mp, device) == cudaSuccess) cudaMemPoolTrimTo(mp, 0);
-    cudaDeviceGraphMemTrim(device);
+  // tn_hvp_trim_memory: drop the per-point caches and graphs (rebuilt by the
+  // next apply) and return the library pool's unused blocks to the device.
+  void trim_memory(cudaStream_t st) {
+    drop_graphs(st);
+    drop_chain_cache(st);
+    TN_CUDA(cudaStreamSynchronize(st));
+    pool_trim(device);
   }
 
-  bool capture(ApplyGraph& g) {
+  bool capture(ApplyGraph& g, cudaStream_t st) {
     const int64_t n = (int64_t)g.batch * K * 16;
-    TN_CUDA(cudaMalloc(&g.in, sizeof(cplx) * n));
-    TN_CUDA(cudaMalloc(&g.out, sizeof(cplx) * n));
-    if (g.aux) TN_CUDA(cudaMalloc(&g.auxb, sizeof(cplx) * (n + g.batch)));
-    TN_CUDA(cudaMemset(g.in, 0, sizeof(cplx) * n));
+    g.in = (cplx*)dalloc(sizeof(cplx) * n, st);
+    g.out = (cplx*)dalloc(sizeof(cplx) * n, st);
+    if (g.aux) g.auxb = (cplx*)dalloc(sizeof(cplx) * (n + g.batch), st);
+    TN_CUDA(cudaMemsetAsync(g.in, 0, sizeof(cplx) * n, st));
+    // the capture stream starts after the caller's stream (buffers ready)
+    TN_CUDA(cudaEventRecord(ev_fork, st));
+    TN_CUDA(cudaStreamWaitEvent(stc, ev_fork, 0));
     const int64_t l0 = launch_count();
     const double w0 = work_counter.load();
     cudaGraph_t graph = nullptr;
@@ -2066,6 +2105,7 @@ struct Engine {
   void apply_call(cudaStream_t st, int batch, const cplx* dirs, cplx* hess, cplx* aux) {
     TN_CUDA(cudaSetDevice(device));
     if (!primal_valid) throw StateError("tn_hvp_apply before tn_hvp_environments");
+    check_dirs(st, at(o_gates), dirs, batch);
     // graphs pay off for launch-bound small batches (truncated CG: batch 1);
     // large batches are GEMM-bound and would double the memory footprint
     if (!graphs_enabled || batch <= 0 || batch > kGraphMaxBatch || gemm_profile_active() || std::getenv("TN_PHASES")) {
@@ -2085,7 +2125,7 @@ struct Engine {
       apply(st, batch, dirs, hess, aux);
       return;
     }
-    if (!g->exec && !capture(*g)) {
+    if (!g->exec && !capture(*g, st)) {
       g->failed = true;
       apply(st, batch, dirs, hess, aux);
       return;
@@ -2118,6 +2158,8 @@ struct Engine {
       environments(st, gates, scalars, grad_R);
       return;
     }
+    check_gates(st, gates, K);
+    check_dirs(st, gates, dirs, batch);
     std::vector<TanSnap> DB0;
     environments(st, gates, scalars, grad_R, std::min(batch, cfg.max_batch), dirs, &DB0);
     apply(st, batch, dirs, hess, aux, &DB0);
@@ -2132,9 +2174,10 @@ struct tn_hvp_ctx {
 
 namespace tn {
 
-tn_hvp_ctx* engine_create(const tn_hvp_config& cfg, const int32_t* ref_bonds, const void* ref_mpo, cudaStream_t st) {
+tn_hvp_ctx* engine_create(const tn_hvp_config& cfg, const int32_t* ref_bonds, const void* ref_mpo, void* primal_buf,
+                          size_t primal_bytes, cudaStream_t st) {
   auto ctx = std::make_unique<tn_hvp_ctx>();
-  ctx->e.setup(cfg, ref_bonds, ref_mpo, st);
+  ctx->e.setup(cfg, ref_bonds, ref_mpo, primal_buf, primal_bytes, st);
   TN_CUDA(cudaStreamSynchronize(st));
   return ctx.release();
 }
@@ -2166,18 +2209,59 @@ void engine_primal_blob(tn_hvp_ctx* ctx, void** ptr, size_t* bytes) {
   *ptr = ctx->e.arena;
   *bytes = ctx->e.arena_bytes;
 }
+// After a collective filled the primal store (tn_hvp_primal_copy into the
+// context): the blob carries the point's gates (o_gates); they must be the
+// caller's `gates` bit for bit, else TN_EINVAL and the store stays invalid.
 void engine_primal_imported(tn_hvp_ctx* ctx, const cplx* gates, cudaStream_t st) {
   Engine& e = ctx->e;
-  (void)gates;
-  e.drop_graphs();
-  e.drop_chain_cache();
+  TN_CUDA(cudaSetDevice(e.device));
+  e.primal_valid = false;
+  e.ti_valid = false;
+  e.drop_graphs(st);
+  e.drop_chain_cache(st);
+  std::vector<cplx> hg((size_t)e.K * 16), hb((size_t)e.K * 16);
+  TN_CUDA(cudaMemcpyAsync(hg.data(), gates, sizeof(cplx) * hg.size(), cudaMemcpyDeviceToHost, st));
+  TN_CUDA(cudaMemcpyAsync(hb.data(), e.at(e.o_gates), sizeof(cplx) * hb.size(), cudaMemcpyDeviceToHost, st));
   for (SidePlan* sp : {&e.bot, &e.top})
     for (auto& ls : sp->steps)
       for (Step& s : ls)
         if (s.type == PAIR)
           TN_CUDA(cudaMemcpyAsync(&e.h_s[s.s_index], e.at<double>(s.o_s), sizeof(double), cudaMemcpyDeviceToHost, st));
   TN_CUDA(cudaStreamSynchronize(st));
+  if (std::memcmp(hg.data(), hb.data(), sizeof(cplx) * hg.size()) != 0)
+    throw std::invalid_argument("tn_hvp_primal_imported: gates differ from the imported primal store's point");
   e.primal_valid = true;
+}
+// tn_hvp_primal_copy: into_ctx = 1 overwrites the store, so everything that
+// describes the old point is invalidated first (valid again after
+// tn_hvp_primal_imported).
+void engine_primal_copy(tn_hvp_ctx* ctx, void* buf, size_t bytes, int into_ctx, cudaStream_t st) {
+  Engine& e = ctx->e;
+  TN_CUDA(cudaSetDevice(e.device));
+  if (bytes != e.arena_bytes) throw std::invalid_argument("tn_hvp_primal_copy: size mismatch");
+  if (into_ctx) {
+    e.primal_valid = false;
+    e.ti_valid = false;
+    e.drop_graphs(st);
+    e.drop_chain_cache(st);
+    if (buf != e.arena)  // buf == the store: the caller fills it in place (invalidate only)
+      TN_CUDA(cudaMemcpyAsync(e.arena, buf, bytes, cudaMemcpyDeviceToDevice, st));
+  } else {
+    if (!e.primal_valid) throw StateError("tn_hvp_primal_copy: no valid primal pass to export");
+    TN_CUDA(cudaMemcpyAsync(buf, e.arena, bytes, cudaMemcpyDeviceToDevice, st));
+  }
+}
+void engine_trim_memory(tn_hvp_ctx* ctx, cudaStream_t st) {
+  TN_CUDA(cudaSetDevice(ctx->e.device));
+  ctx->e.trim_memory(st);
+}
+void engine_query(const tn_hvp_config& cfg, const int32_t* ref_bonds, size_t* primal_bytes, size_t* work_bytes,
+                  size_t* per_dir_bytes) {
+  Engine e;
+  e.plan(cfg, ref_bonds);
+  *primal_bytes = e.arena_bytes;
+  *work_bytes = e.chain_cache_bytes();
+  *per_dir_bytes = e.per_direction_bytes();
 }
 void engine_work(tn_hvp_ctx* ctx, double* per_dir, double* primal) {
   *per_dir = ctx->e.work_apply;

@@ -11,7 +11,8 @@ struct StateError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 
-tn_hvp_ctx* engine_create(const tn_hvp_config& cfg, const int32_t* ref_bonds, const void* ref_mpo, cudaStream_t st);
+tn_hvp_ctx* engine_create(const tn_hvp_config& cfg, const int32_t* ref_bonds, const void* ref_mpo, void* primal_buf,
+                          size_t primal_bytes, cudaStream_t st);
 void engine_environments(tn_hvp_ctx* ctx, const cplx* gates, double* scalars, cplx* grad_R, cudaStream_t st);
 void engine_apply(tn_hvp_ctx* ctx, int batch, const cplx* dirs, cplx* hess_R, cplx* aux, cudaStream_t st);
 void engine_step(tn_hvp_ctx* ctx, const cplx* gates, double* scalars, cplx* grad_R, int batch, const cplx* dirs,
@@ -22,6 +23,8 @@ void engine_ti_apply(tn_hvp_ctx* ctx, int batch, const cplx* v, cplx* hess_R, cu
 void engine_cost(tn_hvp_ctx* ctx, const cplx* gates, double* scalars, cudaStream_t st);
 void engine_primal_blob(tn_hvp_ctx* ctx, void** ptr, size_t* bytes);
 void engine_primal_imported(tn_hvp_ctx* ctx, const cplx* gates, cudaStream_t st);
+void engine_primal_copy(tn_hvp_ctx* ctx, void* buf, size_t bytes, int into_ctx, cudaStream_t st);
+void engine_trim_memory(tn_hvp_ctx* ctx, cudaStream_t st);
 void engine_work(tn_hvp_ctx* ctx, double* per_dir, double* primal);
 void engine_query(const tn_hvp_config& cfg, const int32_t* ref_bonds, size_t* primal_bytes, size_t* work_bytes,
                   size_t* per_dir_bytes);

@@ -309,7 +309,7 @@ void extract_env(cudaStream_t st, cplx* E, int64_t sE, const cplx* top, int64_t 
   if (bx < 1) bx = 1;
   if (bx > 64) bx = 64;
   double* part = nullptr;
-  TN_CUDA(cudaMallocAsync((void**)&part, sizeof(double) * 32 * bx * (size_t)batch, st));
+  part = (double*)dalloc(sizeof(double) * 32 * bx * (size_t)batch, st);
   if (std::getenv("TN_POISON")) TN_CUDA(cudaMemsetAsync(part, 0xFF, sizeof(double) * 32 * bx * (size_t)batch, st));
   dim3 grid(bx, batch);
   extract_env_kernel<<<grid, TPB, 0, st>>>(part, top, stop, z, sz, T, U);
@@ -318,7 +318,7 @@ void extract_env(cudaStream_t st, cplx* E, int64_t sE, const cplx* top, int64_t 
   extract_finish_kernel<<<batch, 32, 0, st>>>(E, sE, part, bx, alpha);
   TN_CUDA(cudaGetLastError());
   count_launch();
-  TN_CUDA(cudaFreeAsync(part, st));
+  dfree(part, st);
 }
 
 void project(cudaStream_t st, int K, int batch, const cplx* G, const cplx* in, cplx* out) {
@@ -367,47 +367,6 @@ __global__ void transpose_kernel(cplx* __restrict__ dst, const cplx* __restrict_
       dst[(int64_t)c * rows + r] = v;
     }
   }
-}
-
-__global__ void svd_post_kernel(const double* __restrict__ S, int mn, int r, double* s_out, double* diag) {
-  __shared__ double red[2][32];
-  double all = 0, kept = 0;
-  for (int i = threadIdx.x; i < mn; i += blockDim.x) {
-    const double v = S[i] * S[i];
-    all += v;
-    if (i < r) kept += v;
-  }
-  for (int off = 16; off > 0; off >>= 1) {
-    all += __shfl_xor_sync(0xffffffffu, all, off);
-    kept += __shfl_xor_sync(0xffffffffu, kept, off);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    red[0][threadIdx.x >> 5] = all;
-    red[1][threadIdx.x >> 5] = kept;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double a = 0, k = 0;
-    for (int j = 0; j < (int)(blockDim.x >> 5); ++j) {
-      a += red[0][j];
-      k += red[1][j];
-    }
-    const double s = sqrt(a / k);
-    s_out[0] = s;
-    if (diag) {
-      diag[0] = fmax(diag[0], 1.0 - k / a);
-      if (r < mn) diag[1] = fmin(diag[1], (S[r - 1] - S[r]) / S[0]);
-      diag[2] = fmax(diag[2], fabs(log10(s)));
-    }
-  }
-}
-
-__global__ void scale_rows_kernel(cplx* __restrict__ dst, const cplx* __restrict__ src, int rows, int cols,
-                                  const double* __restrict__ S, const double* __restrict__ s) {
-  const int64_t n = (int64_t)rows * cols;
-  const double f = s ? s[0] : 1.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    dst[i] = cscale(src[i], f * S[i / cols]);
 }
 
 __global__ void conjT_scale_kernel(cplx* __restrict__ dst, const cplx* __restrict__ uh, int r, int m,
@@ -628,21 +587,6 @@ void transpose(cudaStream_t st, cplx* dst, const cplx* src, int rows, int cols, 
   count_launch();
 }
 
-void svd_post(cudaStream_t st, const double* S, int mn, int r, double* s_out, double* diag) {
-  svd_post_kernel<<<1, 256, 0, st>>>(S, mn, r, s_out, diag);
-  TN_CUDA(cudaGetLastError());
-  count_launch();
-}
-
-void scale_rows_sv(cudaStream_t st, cplx* dst, const cplx* src, int rows, int cols, const double* S,
-                   const double* s) {
-  const int64_t n = (int64_t)rows * cols;
-  if (!n) return;
-  scale_rows_kernel<<<nblocks(n), TPB, 0, st>>>(dst, src, rows, cols, S, s);
-  TN_CUDA(cudaGetLastError());
-  count_launch();
-}
-
 void conjT_scale_cols(cudaStream_t st, cplx* dst, const cplx* uh, int r, int m, const double* S, const double* s) {
   const int64_t n = (int64_t)r * m;
   if (!n) return;
@@ -727,7 +671,7 @@ void tangent_dot(cudaStream_t st, int64_t n, int batch, const cplx* A, const cpl
   int nblk = (int)std::min<int64_t>((n + 2047) / 2048, 256);
   if (nblk < 1) nblk = 1;
   double* part = nullptr;
-  TN_CUDA(cudaMallocAsync((void**)&part, sizeof(double) * (size_t)nblk * batch, st));
+  part = (double*)dalloc(sizeof(double) * (size_t)nblk * batch, st);
   if (std::getenv("TN_POISON")) TN_CUDA(cudaMemsetAsync(part, 0xFF, sizeof(double) * (size_t)nblk * batch, st));
   tangent_dot_kernel<<<dim3(nblk, batch), 256, 0, st>>>(n, A, B, part);
   TN_CUDA(cudaGetLastError());
@@ -735,7 +679,7 @@ void tangent_dot(cudaStream_t st, int64_t n, int batch, const cplx* A, const cpl
   dot_finish_kernel<<<batch, 32, 0, st>>>(part, nblk, out);
   TN_CUDA(cudaGetLastError());
   count_launch();
-  TN_CUDA(cudaFreeAsync(part, st));
+  dfree(part, st);
 }
 
 void finish_cost(cudaStream_t st, double* scalars, const cplx* T11) {
@@ -799,4 +743,64 @@ void set_small(cudaStream_t st, cplx* p, int n, cplx v0, cplx v1, cplx v2, cplx 
   count_launch();
 }
 
+}  // namespace tn
+
+namespace tn {
+// Argument checks of the ABI flags: per gate
+// res[k] = ||G_k^dag G_k - I||_F; per (direction, gate) the squared norms of
+// V - P_G(V) = (V + G V^dag G)/2 and of V (host reduces per direction).
+__global__ void unitarity_kernel(int K, const cplx* __restrict__ G, double* __restrict__ res) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  const cplx* g = G + (int64_t)k * 16;
+  double acc = 0;
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) {
+      cplx v = make_double2(i == j ? -1.0 : 0.0, 0.0);
+      for (int a = 0; a < 4; ++a) v = cadd(v, cmulc(g[a * 4 + i], g[a * 4 + j]));
+      acc += v.x * v.x + v.y * v.y;
+    }
+  res[k] = sqrt(acc);
+}
+
+__global__ void tangency_kernel(int K, int batch, const cplx* __restrict__ G, const cplx* __restrict__ V,
+                                double* __restrict__ res) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)K * batch) return;
+  const int k = (int)(t % K);
+  const cplx* g = G + (int64_t)k * 16;
+  const cplx* v = V + t * 16;
+  cplx w[16];  // V^dag G
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) {
+      cplx a = make_double2(0.0, 0.0);
+      for (int c = 0; c < 4; ++c) a = cadd(a, cmulc(v[c * 4 + i], g[c * 4 + j]));
+      w[i * 4 + j] = a;
+    }
+  double r2 = 0, n2 = 0;
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) {
+      cplx a = v[i * 4 + j];
+      n2 += a.x * a.x + a.y * a.y;
+      for (int c = 0; c < 4; ++c) a = cadd(a, cmul(g[i * 4 + c], w[c * 4 + j]));
+      r2 += 0.25 * (a.x * a.x + a.y * a.y);
+    }
+  res[2 * t] = r2;
+  res[2 * t + 1] = n2;
+}
+
+void check_unitary(cudaStream_t st, int K, const cplx* G, double* res) {
+  if (K <= 0) return;
+  unitarity_kernel<<<(K + 127) / 128, 128, 0, st>>>(K, G, res);
+  TN_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+void check_tangent(cudaStream_t st, int K, int batch, const cplx* G, const cplx* V, double* res) {
+  const int64_t n = (int64_t)K * batch;
+  if (n <= 0) return;
+  tangency_kernel<<<(int)((n + 127) / 128), 128, 0, st>>>(K, batch, G, V, res);
+  TN_CUDA(cudaGetLastError());
+  count_launch();
+}
 }  // namespace tn

@@ -22,13 +22,6 @@ void hessian_post(cudaStream_t st, int K, int batch, const cplx* G, const cplx* 
 namespace tn {
 // dst[c][r] = (conj?) src[r][c]; src rows x cols row-major (ld = cols).
 void transpose(cudaStream_t st, cplx* dst, const cplx* src, int rows, int cols, bool conj);
-// Singular values S[0..mn) descending, keep r: s = ||S|| / ||S_r||.
-// Writes s to s_out[0]; diag[0] = max(diag[0], discarded weight),
-// diag[1] = min(diag[1], relative gap (S[r-1]-S[r])/S[0]), diag[2] = max(diag[2], |log10 s|).
-void svd_post(cudaStream_t st, const double* S, int mn, int r, double* s_out, double* diag);
-// dst[i][j] = s * S[i] * src[i][j]  (rows x cols), s from device (pw 1).
-void scale_rows_sv(cudaStream_t st, cplx* dst, const cplx* src, int rows, int cols, const double* S,
-                   const double* s);
 // dst[a][j] = conj(uh[j][a]) * (S ? s*S[j] : 1)  for uh (r x m) row-major -> dst (m x r).
 void conjT_scale_cols(cudaStream_t st, cplx* dst, const cplx* uh, int r, int m, const double* S, const double* s);
 // Row-major (rows x cols) from the upper triangle of a column-major buffer
@@ -45,7 +38,8 @@ void combine_diag(cudaStream_t st, double* out, const double* d);
 void kept_rotation(cudaStream_t st, cplx* Cm, const cplx* M, const double* S, int nd, int r);
 // heevd output (column-major W, ascending lam) -> uhf = U^H rows (descending), S = sqrt(lam)
 void eig_to_svd(cudaStream_t st, cplx* uhf, double* S, const cplx* W, const double* lam, int R);
-// s = sqrt(nrm[0]/nrm[1]) into s_out; diag as in svd_post
+// s = sqrt(nrm[0]/nrm[1]) into s_out; diag[0] = max(diag[0], discarded weight),
+// diag[1] = min(diag[1], relative gap (S[r-1]-S[r])/S[0]), diag[2] = max(diag[2], |log10 s|)
 void s_from_norms(cudaStream_t st, const double* nrm, const double* S, int mn, int r, double* s_out, double* diag);
 // dst[(o1 o2)][x][i1 i2][y] = src[x][(o1 i1)][(o2 i2)][y]
 void out_leg_split(cudaStream_t st, cplx* dst, const cplx* src, int X, int Y);
@@ -82,4 +76,12 @@ namespace tn {
 // host copies, so the apply path can be captured into a CUDA graph)
 void set_small(cudaStream_t st, cplx* p, int n, cplx v0, cplx v1 = {0.0, 0.0}, cplx v2 = {0.0, 0.0},
                cplx v3 = {0.0, 0.0});
+}  // namespace tn
+
+namespace tn {
+// ABI flag checks.  res[k] = ||G_k^dag G_k - I||_F (DEVICE
+// double[K]); res[2 (b K + k) + {0,1}] = (||V - P_G V||^2, ||V||^2) of gate k of
+// direction b (DEVICE double[2 batch K]).
+void check_unitary(cudaStream_t st, int K, const cplx* G, double* res);
+void check_tangent(cudaStream_t st, int K, int batch, const cplx* G, const cplx* V, double* res);
 }  // namespace tn

@@ -159,7 +159,7 @@ void sym_eig(cudaStream_t st, int n, double* A, double* w, double* asym, bool ve
   const int64_t total = (int64_t)n * n;
   const int nblk = std::min(grid_for(total, 256), 1024);
   double* part = nullptr;
-  TN_CUDA(cudaMallocAsync((void**)&part, sizeof(double) * 2 * nblk, st));
+  part = (double*)dalloc(sizeof(double) * 2 * nblk, st);
   asym_norms_kernel<<<nblk, 256, 0, st>>>(n, A, part);
   TN_CUDA(cudaGetLastError());
   asym_finish_kernel<<<1, 32, 0, st>>>(part, nblk, asym);
@@ -167,7 +167,7 @@ void sym_eig(cudaStream_t st, int n, double* A, double* w, double* asym, bool ve
   symmetrize_kernel<<<grid_for(total, 256), 256, 0, st>>>(n, A);
   TN_CUDA(cudaGetLastError());
   count_launch(3);
-  TN_CUDA(cudaFreeAsync(part, st));
+  dfree(part, st);
   cusolverDnHandle_t h = nullptr;
   auto chk = [](cusolverStatus_t s, const char* what) {
     if (s != CUSOLVER_STATUS_SUCCESS) throw CudaError(std::string(what) + ": cuSOLVER status " + std::to_string((int)s));
@@ -180,13 +180,13 @@ void sym_eig(cudaStream_t st, int n, double* A, double* w, double* asym, bool ve
     chk(cusolverDnDsyevd_bufferSize(h, jobz, CUBLAS_FILL_MODE_LOWER, n, A, n, w, &lwork), "Dsyevd_bufferSize");
     double* work = nullptr;
     int* info = nullptr;
-    TN_CUDA(cudaMallocAsync((void**)&work, sizeof(double) * std::max(lwork, 1), st));
-    TN_CUDA(cudaMallocAsync((void**)&info, sizeof(int), st));
+    work = (double*)dalloc(sizeof(double) * std::max(lwork, 1), st);
+    info = (int*)dalloc(sizeof(int), st);
     chk(cusolverDnDsyevd(h, jobz, CUBLAS_FILL_MODE_LOWER, n, A, n, w, work, lwork, info), "Dsyevd");
     int hinfo = 0;
     TN_CUDA(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, st));
-    TN_CUDA(cudaFreeAsync(work, st));
-    TN_CUDA(cudaFreeAsync(info, st));
+    dfree(work, st);
+    dfree(info, st);
     TN_CUDA(cudaStreamSynchronize(st));
     if (hinfo != 0) throw NumericError("tn_sym_eig: syevd info " + std::to_string(hinfo));
   } catch (...) {

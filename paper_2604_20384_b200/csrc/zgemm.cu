@@ -29,7 +29,7 @@ struct Prof {
   bool on = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
   std::vector<double> cm;
-  std::vector<std::array<int, 6>> shape;  // M, N, K, batch, opa, opb
+  std::vector<std::array<int, 9>> shape;  // M, N, K, batch, opa, opb, A batched, B batched, has beta
 };
 Prof g_prof;
 std::mutex g_prof_mu;
@@ -362,7 +362,7 @@ void launch(const Params& p, int batch, cudaStream_t st) {
     int ks = (int)std::min<int64_t>((296 + ctas - 1) / ctas, nk / 8);
     if (ks > 1) {
       q.ksplit = ks;
-      TN_CUDA(cudaMallocAsync((void**)&q.part, sizeof(cplx) * (size_t)ks * p.M * p.N * batch, st));
+      q.part = (double*)dalloc(sizeof(cplx) * (size_t)ks * p.M * p.N * batch, st);
       if (std::getenv("TN_POISON")) TN_CUDA(cudaMemsetAsync(q.part, 0xFF, sizeof(cplx) * (size_t)ks * p.M * p.N * batch, st));
       grid.z = batch * ks;
     }
@@ -386,14 +386,14 @@ void launch(const Params& p, int batch, cudaStream_t st) {
     zreduce_kernel<<<(int)std::min<int64_t>((tot + 255) / 256, 148 * 16), 256, 0, st>>>(q, batch);
     TN_CUDA(cudaGetLastError());
     count_launch();
-    TN_CUDA(cudaFreeAsync(q.part, st));
+    dfree(q.part, st);
   }
   if (g_prof.on) {
     TN_CUDA(cudaEventRecord(e1, st));
     std::lock_guard<std::mutex> lk(g_prof_mu);
     g_prof.ev.push_back({e0, e1});
     g_prof.cm.push_back((double)p.M * p.N * p.K * batch);
-    g_prof.shape.push_back({p.M, p.N, p.K, batch, (int)OPA, (int)OPB});
+    g_prof.shape.push_back({p.M, p.N, p.K, batch, (int)OPA, (int)OPB, p.sA != 0, p.sB != 0, p.has_beta});
   }
 }
 
@@ -411,6 +411,66 @@ void dispatch_b(char opb, const Params& p, int batch, cudaStream_t st) {
 }  // namespace
 
 void count_launch(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// Library-private stream-ordered memory: one cudaMemPool per device, created on
+// first use, never the device's default pool (so torch's and other libraries'
+// allocations are not affected by its policies).  Cached blocks are kept
+// (release threshold max) and not reused across streams through implicit
+// dependencies (the two primal sweeps run on two streams and must not be
+// serialised through recycled blocks).  Inside a stream capture the allocation
+// becomes a graph memory node (cudaMallocAsync).
+namespace {
+std::mutex g_pool_mu;
+cudaMemPool_t g_pools[64] = {};
+cudaMemPool_t device_pool(int dev) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (dev < 0 || dev >= 64) throw std::invalid_argument("device ordinal");
+  if (!g_pools[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t p = nullptr;
+    TN_CUDA(cudaMemPoolCreate(&p, &props));
+    uint64_t thr = UINT64_MAX;
+    int off = 0;
+    TN_CUDA(cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr));
+    TN_CUDA(cudaMemPoolSetAttribute(p, cudaMemPoolReuseFollowEventDependencies, &off));
+    TN_CUDA(cudaMemPoolSetAttribute(p, cudaMemPoolReuseAllowOpportunistic, &off));
+    TN_CUDA(cudaMemPoolSetAttribute(p, cudaMemPoolReuseAllowInternalDependencies, &off));
+    g_pools[dev] = p;
+  }
+  return g_pools[dev];
+}
+}  // namespace
+
+void* dalloc(size_t bytes, cudaStream_t st) {
+  void* p = nullptr;
+  bytes = std::max<size_t>(bytes, 16);
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  TN_CUDA(cudaStreamIsCapturing(st, &cs));
+  if (cs != cudaStreamCaptureStatusNone) {
+    TN_CUDA(cudaMallocAsync(&p, bytes, st));
+    return p;
+  }
+  int dev = 0;
+  TN_CUDA(cudaGetDevice(&dev));
+  TN_CUDA(cudaMallocFromPoolAsync(&p, bytes, device_pool(dev), st));
+  return p;
+}
+
+void dfree(void* p, cudaStream_t st) {
+  if (p) cudaFreeAsync(p, st);
+}
+
+void pool_trim(int dev) {
+  cudaMemPool_t p = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (dev >= 0 && dev < 64) p = g_pools[dev];
+  }
+  if (p) cudaMemPoolTrimTo(p, 0);
+}
 int64_t launch_count() { return g_launches.load(); }
 
 bool gemm_profile_active() {
@@ -444,7 +504,8 @@ void gemm_profile_end(double* ms, double* cmac) {
     c += g_prof.cm[i];
     if (log) {
       const auto& sh = g_prof.shape[i];
-      std::fprintf(log, "%d %d %d %d %c %c %.6f\n", sh[0], sh[1], sh[2], sh[3], (char)sh[4], (char)sh[5], m);
+      std::fprintf(log, "%d %d %d %d %c %c %.6f %d %d %d\n", sh[0], sh[1], sh[2], sh[3], (char)sh[4], (char)sh[5], m,
+                   sh[6], sh[7], sh[8]);
     }
     cudaEventDestroy(g_prof.ev[i].first);
     cudaEventDestroy(g_prof.ev[i].second);

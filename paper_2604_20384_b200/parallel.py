@@ -7,8 +7,14 @@ HVP is exchanged; the collectives here are outside the hot loop:
   * gather_rows(local, total, group) -- all_gather of per-rank results
                                         (padded to equal length) in rank order;
   * broadcast_primal(eng, gates, src) -- primal store of rank `src` to all
-                                        ranks (strong-scaling use: one primal
-                                        pass, many ranks applying).
+                                        ranks, in place (one primal pass, many
+                                        ranks applying);
+  * sharded_step(eng, gates, dirs)    -- the strong-scaling step bench.py
+                                        times for N > 1: primal once, broadcast,
+                                        B/N directions per rank, all_gather.
+Every function only needs the engine's methods (environments, apply,
+primal_store, invalidate_primal, primal_imported, scalars), so the CPU tests
+drive the same choreography over gloo with a stand-in engine.
 """
 from __future__ import annotations
 
@@ -46,15 +52,43 @@ def gather_rows(local: torch.Tensor, total: int, group=None) -> torch.Tensor:
 
 
 def broadcast_primal(eng, gates: torch.Tensor, src: int = 0, group=None):
-    """Rank `src` has run eng.environments(gates); every other rank receives
-    its primal store over NCCL and marks it valid (tn_hvp_primal_imported)."""
-    from .api import primal_export, primal_import
-    _, nbytes = eng.primal_blob()
-    if dist.get_rank(group) == src:
-        buf = primal_export(eng)
-    else:
-        buf = torch.empty(nbytes, dtype=torch.uint8, device=eng.device)
+    """Rank `src` has run eng.environments(gates) (or eng.step); every other
+    rank receives the primal store IN PLACE (the store is the engine's
+    caller-owned torch buffer, eng.primal_store()) and marks it valid
+    (eng.primal_imported -> tn_hvp_primal_imported, which checks that the
+    received store's point is `gates`).  Returns the store."""
+    buf = eng.primal_store()
+    receiver = dist.get_rank(group) != src
+    if receiver:
+        eng.invalidate_primal()   # the old point's caches must not outlive the overwrite
     dist.broadcast(buf, src=src, group=group)
-    if dist.get_rank(group) != src:
-        primal_import(eng, buf, gates)
+    if receiver:
+        eng.primal_imported(gates)
     return buf
+
+
+def sharded_step(eng, gates: torch.Tensor, dirs: torch.Tensor, src: int = 0, group=None, out=None):
+    """One strong-scaling step of the hot path (north_star):
+    the primal pass once on rank `src` (eng.environments), its store broadcast
+    in place to every rank (broadcast_primal), each rank applying its
+    contiguous share of the B directions (shard), the Riemannian HVPs
+    all-gathered in direction order (gather_rows).  Every rank passes the same
+    gates and all B directions; returns (scalars [8], Hess_R [B, K, 4, 4]) on
+    every rank (scalars broadcast from `src`).  `out`: optional [B,K,4,4]
+    buffer for the gathered result."""
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if rank == src:
+        eng.environments(gates)
+    broadcast_primal(eng, gates, src, group)
+    dist.broadcast(eng.scalars, src=src, group=group)
+    B = dirs.shape[0]
+    start, count = shard(B, rank, world)
+    if count:
+        local = eng.apply(dirs[start:start + count])
+    else:
+        local = dirs.new_zeros((0,) + tuple(dirs.shape[1:]))
+    full = gather_rows(local, B, group)
+    if out is not None:
+        out.copy_(full)
+        full = out
+    return eng.scalars, full

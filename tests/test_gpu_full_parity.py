@@ -1,0 +1,91 @@
+"""Full-size parity, default on: the CUDA path at C3, C4 and a full-width C5
+case against oracle outputs stored in tests/golden/ by tools/golden_full.py
+(which calls only oracle/ and tn_inputs/; commands and oracle timings in the
+.json beside each .npz).
+
+Definition checked: the truncated fixed-projector HVP (SURVEY.md §8(c.2),
+readings X7-X9).  Launch configuration: bench.py's --
+the config's full direction batch in SUB_BATCH sub-batches through the fused
+tn_hvp_step; the stored directions are the first of that batch.  Bar
+(north_star): relative error <= 1e-10 for f, grad_R and every stored
+direction's Hess_R, whole-output and per gate (tests/helpers.gatewise).
+
+"c5r" is config 5 at full width and bond cap (n = 128, chi = 256, C5's
+reference MPO, X17 trust-region start) at depth 4: the full-depth C5 oracle
+does not fit the oracle machine's memory.  It reaches the noise-floor /
+deflation split paths of the trust-region regime; the full-depth C5 engine is
+covered by the identities of test_gpu_parity.py::test_full_size_properties_config5.
+
+The reference MPO is rebuilt with the CPU path of tn_inputs.reference (the
+same input the oracle used); its bonds and per-site sums are checked against
+the stored fingerprint first.
+"""
+import json
+import os
+import time
+
+import numpy as np
+import pytest
+import torch
+
+from tests.helpers import gatewise, rel
+from tn_inputs import configs as C
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+TOL = 1e-10
+
+
+def _load(case):
+    path = os.path.join(GOLDEN, f"full_{case}.npz")
+    if not os.path.exists(path):
+        pytest.fail(f"missing stored oracle outputs {path}: run tools/golden_full.py --case {case}")
+    with open(path.replace(".npz", ".json")) as f:
+        return np.load(path), json.load(f)
+
+
+@pytest.mark.parametrize("case", list(C.FULL_PARITY_CASES))
+def test_full_size_parity(case):
+    from paper_2604_20384_b200.api import SUB_BATCH, HVPEngine, riemannian_project
+    o, meta = _load(case)
+    nd = int(meta["dirs"])
+    cfg, G, V0 = C.full_parity_inputs(case, nd)
+    t0 = time.time()
+    ref_cpu = C.reference_mpo(cfg, device="cpu")
+    t_ref = time.time() - t0
+    bonds, norms = C.ref_fingerprint([x.numpy() for x in ref_cpu])
+    assert bonds == [int(b) for b in o["ref_bonds"]], "reference MPO rebuilt with different bonds"
+    assert np.abs(norms - o["ref_norms"]).max() <= 1e-12 * np.abs(o["ref_norms"]).max()
+    dev = torch.device("cuda")
+    batch = max(cfg.batch, nd)
+    V = C.tangent_directions(cfg.cid, G, batch)
+    assert np.array_equal(V[:nd], V0)
+    mb = SUB_BATCH[cfg.cid] if case != "c5r" else 1
+    eng = HVPEngine(cfg.n, cfg.depth, cfg.chi, [x.to(dev) for x in ref_cpu], cfg.first_offset, max_batch=mb)
+    Gt, Vt = torch.tensor(G, device=dev), torch.tensor(V, device=dev)
+    sc, gR, H = eng.step(Gt, Vt)                       # bench.py's step
+    torch.cuda.synchronize()
+    f = sc[0].item()
+    T = complex(sc[1].item(), sc[2].item())
+    gR, Hn = gR.cpu().numpy(), H.cpu().numpy()
+    report = {"case": case, "t_reference_cpu_s": t_ref, "f_rel": abs(f - float(o["f"])) / abs(float(o["f"])),
+              "T_rel": abs(T - complex(o["T"])) / abs(complex(o["T"])), "grad_R_rel": rel(gR, o["grad_R"]),
+              "grad_R_gate": gatewise(gR, o["grad_R"], TOL), "diag": sc[3:8].cpu().tolist()}
+    assert report["f_rel"] <= TOL and report["T_rel"] <= TOL
+    assert report["grad_R_rel"] <= TOL
+    report["hess_R_rel"], report["hess_R_gate"] = [], []
+    for b in range(nd):
+        report["hess_R_rel"].append(rel(Hn[b], o["HR"][b]))
+        report["hess_R_gate"].append(gatewise(Hn[b], o["HR"][b], TOL))
+        assert report["hess_R_rel"][-1] <= TOL, b
+    print(json.dumps(report))
+    # identities at full size on the same engine (any-size properties):
+    # every output in the tangent space, Hess_R real-linear in V
+    assert rel(riemannian_project(Gt, torch.tensor(gR, device=dev)).cpu().numpy(), gR) < 1e-13
+    assert rel(riemannian_project(Gt, H).cpu().numpy(), Hn) < 1e-13
+    comb = torch.stack([Vt[0] + 2.5 * Vt[1 % batch], Vt[1 % batch]]).contiguous()
+    Hc = eng.apply(comb).cpu().numpy()
+    assert rel(Hc[0], Hn[0] + 2.5 * Hn[1 % batch]) < 1e-11
+    eng.close()

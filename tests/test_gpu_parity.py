@@ -3,15 +3,13 @@
 Bar (BASELINE.json north_star): relative error <= 1e-10 in complex128 on the
 same seeded inputs (X18: rel = ||x_gpu - x_ref|| / ||x_ref|| per output; for
 Hess_R the max over directions)."""
-import os
-
 import numpy as np
 import pytest
 import torch
 
 pytestmark = pytest.mark.gpu
 
-from tests.helpers import oracle_outputs, rel, workload  # noqa: E402
+from tests.helpers import gatewise, o2_outputs, oracle_outputs, rel, workload  # noqa: E402
 from tn_inputs import configs as C  # noqa: E402
 
 TOL = 1e-10
@@ -42,27 +40,35 @@ CASES = [
 
 @pytest.mark.parametrize("cfg", CASES, ids=lambda c: c.name)
 def test_parity_small(cfg):
+    """Against O3 (MPO sweeps) AND O2 (the dense plain definition with explicit
+    Schmidt projectors, n <= 8), whole-output and per gate."""
     ref, G, V = workload(cfg, ref_chi=max(cfg.chi, 4))
-    o = oracle_outputs(cfg, ref, G, V)
     g = gpu_outputs(cfg, ref, G, V)
-    assert abs(g["T"] - o["T"]) <= TOL * abs(o["T"])
-    assert abs(g["f"] - o["f"]) <= TOL * abs(o["f"])
-    assert rel(g["E"], o["E"]) < TOL
-    assert rel(g["grad_R"], o["grad_R"]) < TOL
-    for b in range(V.shape[0]):
-        assert rel(g["HT"][b], o["HT"][b]) < TOL, b
-        assert rel(g["HR"][b], o["HR"][b]) < TOL, b
-        assert abs(g["OM"][b] - o["OM"][b]) <= TOL * abs(o["OM"][b])
+    for o in (oracle_outputs(cfg, ref, G, V), o2_outputs(cfg, ref, G, V)):
+        assert abs(g["T"] - o["T"]) <= TOL * abs(o["T"])
+        assert abs(g["f"] - o["f"]) <= TOL * abs(o["f"])
+        assert rel(g["E"], o["E"]) < TOL
+        gatewise(g["E"], o["E"], TOL)
+        assert rel(g["grad_R"], o["grad_R"]) < TOL
+        gatewise(g["grad_R"], o["grad_R"], TOL)
+        for b in range(V.shape[0]):
+            assert rel(g["HT"][b], o["HT"][b]) < TOL, b
+            assert rel(g["HR"][b], o["HR"][b]) < TOL, b
+            gatewise(g["HR"][b], o["HR"][b], TOL)
+            assert abs(g["OM"][b] - o["OM"][b]) <= TOL * abs(o["OM"][b])
 
 
 def test_parity_config1():
+    """C1 (n = 6, exact MPO) against O3 and O2."""
     cfg = C.CONFIGS[1]
     ref, G, V = workload(cfg)
-    o = oracle_outputs(cfg, ref, G, V)
     g = gpu_outputs(cfg, ref, G, V)
-    assert abs(g["f"] - o["f"]) <= TOL * abs(o["f"])
-    assert rel(g["grad_R"], o["grad_R"]) < TOL
-    assert rel(g["HR"][0], o["HR"][0]) < TOL
+    for o in (oracle_outputs(cfg, ref, G, V), o2_outputs(cfg, ref, G, V)):
+        assert abs(g["f"] - o["f"]) <= TOL * abs(o["f"])
+        assert rel(g["grad_R"], o["grad_R"]) < TOL
+        gatewise(g["grad_R"], o["grad_R"], TOL)
+        assert rel(g["HR"][0], o["HR"][0]) < TOL
+        gatewise(g["HR"][0], o["HR"][0], TOL)
 
 
 def test_parity_config2():
@@ -72,8 +78,10 @@ def test_parity_config2():
     g = gpu_outputs(cfg, ref, G, V, max_batch=6)   # ragged sub-batches
     assert abs(g["f"] - o["f"]) <= TOL * abs(o["f"])
     assert rel(g["grad_R"], o["grad_R"]) < TOL
+    gatewise(g["grad_R"], o["grad_R"], TOL)
     for b in (0, 7, 15):
         assert rel(g["HR"][b], o["HR"][b]) < TOL, b
+        gatewise(g["HR"][b], o["HR"][b], TOL)
 
 
 def test_apply_is_linear_and_batch_independent():
@@ -92,7 +100,7 @@ def _layer_sites(cfg):
     return layers(cfg.n, cfg.depth, cfg.first_offset)
 
 
-@pytest.mark.parametrize("cid", [3, 4])
+@pytest.mark.parametrize("cid", [3])
 def test_full_size_properties(cid):
     """Properties that hold at any size, at the full config and in the launch
     configuration bench.py times (cfg.batch directions in SUB_BATCH sub-batches):
@@ -153,21 +161,6 @@ def test_full_size_properties_config5():
     eng.close()
 
 
-@pytest.mark.skipif(os.environ.get("TN_FULL_PARITY") != "1", reason="~8 min of oracle CPU time; TN_FULL_PARITY=1")
-def test_parity_config3_sampled():
-    cfg = C.CONFIGS[3]
-    dev = torch.device("cuda")
-    ref = C.reference_mpo(cfg, device=dev)
-    K = C.num_gates(cfg.n, cfg.depth)
-    G = C.haar_gates(cfg.cid, K)
-    V = C.tangent_directions(cfg.cid, G, 1)
-    o = oracle_outputs(cfg, ref, G, V)
-    g = gpu_outputs(cfg, ref, G, V, max_batch=1)
-    assert abs(g["f"] - o["f"]) <= TOL * abs(o["f"])
-    assert rel(g["grad_R"], o["grad_R"]) < TOL
-    assert rel(g["HR"][0], o["HR"][0]) < TOL
-
-
 @pytest.mark.parametrize("cid,max_batch", [(2, 8), (3, 64)])
 def test_fused_step_equals_environments_plus_apply(cid, max_batch):
     """tn_hvp_step (first sub-batch's forward tangents replayed during the
@@ -188,30 +181,4 @@ def test_fused_step_equals_environments_plus_apply(cid, max_batch):
     assert torch.equal(sc1[:6], sc2[:6]) and torch.equal(gR1, gR2) and torch.equal(H1, H2)
     H3 = eng.apply(V)                                  # state after the fused step is the same
     assert torch.equal(H3, H1)
-    eng.close()
-
-
-@pytest.mark.skipif(os.environ.get("TN_FULL_PARITY") != "1", reason="~2 min CPU reference build; TN_FULL_PARITY=1")
-def test_parity_config4_stored_oracle():
-    """C4 at full size in bench.py's launch configuration (64 directions,
-    SUB_BATCH sub-batches, fused tn_hvp_step) against oracle outputs stored by
-    tools/oracle_full.py (oracle/ only; 28 min of numpy on 16 cores): f and
-    grad_R, on the reference MPO rebuilt by the same CPU path."""
-    import os as _os
-    from paper_2604_20384_b200.api import SUB_BATCH, HVPEngine
-    root = _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__)))
-    o = np.load(_os.path.join(root, "profiles", "r01_oracle_c4.npz"))
-    cfg = C.CONFIGS[4]
-    ref_cpu = C.reference_mpo(cfg, device="cpu")
-    ref_sum = np.array([float(x.abs().sum()) for x in ref_cpu])
-    assert np.abs(ref_sum - o["ref_sum"]).max() <= 1e-12 * np.abs(o["ref_sum"]).max()
-    dev = torch.device("cuda")
-    K = C.num_gates(cfg.n, cfg.depth)
-    G = C.haar_gates(cfg.cid, K)
-    V = C.tangent_directions(cfg.cid, G, cfg.batch)
-    eng = HVPEngine(cfg.n, cfg.depth, cfg.chi, [x.to(dev) for x in ref_cpu], max_batch=SUB_BATCH[4])
-    sc, gR, H = eng.step(torch.tensor(G, device=dev), torch.tensor(V, device=dev))
-    assert abs(sc[0].item() - float(o["f"])) <= TOL * abs(float(o["f"]))
-    assert rel(gR.cpu().numpy(), o["grad_R"]) < TOL
-    assert torch.isfinite(H).all()
     eng.close()

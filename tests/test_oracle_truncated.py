@@ -122,3 +122,35 @@ def test_insensitive_to_noise_floor_directions():
     assert min(sig) < 1e-13                      # the cut really is in the noise floor
     assert abs(outs[0][0] - outs[1][0]) < 1e-12 * abs(outs[0][0])
     assert rel(outs[1][2], outs[0][2]) < 1e-12
+
+
+def test_tangent_projector_is_the_orthogonal_tangent_projection():
+    """O2's frozen-projector map P_T = P^L(x)I + I(x)P^R - P^L(x)P^R (SURVEY.md
+    §8(c.5)(iii)): idempotent, self-adjoint in the
+    Frobenius inner product, identity on tangent vectors Ur A + B Vr, and its
+    complement is (1 - P^L) D (1 - P^R).  A sign error on the -P^L(x)P^R term
+    (or a dropped term) breaks idempotence and the complement identity."""
+    rng = np.random.default_rng(7)
+
+    def cn(*s):
+        return rng.standard_normal(s) + 1j * rng.standard_normal(s)
+
+    for (m, n_, r) in ((12, 10, 3), (16, 16, 5), (8, 20, 8)):
+        Ur = np.linalg.qr(cn(m, r))[0]
+        Vr = np.linalg.qr(cn(n_, r))[0].conj().T          # rows orthonormal (r x n)
+        D, E = cn(m, n_), cn(m, n_)
+        P = O.tangent_project(D, Ur, Vr)
+        assert np.abs(O.tangent_project(P, Ur, Vr) - P).max() < 1e-13
+        assert abs(np.vdot(E, P) - np.vdot(O.tangent_project(E, Ur, Vr), D)) < 1e-12 * np.abs(D).sum()
+        Y = Ur @ cn(r, n_) + cn(m, r) @ Vr
+        assert np.abs(O.tangent_project(Y, Ur, Vr) - Y).max() < 1e-12
+        PL, PR = Ur @ Ur.conj().T, Vr.conj().T @ Vr
+        comp = (np.eye(m) - PL) @ D @ (np.eye(n_) - PR)
+        assert np.abs(D - P - comp).max() < 1e-12
+        # rank of the projection <= 2 r (the 2-chi tangent bound, PAPER.md:1013-1017)
+        assert np.linalg.matrix_rank(P, tol=1e-10) <= 2 * r
+    # the wrong-sign variant fails idempotence (the pin is sensitive to it)
+    def wrong(X):
+        PLX = Ur @ (Ur.conj().T @ X)
+        return PLX + (X @ Vr.conj().T) @ Vr + (PLX @ Vr.conj().T) @ Vr
+    assert np.abs(wrong(wrong(D)) - wrong(D)).max() > 1e-3

@@ -57,3 +57,80 @@ def test_gather_rows_world2_gloo(total):
     for i in range(total):
         assert (full[i] == complex(i, 2 * i)).all()
     assert (realv[:, 0] == range(total)).all()
+
+
+class _StandInEngine:
+    """Host-side stand-in of api.HVPEngine for the CPU choreography test: the
+    'primal store' is a function of the gates, apply needs a valid store."""
+
+    def __init__(self):
+        self.store = torch.zeros(8, dtype=torch.float64)
+        self.scalars = torch.zeros(8, dtype=torch.float64)
+        self.valid = False
+        self.calls = []
+
+    @staticmethod
+    def _primal(gates):
+        return gates.real.reshape(-1)[:8].clone() + 1.0
+
+    def environments(self, gates):
+        self.calls.append("environments")
+        self.store.copy_(self._primal(gates))
+        self.scalars.copy_(2 * self.store)
+        self.valid = True
+
+    def primal_store(self):
+        return self.store
+
+    def invalidate_primal(self):
+        self.calls.append("invalidate")
+        self.valid = False
+
+    def primal_imported(self, gates):
+        self.calls.append("imported")
+        assert torch.equal(self.store, self._primal(gates)), "store does not match the point"
+        self.valid = True
+
+    def apply(self, dirs):
+        assert self.valid
+        self.calls.append(f"apply{dirs.shape[0]}")
+        return dirs * complex(float(self.store.sum()), 0.5)
+
+
+def _step_worker(rank, world, port, B, q):
+    from paper_2604_20384_b200.parallel import sharded_step
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = torch.Generator().manual_seed(3)
+    gates = torch.randn(5, 4, 4, dtype=torch.complex128, generator=g)
+    dirs = torch.randn(B, 5, 4, 4, dtype=torch.complex128, generator=g)
+    eng = _StandInEngine()
+    sc, full = sharded_step(eng, gates, dirs)
+    want = dirs * complex(float(_StandInEngine._primal(gates).sum()), 0.5)
+    q.put((rank, bool(torch.equal(full, want)), bool(torch.equal(sc, 2 * _StandInEngine._primal(gates))),
+           eng.calls))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("B", [5, 1])
+def test_sharded_step_world2_gloo(B):
+    """primal once on rank 0 -> in-place broadcast of the store -> import
+    check on rank 1 -> B/2 directions per rank -> all_gather in order."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_step_worker, args=(r, 2, port, B, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(2)])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (r0, ok0, sc0, calls0), (r1, ok1, sc1, calls1) = res
+    assert ok0 and ok1 and sc0 and sc1
+    assert calls0[0] == "environments" and "imported" not in calls0
+    assert calls1[:2] == ["invalidate", "imported"] and "environments" not in calls1
+    n0 = (B + 1) // 2
+    assert calls0[-1] == f"apply{n0}"
+    assert (calls1[-1] == f"apply{B - n0}") if B - n0 else calls1[-1] == "imported"

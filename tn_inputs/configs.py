@@ -102,3 +102,42 @@ def trotter_init_gates(cfg: Config, problem: int, steps: int | None = None, eps:
         hs = 0.5 * (a + a.conj().T)
         out[k] = expm_herm(bond_term(cfg.model, cfg.n, s), dt) @ expm_herm(hs, eps)
     return out
+
+
+# Full-size parity cases with stored oracle outputs (tests/golden/full_*.npz,
+# written by tools/golden_full.py).  "c5r" is config 5 at full width and
+# bond cap (n = 128, chi = 256, C5's reference MPO) with a reduced depth D = 4
+# and the X17 Trotter start of problem 0 (the trust-region regime whose cuts
+# fall in the noise floor); the full-depth C5 oracle does not fit this
+# container's memory.
+FULL_PARITY_CASES = ("c3", "c4", "c5r")
+
+
+def full_parity_config(case: str) -> Config:
+    if case == "c3":
+        return CONFIGS[3]
+    if case == "c4":
+        return CONFIGS[4]
+    if case == "c5r":
+        c5 = CONFIGS[5]
+        return Config(5, "C5r-tfim-n128-D4", c5.n, 4, c5.chi, c5.model, c5.t, c5.steps, c5.order, 1)
+    raise ValueError(case)
+
+
+def full_parity_inputs(case: str, dirs: int):
+    """(config, gates, first `dirs` directions) of a full-size parity case."""
+    cfg = full_parity_config(case)
+    K = num_gates(cfg.n, cfg.depth, cfg.first_offset)
+    if case == "c5r":
+        G = trotter_init_gates(cfg, 0)
+    else:
+        G = haar_gates(cfg.cid, K)
+    return cfg, G, tangent_directions(cfg.cid, G, dirs)
+
+
+def ref_fingerprint(sites):
+    """(bonds, per-site sum |x|) of a reference MPO: identifies the rebuilt input."""
+    import numpy as _np
+    bonds = [1] + [int(x.shape[2]) for x in sites]
+    norms = _np.array([float(_np.abs(_np.asarray(x)).sum()) for x in sites])
+    return bonds, norms
