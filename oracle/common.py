@@ -48,6 +48,16 @@ def apply_out_gate(x: np.ndarray, g: np.ndarray) -> np.ndarray:
     return np.einsum("abcd,xcidjy->xaibjy", gg, t).reshape(bl, 4, 4, br)
 
 
+def apply_pair_gate(x: np.ndarray, g: np.ndarray) -> np.ndarray:
+    """The gate on the OUT legs of a two-site block x[bl, p, p, br]: operator
+    sites p = 4 (p = 2 out + in, apply_out_gate) or state sites p = 2 (p = out;
+    the N1 MPS setting of PAPER.md:325-336)."""
+    if x.shape[1] == 4:
+        return apply_out_gate(x, g)
+    bl, _, _, br = x.shape
+    return np.einsum("ab,xby->xay", g, x.reshape(bl, 4, br)).reshape(bl, 2, 2, br)
+
+
 # ------------------------------------------------------ Alg. 2 postprocess --
 def postprocess_gradient(T: complex, E: np.ndarray):
     """f and the Euclidean gradient from (T, grad T = E).

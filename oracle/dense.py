@@ -24,16 +24,17 @@ def _svd(a):
     except np.linalg.LinAlgError:
         return _sla.svd(a, full_matrices=False, lapack_driver="gesvd")
 
-from .common import apply_out_gate, bottom_order_lr, layers, top_order_lr
+from .common import apply_pair_gate, bottom_order_lr, layers, top_order_lr
 
 # ====================================================================== O1 ==
 
 
 def apply_op(X: np.ndarray, n: int, s: int, G: np.ndarray) -> np.ndarray:
-    """(G on qubits s, s+1) @ X for a 2^n x 2^n operator X."""
-    d = 2 ** n
-    t = X.reshape(2 ** s, 4, 2 ** (n - s - 2), d)
-    return np.einsum("ab,xbyz->xayz", G, t).reshape(d, d)
+    """(G on qubits s, s+1) @ X for a 2^n x m matrix X (m = 2^n: an operator;
+    m = 1: a state vector, the N1 setting)."""
+    d, m = 2 ** n, X.shape[1]
+    t = X.reshape(2 ** s, 4, 2 ** (n - s - 2), m)
+    return np.einsum("ab,xbyz->xayz", G, t).reshape(d, m)
 
 
 def env_op(phi: np.ndarray, psi: np.ndarray, n: int, s: int) -> np.ndarray:
@@ -44,9 +45,9 @@ def env_op(phi: np.ndarray, psi: np.ndarray, n: int, s: int) -> np.ndarray:
     Reading X4: row = gate output index a, column = gate input index b, so that
     T = sum_ab G_ab E_ab (Euler identity).
     """
-    d = 2 ** n
-    f = phi.reshape(2 ** s, 4, 2 ** (n - s - 2), d)
-    p = psi.reshape(2 ** s, 4, 2 ** (n - s - 2), d)
+    m = psi.shape[1]
+    f = phi.reshape(2 ** s, 4, 2 ** (n - s - 2), m)
+    p = psi.reshape(2 ** s, 4, 2 ** (n - s - 2), m)
     return np.einsum("xayz,xbyz->ab", np.conj(f), p)
 
 
@@ -54,7 +55,7 @@ def overlap(phi: np.ndarray, psi: np.ndarray) -> complex:
     return complex(np.vdot(phi.ravel(), psi.ravel()))
 
 
-def alg1(n, sites, G, Uref, V=None):
+def alg1(n, sites, G, Uref, V=None, psi0=None, phi0=None):
     """Algorithm 1 HVP_Kernel, forward pass first.
 
     Forward pass (lines 278-281) caches psi^(k) and Dpsi^(k) (eq:fis, eq:dfis);
@@ -65,16 +66,20 @@ def alg1(n, sites, G, Uref, V=None):
     (line 289 is written with Dphi^(K-k)); line 287's update is applied after.
     T = <phi^(K)|psi^(0)> at the boundary (line 292).
     Returns (T, E[K,4,4], H[K,4,4] or None).
+    State mode (N1): psi0 = |psi> and phi0 = U_ref |psi> as
+    2^n x 1 columns (then Uref is unused), T = <phi| W |psi>.
     """
     K = len(sites)
     d = 2 ** n
-    psi = [np.eye(d, dtype=np.complex128) / 2 ** (n / 2)]
-    dpsi = [np.zeros((d, d), dtype=np.complex128)]
+    if psi0 is None:
+        psi0, phi0 = np.eye(d, dtype=np.complex128) / 2 ** (n / 2), Uref / 2 ** (n / 2)
+    psi = [np.asarray(psi0, dtype=np.complex128)]
+    dpsi = [np.zeros_like(psi[0])]
     for k in range(K):                                   # forward pass
         if V is not None:
             dpsi.append(apply_op(dpsi[k], n, sites[k], G[k]) + apply_op(psi[k], n, sites[k], V[k]))
         psi.append(apply_op(psi[k], n, sites[k], G[k]))
-    phi = Uref / 2 ** (n / 2)
+    phi = np.asarray(phi0, dtype=np.complex128)
     dphi = np.zeros_like(phi)
     E = np.zeros((K, 4, 4), dtype=np.complex128)
     H = np.zeros((K, 4, 4), dtype=np.complex128) if V is not None else None
@@ -157,12 +162,21 @@ def op_to_vec(X: np.ndarray, n: int) -> np.ndarray:
 
 
 def vec_apply(x: np.ndarray, n: int, s: int, M: np.ndarray) -> np.ndarray:
-    t = x.reshape(4 ** s, 4, 4, 4 ** (n - s - 2))
-    return apply_out_gate(t, M).reshape((4,) * n)
+    """Gate on the out legs of sites (s, s+1) of a p^n vector: p = 4 operator
+    (p = 2 out + in), p = 2 state (N1)."""
+    p = x.shape[0]
+    t = x.reshape(p ** s, p, p, p ** (n - s - 2))
+    return apply_pair_gate(t, M).reshape((p,) * n)
 
 
 def vec_env(top: np.ndarray, bot: np.ndarray, n: int, s: int) -> np.ndarray:
-    """E[(o1 o2), (o1' o2')] = sum conj(top[.., o1 i1, o2 i2, ..]) bot[.., o1' i1, o2' i2, ..]."""
+    """E[(o1 o2), (o1' o2')] = sum conj(top[.., o1 i1, o2 i2, ..]) bot[.., o1' i1, o2' i2, ..]
+    (state vectors: no in legs)."""
+    p = top.shape[0]
+    if p == 2:
+        t = top.reshape(2 ** s, 4, 2 ** (n - s - 2))
+        b = bot.reshape(2 ** s, 4, 2 ** (n - s - 2))
+        return np.einsum("xay,xby->ab", np.conj(t), b)
     t = top.reshape(4 ** s, 2, 2, 2, 2, 4 ** (n - s - 2))
     b = bot.reshape(4 ** s, 2, 2, 2, 2, 4 ** (n - s - 2))
     return np.einsum("xaibjy,xcidjy->abcd", np.conj(t), b).reshape(4, 4)
@@ -194,15 +208,25 @@ class DenseTruncated:
     taken layer-wise with the layer's own gates exact (X9); T = <<T_0|B_0>>.
     """
 
-    def __init__(self, n, depth, chi, G, Uref_vec, ref_bonds, V=None, first_offset=0):
+    def __init__(self, n, depth, chi, G, Uref_vec, ref_bonds, V=None, first_offset=0, psi=None):
+        """Operator mode: Uref_vec = U_ref/2^{n/2} as a 4^n vector.  State mode
+        (N1): psi [n][2] the product state and Uref_vec the label phi = U_ref psi
+        as a 2^n vector (bottom start psi, T = <phi|W|psi>)."""
         self.n, self.D, self.chi = n, depth, chi
         self.G = np.asarray(G)
         self.V = None if V is None else np.asarray(V)
         self.layers = layers(n, depth, first_offset)
         self.diag = []
         nb = 0 if V is None else self.V.shape[0]
-        # bottom sweep: B_0 = I/2^{n/2}
-        x = op_to_vec(np.eye(2 ** n, dtype=np.complex128) / 2 ** (n / 2), n)
+        # bottom sweep: B_0 = I/2^{n/2} (operator) or the product state psi (state)
+        if psi is None:
+            x = op_to_vec(np.eye(2 ** n, dtype=np.complex128) / 2 ** (n / 2), n)
+        else:
+            x = np.asarray(psi[0], dtype=np.complex128)
+            for s in range(1, n):
+                x = np.kron(x, psi[s])
+            x = x.reshape((2,) * n)
+        self.p = x.shape[0]
         dx = [np.zeros_like(x) for _ in range(nb)]
         bonds = [1] * (n + 1)
         self.B, self.DB = [], []
@@ -231,12 +255,13 @@ class DenseTruncated:
         self.T = complex(np.vdot(self.Ttop[0].ravel(), self.B[0].ravel()))
 
     def _step(self, x, dx, s, M, VM, bonds):
-        n, c = self.n, s + 1
+        n, c, p = self.n, s + 1, self.p
         xp = vec_apply(x, n, s, M)
         dxp = [vec_apply(d, n, s, M) + vec_apply(x, n, s, vm) for d, vm in zip(dx, VM)]
-        mat = xp.reshape(4 ** c, -1)
+        mat = xp.reshape(p ** c, -1)
         U, S, Vh = _svd(mat)
-        r = min(self.chi, 4 * bonds[c], 4 * bonds[c - 1], 4 * bonds[c + 1], len(S))
+        # X7: r = min(chi, 4 m_c, p b_{c-1}, p b_{c+1}) (gate operator-Schmidt rank <= 4)
+        r = min(self.chi, 4 * bonds[c], p * bonds[c - 1], p * bonds[c + 1], len(S))
         Ur, Vr = U[:, :r], Vh[:r]
         y = Ur @ (Ur.conj().T @ mat)
         sc = np.linalg.norm(mat) / np.linalg.norm(y)

@@ -38,7 +38,7 @@ def _svd(a):
     except np.linalg.LinAlgError:
         return _sla.svd(a, full_matrices=False, lapack_driver="gesvd")
 
-from .common import apply_out_gate, bottom_order_lr, layers, top_order_lr
+from .common import apply_pair_gate, bottom_order_lr, layers, top_order_lr
 
 
 def _c(a):
@@ -51,6 +51,7 @@ class MPOSweep:
 
     def __init__(self, sites, chi, nb):
         self.n = len(sites)
+        self.p = int(np.asarray(sites[0]).shape[1])   # 4: operator sites, 2: state sites (N1)
         self.chi = chi
         self.P = [np.array(a, dtype=np.complex128) for a in sites]
         self.c = 0
@@ -65,20 +66,20 @@ class MPOSweep:
         c = self.c
         P = self.P
         b, _, bp = P[c].shape
-        Q, R = np.linalg.qr(P[c].reshape(b * 4, bp))
+        Q, R = np.linalg.qr(P[c].reshape(b * self.p, bp))
         k = Q.shape[1]
-        P[c] = Q.reshape(b, 4, k)
+        P[c] = Q.reshape(b, self.p, k)
         P[c + 1] = np.einsum("ab,bpc->apc", R, P[c + 1])
         # before-chain reduction Ab_c = Q X (remainder zero in exact arithmetic)
-        Abc = self.Ab[c].reshape(b * 4, -1)
+        Abc = self.Ab[c].reshape(b * self.p, -1)
         X = Q.conj().T @ Abc
         self.remainder = max(self.remainder, float(np.linalg.norm(Abc - Q @ X)))
-        self.Ab[c] = Q.reshape(b, 4, k)
+        self.Ab[c] = Q.reshape(b, self.p, k)
         self.Ab[c + 1] = np.einsum("ab,bpc->apc", X, self.Ab[c + 1])
         for Bd in self.Bd:
-            Bc = Bd[c].reshape(b * 4, -1)
+            Bc = Bd[c].reshape(b * self.p, -1)
             Y = Q.conj().T @ Bc
-            Bd[c] = (Bc - Q @ Y).reshape(b, 4, -1)
+            Bd[c] = (Bc - Q @ Y).reshape(b, self.p, -1)
             Bd[c + 1] = (np.einsum("ab,bpc->apc", X, Bd[c + 1])
                          + np.einsum("ab,bpc->apc", Y, self.Aa[c + 1]))
         self.c = c + 1
@@ -87,20 +88,20 @@ class MPOSweep:
         c = self.c
         P = self.P
         b, _, bp = P[c].shape
-        Qh, Rh = np.linalg.qr(P[c].reshape(b, 4 * bp).conj().T)
+        Qh, Rh = np.linalg.qr(P[c].reshape(b, self.p * bp).conj().T)
         Q, L = Qh.conj().T, Rh.conj().T          # P_c = L Q, Q row-orthonormal
         k = Q.shape[0]
-        P[c] = Q.reshape(k, 4, bp)
+        P[c] = Q.reshape(k, self.p, bp)
         P[c - 1] = np.einsum("apb,bc->apc", P[c - 1], L)
-        Aac = self.Aa[c].reshape(-1, 4 * bp)
+        Aac = self.Aa[c].reshape(-1, self.p * bp)
         X = Aac @ Q.conj().T
         self.remainder = max(self.remainder, float(np.linalg.norm(Aac - X @ Q)))
-        self.Aa[c] = Q.reshape(k, 4, bp)
+        self.Aa[c] = Q.reshape(k, self.p, bp)
         self.Aa[c - 1] = np.einsum("apb,bc->apc", self.Aa[c - 1], X)
         for Bd in self.Bd:
-            Bc = Bd[c].reshape(-1, 4 * bp)
+            Bc = Bd[c].reshape(-1, self.p * bp)
             Y = Bc @ Q.conj().T
-            Bd[c] = (Bc - Y @ Q).reshape(-1, 4, bp)
+            Bd[c] = (Bc - Y @ Q).reshape(-1, self.p, bp)
             Bd[c - 1] = (np.einsum("apb,bc->apc", Bd[c - 1], X)
                          + np.einsum("apb,bc->apc", self.Ab[c - 1], Y))
         self.c = c - 1
@@ -117,9 +118,10 @@ class MPOSweep:
         self.move_to(i if lr else i + 1)
         bl, m, br = P[i].shape[0], P[i].shape[2], P[i + 1].shape[2]
         theta = np.einsum("apb,bqc->apqc", P[i], P[i + 1])
-        thp = apply_out_gate(theta, M).reshape(bl * 4, 4 * br)
+        p = self.p
+        thp = apply_pair_gate(theta, M).reshape(bl * p, p * br)
         U, S, Vh = _svd(thp)
-        r = min(self.chi, 4 * m, 4 * bl, 4 * br, len(S))
+        r = min(self.chi, 4 * m, p * bl, p * br, len(S))   # gate operator-Schmidt rank <= 4
         Ur, Sr, Vr = U[:, :r], S[:r], Vh[:r]
         W = Vr.conj().T
         s = float(np.linalg.norm(S) / np.linalg.norm(Sr))
@@ -129,32 +131,32 @@ class MPOSweep:
         for Bd, vm in zip(self.Bd, VM):
             d1 = np.einsum("apb,bqc->apqc", Bd[i], self.Aa[i + 1])
             d2 = np.einsum("apb,bqc->apqc", self.Ab[i], Bd[i + 1])
-            dth = (apply_out_gate(d1 + d2, M) + apply_out_gate(theta, vm)).reshape(bl * 4, 4 * br)
+            dth = (apply_pair_gate(d1 + d2, M) + apply_pair_gate(theta, vm)).reshape(bl * p, p * br)
             if lr:
                 UD = Ur.conj().T @ dth
-                Bd[i] = (s * ((dth - Ur @ UD) @ W)).reshape(bl, 4, r)
-                Bd[i + 1] = (s * UD).reshape(r, 4, br)
+                Bd[i] = (s * ((dth - Ur @ UD) @ W)).reshape(bl, p, r)
+                Bd[i + 1] = (s * UD).reshape(r, p, br)
             else:
                 DW = dth @ W
-                Bd[i] = (s * DW).reshape(bl, 4, r)
-                Bd[i + 1] = (s * (Ur.conj().T @ (dth - DW @ W.conj().T))).reshape(r, 4, br)
+                Bd[i] = (s * DW).reshape(bl, p, r)
+                Bd[i + 1] = (s * (Ur.conj().T @ (dth - DW @ W.conj().T))).reshape(r, p, br)
         # direction-independent chain pass-throughs
         ba_i = self.Aa[i].shape[0]
-        aa = apply_out_gate(np.einsum("apb,bqc->apqc", self.Aa[i], self.Aa[i + 1]), M)
-        self.Aa[i] = (s * (aa.reshape(ba_i * 4, 4 * br) @ W)).reshape(ba_i, 4, r)
-        self.Aa[i + 1] = Vr.reshape(r, 4, br)
+        aa = apply_pair_gate(np.einsum("apb,bqc->apqc", self.Aa[i], self.Aa[i + 1]), M)
+        self.Aa[i] = (s * (aa.reshape(ba_i * p, p * br) @ W)).reshape(ba_i, p, r)
+        self.Aa[i + 1] = Vr.reshape(r, p, br)
         bb_n = self.Ab[i + 1].shape[2]
-        ab = apply_out_gate(np.einsum("apb,bqc->apqc", self.Ab[i], self.Ab[i + 1]), M)
-        self.Ab[i + 1] = (s * (Ur.conj().T @ ab.reshape(bl * 4, 4 * bb_n))).reshape(r, 4, bb_n)
-        self.Ab[i] = Ur.reshape(bl, 4, r)
+        ab = apply_pair_gate(np.einsum("apb,bqc->apqc", self.Ab[i], self.Ab[i + 1]), M)
+        self.Ab[i + 1] = (s * (Ur.conj().T @ ab.reshape(bl * p, p * bb_n))).reshape(r, p, bb_n)
+        self.Ab[i] = Ur.reshape(bl, p, r)
         # primal
         if lr:
-            P[i] = Ur.reshape(bl, 4, r)
-            P[i + 1] = (s * (Sr[:, None] * Vr)).reshape(r, 4, br)
+            P[i] = Ur.reshape(bl, p, r)
+            P[i + 1] = (s * (Sr[:, None] * Vr)).reshape(r, p, br)
             self.c = i + 1
         else:
-            P[i] = (s * (Ur * Sr[None, :])).reshape(bl, 4, r)
-            P[i + 1] = Vr.reshape(r, 4, br)
+            P[i] = (s * (Ur * Sr[None, :])).reshape(bl, p, r)
+            P[i + 1] = Vr.reshape(r, p, br)
             self.c = i
 
     def snapshot(self):
@@ -171,7 +173,7 @@ def augmented(Ab, Aa, B):
     for s in range(n):
         bb, _, bbn = Ab[s].shape
         ba, _, ban = Aa[s].shape
-        M = np.zeros((bb + ba, 4, bbn + ban), dtype=np.complex128)
+        M = np.zeros((bb + ba, Ab[s].shape[1], bbn + ban), dtype=np.complex128)
         M[:bb, :, :bbn] = Ab[s]
         M[:bb, :, bbn:] = B[s]
         M[bb:, :, bbn:] = Aa[s]
@@ -202,7 +204,7 @@ def _upd_left(L, top, bot, blk, G):
     if k is None:
         return np.einsum("tb,tpu,bpv->uv", L, _c(top[s]), bot[s], optimize=True)
     tt = np.einsum("apb,bqc->apqc", top[s], top[s + 1])
-    bb = apply_out_gate(np.einsum("apb,bqc->apqc", bot[s], bot[s + 1]), G)
+    bb = apply_pair_gate(np.einsum("apb,bqc->apqc", bot[s], bot[s + 1]), G)
     return np.einsum("tb,tpqu,bpqv->uv", L, _c(tt), bb, optimize=True)
 
 
@@ -211,7 +213,7 @@ def _upd_right(R, top, bot, blk, G):
     if k is None:
         return np.einsum("uv,tpu,bpv->tb", R, _c(top[s]), bot[s], optimize=True)
     tt = np.einsum("apb,bqc->apqc", top[s], top[s + 1])
-    bb = apply_out_gate(np.einsum("apb,bqc->apqc", bot[s], bot[s + 1]), G)
+    bb = apply_pair_gate(np.einsum("apb,bqc->apqc", bot[s], bot[s + 1]), G)
     return np.einsum("uv,tpqu,bpqv->tb", R, _c(tt), bb, optimize=True)
 
 
@@ -220,6 +222,8 @@ def _extract(L, R, top, bot, blk):
     s = blk[0]
     tt = np.einsum("apb,bqc->apqc", top[s], top[s + 1])
     bb = np.einsum("apb,bqc->apqc", bot[s], bot[s + 1])
+    if tt.shape[1] == 2:        # state sites: p = out
+        return np.einsum("XY,XabU,YcdV,UV->abcd", L, _c(tt), bb, R, optimize=True).reshape(4, 4)
     t6 = tt.reshape(tt.shape[0], 2, 2, 2, 2, tt.shape[3])
     b6 = bb.reshape(bb.shape[0], 2, 2, 2, 2, bb.shape[3])
     return np.einsum("XY,XaibjU,YcidjV,UV->abcd", L, _c(t6), b6, R, optimize=True).reshape(4, 4)
@@ -285,15 +289,24 @@ class MPOOracle:
     future variations via DT, past via DB, plus the in-layer k' != k gates).
     """
 
-    def __init__(self, n, depth, chi, G, ref_sites, V=None, first_offset=0):
+    def __init__(self, n, depth, chi, G, ref_sites, V=None, first_offset=0, psi=None):
+        """Operator mode: ref_sites the MPO of U_ref / 2^{n/2} ([b][4][b']), bottom
+        start I/2^{n/2}.  State mode (N1): ref_sites the label
+        MPS phi = U_ref psi ([b][2][b']) and psi [n][2] the product state, so
+        T = <phi| W |psi>."""
         self.n, self.D, self.chi = n, depth, chi
         self.G = np.asarray(G)
         self.V = None if V is None else np.asarray(V)
         nb = 0 if V is None else self.V.shape[0]
         self.layers = layers(n, depth, first_offset)
-        ident = np.zeros((1, 4, 1), dtype=np.complex128)
-        ident[0, 0, 0] = ident[0, 3, 0] = 1.0 / np.sqrt(2.0)
-        bot = MPOSweep([ident] * n, chi, nb)
+        if np.asarray(ref_sites[0]).shape[1] == 2:
+            psi = np.asarray(psi, dtype=np.complex128)
+            start = [psi[s].reshape(1, 2, 1) for s in range(n)]
+        else:
+            ident = np.zeros((1, 4, 1), dtype=np.complex128)
+            ident[0, 0, 0] = ident[0, 3, 0] = 1.0 / np.sqrt(2.0)
+            start = [ident] * n
+        bot = MPOSweep(start, chi, nb)
         self.Bs = []
         for ell in range(1, depth + 1):
             self.Bs.append(bot.snapshot())

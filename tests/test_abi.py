@@ -31,11 +31,11 @@ def test_num_gates():
 
 
 def test_invalid_arguments_rejected_without_gpu():
-    cfg = N.Config(1, 4, 0, 8, N.TN_C128, 4, 0, 0)         # n < 2
+    cfg = N.make_config(1, 4, 8, max_batch=4)         # n < 2
     with pytest.raises(N.TNError) as e:
         N.tn_hvp_setup(cfg, [1, 1], 1, 0)
     assert e.value.status == N.TN_EINVAL
-    cfg = N.Config(4, 4, 0, 8, N.TN_C128, 4, 0, 0)
+    cfg = N.make_config(4, 4, 8, max_batch=4)
     with pytest.raises(N.TNError) as e:
         N.tn_hvp_setup(cfg, [2, 1, 1, 1, 1], 1, 0)  # boundary bond != 1
     assert e.value.status == N.TN_EINVAL
@@ -68,28 +68,30 @@ def test_query_sizes_without_gpu():
     bonds = [1] + [4] * 7 + [1]
     sizes = []
     for chi in (4, 8, 16):
-        cfg = N.Config(8, 6, 0, chi, N.TN_C128, 2, 0, 0)
+        cfg = N.make_config(8, 6, chi, max_batch=2)
         p, w, d = N.tn_hvp_query(cfg, bonds)
         assert p > 0 and w > 0 and d > 0 and p % 256 == 0
         sizes.append((p, w, d))
     assert sizes[0][0] < sizes[1][0] < sizes[2][0]
     assert sizes[0][2] < sizes[1][2] <= sizes[2][2]
     # C4-sized plan (host only): the primal store is GiB-scale, a direction ~1 GiB
-    c4 = N.Config(50, 16, 0, 256, N.TN_C128, 32, 0, 0)
+    c4 = N.make_config(50, 16, 256, max_batch=32)
     p, w, d = N.tn_hvp_query(c4, [1] + [min(4 ** min(s, 50 - s), 256) for s in range(1, 50)] + [1])
     assert 1 << 30 < p < 64 << 30 and 1 << 28 < d < 8 << 30
 
 
 def test_config_checks_without_gpu():
     bonds = [1, 4, 4, 4, 1]
-    for cfg, why in ((N.Config(4, 4, 0, 8, N.TN_C64, 2, 0, 0), "complex64 not built"),
-                     (N.Config(4, 4, 0, 8, N.TN_C128, 2, 0, 1 << 7), "unknown flag"),
-                     (N.Config(4, 4, 2, 8, N.TN_C128, 2, 0, 0), "offset"),
-                     (N.Config(4, 4, 0, 8, N.TN_C128, 0, 0, 0), "max_batch")):
+    for cfg, why in ((N.make_config(4, 4, 8, 2, dtype=N.TN_C64), "complex64 not built"),
+                     (N.make_config(4, 4, 8, 2, flags=1 << 7), "unknown flag"),
+                     (N.make_config(4, 4, 8, 2, first_offset=2), "offset"),
+                     (N.make_config(4, 4, 8, 0), "max_batch"),
+                     (N.make_config(4, 4, 8, 2, site_dim=3), "site_dim"),
+                     (N.make_config(4, 4, 8, 2, site_dim=2), "state-mode bonds within a factor 2")):
         with pytest.raises(N.TNError) as e:
             N.tn_hvp_query(cfg, bonds)
         assert e.value.status == N.TN_EINVAL, why
-    ok = N.Config(4, 4, 0, 8, N.TN_C128, 2, 0, N.TN_CHECK_UNITARY | N.TN_CHECK_TANGENT)
+    ok = N.make_config(4, 4, 8, 2, flags=N.TN_CHECK_UNITARY | N.TN_CHECK_TANGENT)
     p, _, _ = N.tn_hvp_query(ok, bonds)
     # a caller-owned primal store smaller than the query's size is rejected
     # before any CUDA call (fake, aligned device pointers: nothing is touched)

@@ -136,8 +136,26 @@ def full_parity_inputs(case: str, dirs: int):
 
 
 def ref_fingerprint(sites):
-    """(bonds, per-site sum |x|) of a reference MPO: identifies the rebuilt input."""
+    """(bonds, per-site sum |x|) of a reference MPO (gauge dependent)."""
     import numpy as _np
     bonds = [1] + [int(x.shape[2]) for x in sites]
     norms = _np.array([float(_np.abs(_np.asarray(x)).sum()) for x in sites])
     return bonds, norms
+
+
+def ref_schmidt_spectra(sites):
+    """Operator Schmidt values of a right-canonical MPO at every cut c = 1..n-1
+    (singular values of the bond matrix after moving the centre there by QR):
+    a gauge-invariant fingerprint of the operator, so a reference rebuilt on
+    another machine (different LAPACK rounding, different bond gauge) can be
+    checked to be the same input.  Returns a list of descending arrays."""
+    import numpy as _np
+    a = [_np.asarray(x, dtype=_np.complex128) for x in sites]
+    out = []
+    c = a[0]
+    for j in range(len(a) - 1):
+        b, p, bp = c.shape
+        q, r = _np.linalg.qr(c.reshape(b * p, bp))
+        out.append(_np.linalg.svd(r, compute_uv=False))
+        c = _np.einsum("ab,bpc->apc", r, a[j + 1])
+    return out
