@@ -51,6 +51,10 @@ def parse():
     ap.add_argument("--unfused", action="store_true",
                     help="time tn_hvp_environments + tn_hvp_apply instead of the fused tn_hvp_step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="config", choices=["config", "n1"],
+                    help="config: the BASELINE.json config (default); n1: the sampled-state empirical risk "
+                         "(SURVEY.md 8(f) N1) at the config's width")
+    ap.add_argument("--samples", type=int, default=8, help="N1: product states S")
     return ap.parse_args()
 
 
@@ -245,6 +249,80 @@ class Phase:
         self.ms = self.e0.elapsed_time(self.e1)
 
 
+# ------------------------------------------------------------------ N1 --
+def run_n1(args, cfg, rank, world, local):
+    """N1: risk HVPs/s = directions / step, a step being the
+    risk's primal pass over all S samples (concurrent per-sample streams) and
+    its Riemannian HVPs for B directions; samples sharded over ranks with one
+    all_reduce per call (risk.EmpiricalRisk)."""
+    import torch.distributed as dist
+    from paper_2604_20384_b200 import _native as N
+    from paper_2604_20384_b200.risk import EmpiricalRisk
+    from tn_inputs import samples as SMP
+    dev = torch.device("cuda", torch.cuda.current_device())
+    S, B = args.samples, args.batch or 8
+    K = C.num_gates(cfg.n, cfg.depth, cfg.first_offset)
+    ref = [a.detach().resolve_conj().cpu().numpy() for a in C.reference_mpo(cfg, device=dev)]
+    psis = SMP.haar_product_states(cfg.cid, S, cfg.n)
+    labels = [[torch.tensor(a, device=dev) for a in SMP.label_mps(ref, p)] for p in psis]
+    Gnp = C.haar_gates(cfg.cid, K)
+    G = torch.tensor(Gnp, device=dev)
+    V = torch.tensor(C.tangent_directions(cfg.cid, Gnp, B), device=dev)
+    er = EmpiricalRisk(cfg.n, cfg.depth, cfg.chi, labels, psis, cfg.first_offset, max_batch=B,
+                       group=dist.group.WORLD if world > 1 else None)
+
+    def step():
+        er.environments(G)
+        return er.apply(V)
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    torch.cuda.synchronize()
+    N.tn_gemm_profile(1)
+    er.apply(V)
+    torch.cuda.synchronize()
+    gemm_ms, gemm_cmac = N.tn_gemm_profile(0)
+    barrier(world)
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        l0 = N.tn_hvp_launch_count()
+        e0.record(st)
+        for _ in range(args.steps):
+            step()
+        e1.record(st)
+        torch.cuda.synchronize()
+        launches = N.tn_hvp_launch_count() - l0
+    barrier(world)
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+    with Phase() as p_env:
+        er.environments(G)
+    with Phase() as p_ap:
+        er.apply(V)
+    peak, peak_src = fp64_peak()
+    achieved = 8 * gemm_cmac / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
+    line = {
+        "metric": "risk HVPs/sec of the N1 sampled-state empirical risk (complex128)", "value": B / (ms / 1e3),
+        "unit": "risk HVPs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": f"N1-{cfg.name}-S{S}", "n": cfg.n, "depth": cfg.depth, "chi": cfg.chi,
+                   "samples": S, "directions_per_step": B,
+                   "parallelism": f"samples over {world} rank(s), concurrent per-sample streams, all_reduce",
+                   "l2": "working set > 126 MB L2; no flush"},
+        "sample_hvps_per_s": S * B / (ms / 1e3),
+        "phases": {"primal_all_samples_ms": max_over_ranks(p_env.ms, world),
+                   "apply_all_samples_ms": max_over_ranks(p_ap.ms, world)},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak if achieved else None, "traffic": None,
+                     "kernel": "tn::zgemm3m_kernel over one risk apply (per-launch CUDA events, concurrent streams)",
+                     "peak_source": peak_src},
+        "clocks": clk.summary(), "gpu_launches": int(launches)}
+    if rank == 0:
+        print(json.dumps(line))
+    er.close()
+
+
 # ----------------------------------------------------------------- ours --
 def main():
     args = parse()
@@ -252,6 +330,12 @@ def main():
     rank, world, local = dist_init(args.gpus)
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+    if args.workload == "n1":
+        run_n1(args, cfg, rank, world, local)
         if world > 1:
             import torch.distributed as dist
             dist.destroy_process_group()

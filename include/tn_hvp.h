@@ -77,6 +77,9 @@ typedef struct {
   int32_t depth;        /* D >= 1 brickwall layers                              */
   int32_t first_offset; /* 0 | 1: first layer on (0,1),(2,3).. or (1,2),(3,4).. */
   int32_t chi;          /* primal bond cap; tangent bonds <= 2*chi              */
+  int32_t site_dim;     /* 4: operator mode (MPO reference, bottom start        */
+                        /*    I/2^{n/2}); 2: state mode (MPS label, bottom      */
+                        /*    start a product state)         */
   int32_t dtype;        /* tn_dtype; TN_C128                                    */
   int32_t max_batch;    /* directions per internal sub-batch of tn_hvp_apply    */
   int32_t device;       /* CUDA device ordinal                                  */
@@ -99,7 +102,7 @@ int32_t tn_hvp_num_gates(int32_t n_sites, int32_t depth, int32_t first_offset);
 tn_status tn_hvp_query(const tn_hvp_config* cfg, const int32_t* ref_bonds, tn_hvp_sizes* out);
 
 /* Create a context.  ref_bonds: HOST int32[n+1] (b_0 = b_n = 1, neighbouring
- * bonds within a factor 4); ref_mpo: DEVICE, the n site tensors packed back to
+ * bonds within a factor site_dim); ref_mpo: DEVICE, the n site tensors packed back to
  * back in site order, sum_s b_s*4*b_{s+1} complex128 (copied into the context).
  * primal_buf: DEVICE, 256-byte aligned, >= tn_hvp_query's primal_bytes
  * (primal_bytes_avail), caller-owned and kept until tn_hvp_destroy; or NULL:
@@ -188,6 +191,23 @@ tn_status tn_hvp_primal_blob(tn_hvp_ctx* ctx, void** ptr, size_t* bytes);
  * TN_EINVAL and the store stays invalid.  Drops the per-point caches and the
  * translation-invariant state.  Synchronises the stream. */
 tn_status tn_hvp_primal_imported(tn_hvp_ctx* ctx, const void* gates, void* stream);
+
+/* ---- N1: sampled-state empirical risk (PAPER.md:525-554,
+ * eq:costHS) ------------------------------------------------------------------
+ * State mode (site_dim = 2): site tensors [b][2][b'] (p = out), the bottom
+ * start is a product state |psi> = (x)_s psi_s and the top start the label MPS
+ * phi = U_ref |psi>, so T = <phi| W |psi> and f = -|T|^2 is
+ * minus the sample's L_HS; every other call behaves as in operator mode (the
+ * empirical risk 1 - mean_s |T_s|^2 and its derivatives are sample means).
+ * tn_hvp_set_product_state: psi DEVICE complex128 [n][2] (each site normalised
+ *   by the caller); default |0...0>.  TN_EINVAL in operator mode.  Invalidates
+ *   the stored point.
+ * tn_hvp_set_reference: new reference / label tensors, same bonds as at setup,
+ *   packed as in tn_hvp_setup (DEVICE).  Invalidates the stored point.
+ * The label MPS phi = U_ref |psi> is input data (tn_inputs/samples.py builds it,
+ * right-canonical with structural bonds, as the reference MPO is). */
+tn_status tn_hvp_set_product_state(tn_hvp_ctx* ctx, const void* psi, void* stream);
+tn_status tn_hvp_set_reference(tn_hvp_ctx* ctx, const void* ref, void* stream);
 
 /* Release the per-point caches and CUDA graphs (the next apply rebuilds them)
  * and return the library pool's unused device memory to the device, e.g.

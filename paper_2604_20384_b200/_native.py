@@ -19,6 +19,7 @@ EXPORTS = ["tn_hvp_num_gates", "tn_hvp_setup", "tn_hvp_environments", "tn_hvp_ap
            "tn_hvp_work", "tn_retract", "tn_tangent_dot", "tn_tangent_axpby", "tn_hvp_primal_copy",
            "tn_hvp_launch_count", "tn_gemm_profile", "tn_pauli_basis", "tn_pauli_coords", "tn_sym_eig",
            "tn_hvp_ti_environments", "tn_hvp_ti_apply", "tn_hvp_step", "tn_hvp_query", "tn_hvp_trim_memory",
+           "tn_hvp_set_product_state", "tn_hvp_set_reference",
            "tn_hvp_destroy", "tn_hvp_last_error"]
 TN_C128, TN_C64 = 0, 1
 TN_CHECK_UNITARY, TN_CHECK_TANGENT = 1, 2
@@ -32,7 +33,12 @@ class TNError(RuntimeError):
 
 class Config(C.Structure):
     _fields_ = [("n_sites", C.c_int32), ("depth", C.c_int32), ("first_offset", C.c_int32), ("chi", C.c_int32),
-                ("dtype", C.c_int32), ("max_batch", C.c_int32), ("device", C.c_int32), ("flags", C.c_uint32)]
+                ("site_dim", C.c_int32), ("dtype", C.c_int32), ("max_batch", C.c_int32), ("device", C.c_int32),
+                ("flags", C.c_uint32)]
+
+
+def make_config(n, depth, chi, max_batch=1, first_offset=0, site_dim=4, dtype=0, device=0, flags=0) -> Config:
+    return Config(n, depth, first_offset, chi, site_dim, dtype, max_batch, device, flags)
 
 
 class Sizes(C.Structure):
@@ -54,6 +60,8 @@ def lib():
         L.tn_hvp_setup.argtypes = [C.POINTER(Config), C.POINTER(i32), vp, vp, C.c_size_t, vp, C.POINTER(vp)]
         L.tn_hvp_query.argtypes = [C.POINTER(Config), C.POINTER(i32), C.POINTER(Sizes)]
         L.tn_hvp_trim_memory.argtypes = [vp, vp]
+        L.tn_hvp_set_product_state.argtypes = [vp, vp, vp]
+        L.tn_hvp_set_reference.argtypes = [vp, vp, vp]
         L.tn_hvp_environments.argtypes = [vp, vp, vp, vp, vp]
         L.tn_hvp_apply.argtypes = [vp, i32, vp, vp, vp, vp]
         L.tn_hvp_gradient_T.argtypes = [vp, vp, vp]
@@ -76,7 +84,8 @@ def lib():
         L.tn_sym_eig.argtypes = [i32, vp, vp, vp, i32, vp]
         for name in ("tn_retract", "tn_tangent_dot", "tn_tangent_axpby", "tn_hvp_primal_copy", "tn_pauli_basis",
                      "tn_pauli_coords", "tn_sym_eig", "tn_hvp_ti_environments", "tn_hvp_ti_apply",
-                     "tn_hvp_step", "tn_hvp_query", "tn_hvp_trim_memory"):
+                     "tn_hvp_step", "tn_hvp_query", "tn_hvp_trim_memory", "tn_hvp_set_product_state",
+                     "tn_hvp_set_reference"):
             getattr(L, name).restype = C.c_int
         L.tn_hvp_launch_count.argtypes = []
         L.tn_hvp_launch_count.restype = C.c_int64
@@ -122,6 +131,14 @@ def tn_hvp_setup(cfg: Config, ref_bonds, ref_mpo_ptr, stream, primal_ptr=0, prim
 
 def tn_hvp_trim_memory(ctx, stream):
     check(lib().tn_hvp_trim_memory(ctx, C.c_void_p(stream)), ctx)
+
+
+def tn_hvp_set_product_state(ctx, psi_ptr, stream):
+    check(lib().tn_hvp_set_product_state(ctx, C.c_void_p(psi_ptr), C.c_void_p(stream)), ctx)
+
+
+def tn_hvp_set_reference(ctx, ref_ptr, stream):
+    check(lib().tn_hvp_set_reference(ctx, C.c_void_p(ref_ptr), C.c_void_p(stream)), ctx)
 
 
 def tn_hvp_environments(ctx, gates_ptr, scalars_ptr, grad_R_ptr, stream):

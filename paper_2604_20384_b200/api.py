@@ -31,7 +31,7 @@ class HVPEngine:
     U_ref/2^{n/2} (right-canonical, centre at site 0).
     """
 
-    def __init__(self, n, depth, chi, ref_sites, first_offset=0, max_batch=64, device=None, flags=0):
+    def __init__(self, n, depth, chi, ref_sites, first_offset=0, max_batch=64, device=None, flags=0, site_dim=4):
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2604_20384_b200 needs a CUDA device (no CPU fallback)")
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
@@ -39,7 +39,8 @@ class HVPEngine:
         self.K = N.tn_hvp_num_gates(n, depth, first_offset)
         self.ref_bonds = [1] + [int(a.shape[2]) for a in ref_sites]
         packed = torch.cat([a.to(self.device, torch.complex128).contiguous().reshape(-1) for a in ref_sites])
-        cfg = N.Config(n, depth, first_offset, chi, N.TN_C128, max_batch, self.device.index, flags)
+        self.site_dim = site_dim
+        cfg = N.make_config(n, depth, chi, max_batch, first_offset, site_dim, N.TN_C128, self.device.index, flags)
         # the primal store is a caller-owned torch buffer (tn_hvp_query's size):
         # visible to torch's allocator and broadcastable in place (parallel.py)
         self.primal_bytes, self.workspace_bytes, self.per_direction_bytes = N.tn_hvp_query(cfg, self.ref_bonds)
@@ -56,6 +57,17 @@ class HVPEngine:
             N.tn_hvp_destroy(self.ctx)
             self.ctx = None
             self.primal = None
+
+    def set_product_state(self, psi: torch.Tensor):
+        """State mode: the bottom start |psi> = (x)_s psi[s] (psi [n, 2] complex128)."""
+        _require_cuda(psi, "psi")
+        N.tn_hvp_set_product_state(self.ctx, psi.data_ptr(), _stream())
+
+    def set_reference(self, sites):
+        """New reference / label tensors with the bonds given at construction."""
+        packed = torch.cat([a.to(self.device, torch.complex128).contiguous().reshape(-1) for a in sites])
+        N.tn_hvp_set_reference(self.ctx, packed.data_ptr(), _stream())
+        torch.cuda.current_stream().synchronize()      # packed is a temporary
 
     def trim_memory(self):
         """Drop per-point caches / graphs and return the library pool's unused memory."""

@@ -2,6 +2,7 @@
 // last-error text; the work itself lives in engine.cu / zgemm.cu / kernels.cu.
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/tn_hvp.h"
 #include "common.cuh"
@@ -79,6 +80,8 @@ tn_status check_config(const tn_hvp_config* cfg, const int32_t* ref_bonds, const
   if (cfg->n_sites < 2 || cfg->depth < 1 || (cfg->first_offset != 0 && cfg->first_offset != 1) || cfg->chi < 1 ||
       cfg->max_batch < 1 || cfg->device < 0)
     return fail(nullptr, TN_EINVAL, w + ": n>=2, depth>=1, offset in {0,1}, chi>=1, max_batch>=1, device>=0");
+  if (cfg->site_dim != 4 && cfg->site_dim != 2)
+    return fail(nullptr, TN_EINVAL, w + ": site_dim must be 4 (operator mode) or 2 (state mode)");
   if (cfg->dtype != TN_C128)
     return fail(nullptr, TN_EINVAL, w + ": only dtype TN_C128 is built (the complex64 mode is not implemented)");
   if (cfg->flags & ~(TN_CHECK_UNITARY | TN_CHECK_TANGENT))
@@ -87,8 +90,9 @@ tn_status check_config(const tn_hvp_config* cfg, const int32_t* ref_bonds, const
     return fail(nullptr, TN_EINVAL, w + ": boundary bonds must be 1");
   for (int s = 0; s < cfg->n_sites; ++s) {
     const int64_t bl = ref_bonds[s], br = ref_bonds[s + 1];
-    if (bl < 1 || br < 1 || br > 4 * bl || bl > 4 * br)
-      return fail(nullptr, TN_EINVAL, w + ": reference bonds must satisfy 1 <= b_{s+1} <= 4 b_s and vice versa");
+    const int64_t P = cfg->site_dim;
+    if (bl < 1 || br < 1 || br > P * bl || bl > P * br)
+      return fail(nullptr, TN_EINVAL, w + ": reference bonds must satisfy 1 <= b_{s+1} <= site_dim b_s and vice versa");
   }
   return TN_OK;
 }
@@ -110,6 +114,16 @@ tn_status tn_hvp_setup(const tn_hvp_config* cfg, const int32_t* ref_bonds, const
   return guarded(nullptr, [&] {
     *out = tn::engine_create(*cfg, ref_bonds, ref_mpo, primal_buf, primal_bytes_avail, (cudaStream_t)stream);
   });
+}
+
+tn_status tn_hvp_set_product_state(tn_hvp_ctx* ctx, const void* psi, void* stream) {
+  if (!ctx || !psi) return fail(ctx, TN_EINVAL, "tn_hvp_set_product_state: null argument");
+  return guarded(ctx, [&] { tn::engine_set_product_state(ctx, (const tn::cplx*)psi, (cudaStream_t)stream); });
+}
+
+tn_status tn_hvp_set_reference(tn_hvp_ctx* ctx, const void* ref, void* stream) {
+  if (!ctx || !ref) return fail(ctx, TN_EINVAL, "tn_hvp_set_reference: null argument");
+  return guarded(ctx, [&] { tn::engine_set_reference(ctx, (const tn::cplx*)ref, (cudaStream_t)stream); });
 }
 
 tn_status tn_hvp_trim_memory(tn_hvp_ctx* ctx, void* stream) {

@@ -133,6 +133,11 @@ thread_local bool g_fwd_thread = false;
 struct Engine {
   tn_hvp_config cfg{};
   int n = 0, D = 0, off = 0, chi = 0, K = 0;
+  // Site physical dimension P = 2 NI (index p = out * NI + in): operator mode
+  // P = 4 (MPO sites, bottom start I/2^{n/2}); state mode P = 2 (MPS sites,
+  // bottom start a product state).  PP = P^2, NI2 = NI^2.
+  int P = 4, PP = 16, NI = 2, NI2 = 4;
+  cplx* d_init = nullptr;  // [n][P] bond-1 bottom start (identity/sqrt 2 per site, or the product state)
   std::vector<std::vector<std::pair<int, int>>> layers;  // per layer (k, s)
   std::vector<int> ref_bonds;
   SidePlan bot, top;
@@ -301,14 +306,14 @@ struct Engine {
           st.aa1 = b.aa[c + 1];
           st.aa2 = c + 2 <= n ? b.aa[c + 2] : 0;
           if (right) {
-            st.kq = std::min(4 * st.b, st.bp);
+            st.kq = std::min(P * st.b, st.bp);
             st.nb2 = b.p[c + 2];
             if (b.ab[c] != b.p[c]) throw std::logic_error("plan: before-chain bond != primal bond (move right)");
             b.p[c + 1] = st.kq;
             b.ab[c + 1] = st.kq;
             ++c;
           } else {
-            st.kq = std::min(st.b, 4 * st.bp);
+            st.kq = std::min(st.b, P * st.bp);
             st.nb2 = b.p[c - 1];
             if (b.aa[c + 1] != b.p[c + 1]) throw std::logic_error("plan: after-chain bond != primal bond (move left)");
             b.p[c] = st.kq;
@@ -325,8 +330,8 @@ struct Engine {
         st.bl = b.p[i];
         st.m = b.p[i + 1];
         st.br = b.p[i + 2];
-        st.mn = std::min(4 * st.bl, 4 * st.br);
-        st.r = std::min({chi, 4 * st.m, 4 * st.bl, 4 * st.br});
+        st.mn = std::min(P * st.bl, P * st.br);
+        st.r = std::min({chi, 4 * st.m, P * st.bl, P * st.br});  // gate operator-Schmidt rank <= 4
         st.abm = i > 0 ? b.ab[i - 1] : 0;
         st.ab0 = b.ab[i];
         st.ab1 = b.ab[i + 1];
@@ -350,7 +355,7 @@ struct Engine {
 
   size_t mpo_elems(const std::vector<int>& p) const {
     size_t e = 0;
-    for (int s = 0; s < n; ++s) e += (size_t)p[s] * 4 * p[s + 1];
+    for (int s = 0; s < n; ++s) e += (size_t)p[s] * P * p[s + 1];
     return e;
   }
 
@@ -373,20 +378,20 @@ struct Engine {
       sp->o_snap.clear();
       for (const Bonds& b : sp->snap) {
         std::vector<size_t> offs(n);
-        for (int s = 0; s < n; ++s) offs[s] = take((size_t)b.p[s] * 4 * b.p[s + 1] * C);
+        for (int s = 0; s < n; ++s) offs[s] = take((size_t)b.p[s] * P * b.p[s + 1] * C);
         sp->o_snap.push_back(offs);
       }
       for (auto& ls : sp->steps)
         for (Step& st : ls) {
           if (st.type == PAIR) {
-            st.o_theta = take((size_t)16 * st.bl * st.br * C);
-            st.o_uh = take((size_t)st.r * 4 * st.bl * C);
-            st.o_vh = take((size_t)st.r * 4 * st.br * C);
+            st.o_theta = take((size_t)PP * st.bl * st.br * C);
+            st.o_uh = take((size_t)st.r * P * st.bl * C);
+            st.o_vh = take((size_t)st.r * P * st.br * C);
             st.o_S = take((size_t)st.mn * sizeof(double));
             st.o_s = take(sizeof(double));
             st.s_index = s_index++;
           } else {
-            st.o_q = take((size_t)4 * std::max(st.b, st.bp) * st.kq * C);
+            st.o_q = take((size_t)P * std::max(st.b, st.bp) * st.kq * C);
           }
         }
     }
@@ -417,6 +422,10 @@ struct Engine {
   // profiles (a2/a3 keep rule, X7), and the primal-arena layout.
   void plan(const tn_hvp_config& c, const int32_t* rb) {
     cfg = c;
+    P = c.site_dim == 2 ? 2 : 4;
+    NI = P / 2;
+    PP = P * P;
+    NI2 = NI * NI;
     n = c.n_sites;
     D = c.depth;
     off = c.first_offset;
@@ -473,6 +482,20 @@ struct Engine {
       if (!lo.empty()) TN_CUDA(cudaMemcpy(d_layer_of, lo.data(), sizeof(int) * lo.size(), cudaMemcpyHostToDevice));
       TN_CUDA(cudaMemcpy(d_layer_start, ls.data(), sizeof(int) * ls.size(), cudaMemcpyHostToDevice));
     }
+    {  // bottom start: operator mode delta_{oi}/sqrt 2 per site; state mode |0> (tn_hvp_set_product_state)
+      std::vector<cplx> h((size_t)n * P, ZERO);
+      const double r2 = 1.0 / std::sqrt(2.0);
+      for (int s = 0; s < n; ++s) {
+        if (P == 4) {
+          h[(size_t)s * 4] = {r2, 0.0};
+          h[(size_t)s * 4 + 3] = {r2, 0.0};
+        } else {
+          h[(size_t)s * 2] = ONE;
+        }
+      }
+      TN_CUDA(cudaMalloc(&d_init, sizeof(cplx) * h.size()));
+      TN_CUDA(cudaMemcpy(d_init, h.data(), sizeof(cplx) * h.size(), cudaMemcpyHostToDevice));
+    }
     if (primal_buf) {
       arena = static_cast<char*>(primal_buf);
       own_arena = false;
@@ -486,7 +509,7 @@ struct Engine {
     size_t e = 0;
     for (int s = 0; s < n; ++s) {
       ref_off[s] = e;
-      e += (size_t)ref_bonds[s] * 4 * ref_bonds[s + 1];
+      e += (size_t)ref_bonds[s] * P * ref_bonds[s + 1];
     }
     TN_CUDA(cudaMalloc(&ref, e * sizeof(cplx)));
     TN_CUDA(cudaMemcpyAsync(ref, ref_mpo, e * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
@@ -515,11 +538,11 @@ struct Engine {
       for (auto& ls : sp->steps)
         for (Step& s : ls) {
           if (s.type == PAIR) {
-            const int mr = std::max(4 * s.bl, 4 * s.br), nc_ = std::min(4 * s.bl, 4 * s.br);
+            const int mr = std::max(P * s.bl, P * s.br), nc_ = std::min(P * s.bl, P * s.br);
             {
               int lw = 0;
-              TN_SOLVER(cusolverDnZheevd_bufferSize(so.h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, 4 * s.bl,
-                                                    nullptr, 4 * s.bl, nullptr, &lw));
+              TN_SOLVER(cusolverDnZheevd_bufferSize(so.h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, P * s.bl,
+                                                    nullptr, P * s.bl, nullptr, &lw));
               lwork_heevd = std::max(lwork_heevd, lw);
             }
             {  // QR-iteration SVD workspace (fallback of the Gram split)
@@ -531,12 +554,12 @@ struct Engine {
               svd_hws = std::max(svd_hws, h2);
             }
             int lw = 0;  // LQ of Y (r x 4br): geqrf on the column-major (4br x r) view
-            TN_SOLVER(cusolverDnZgeqrf_bufferSize(so.h, 4 * s.br, s.r, nullptr, 4 * s.br, &lw));
+            TN_SOLVER(cusolverDnZgeqrf_bufferSize(so.h, P * s.br, s.r, nullptr, P * s.br, &lw));
             lwork_geqrf = std::max(lwork_geqrf, lw);
-            TN_SOLVER(cusolverDnZungqr_bufferSize(so.h, 4 * s.br, s.r, s.r, nullptr, 4 * s.br, nullptr, &lw));
+            TN_SOLVER(cusolverDnZungqr_bufferSize(so.h, P * s.br, s.r, s.r, nullptr, P * s.br, nullptr, &lw));
             lwork_ungqr = std::max(lwork_ungqr, lw);
           } else {
-            const int mr = s.type == MOVE_R ? 4 * s.b : 4 * s.bp;
+            const int mr = s.type == MOVE_R ? P * s.b : P * s.bp;
             const int nc_ = s.type == MOVE_R ? s.bp : s.b;
             int lw = 0;
             TN_SOLVER(cusolverDnZgeqrf_bufferSize(so.h, mr, nc_, nullptr, mr, &lw));
@@ -552,6 +575,7 @@ struct Engine {
   // (tn_hvp_destroy contract); the engine drains its own streams.
   ~Engine() {
     if (!st1) {  // never set up (tn_hvp_query, or setup failed early)
+      if (d_init) cudaFree(d_init);
       if (d_layer_of) cudaFree(d_layer_of);
       if (d_layer_start) cudaFree(d_layer_start);
       if (ti_buf) cudaFree(ti_buf);
@@ -564,6 +588,7 @@ struct Engine {
     drop_graphs(stc);
     drop_chain_cache(stc);
     cudaStreamSynchronize(stc);
+    if (d_init) cudaFree(d_init);
     if (d_layer_of) cudaFree(d_layer_of);
     if (d_layer_start) cudaFree(d_layer_start);
     if (ti_buf) cudaFree(ti_buf);
@@ -741,76 +766,71 @@ struct Engine {
                   const std::function<void(int)>& on_snap = nullptr, const cplx* gmat = nullptr) {
     SidePlan& sp = is_top ? top : bot;
     const cplx* G = gmat ? gmat : is_top ? at(o_gdag) : at(o_gates);
-    Mps P;
-    P.a.assign(n, nullptr);
-    P.b = sp.init.p;
+    Mps ps;
+    ps.a.assign(n, nullptr);
+    ps.b = sp.init.p;
     for (int s = 0; s < n; ++s) {
-      const int64_t e = (int64_t)P.b[s] * 4 * P.b[s + 1];
-      P.a[s] = dnew(e, st);
-      if (is_top) {
-        TN_CUDA(cudaMemcpyAsync(P.a[s], ref + ref_off[s], e * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-      } else {
-        const double h = 1.0 / std::sqrt(2.0);
-        cplx id[4] = {{h, 0}, {0, 0}, {0, 0}, {h, 0}};
-        TN_CUDA(cudaMemcpyAsync(P.a[s], id, sizeof(id), cudaMemcpyHostToDevice, st));
-      }
+      const int64_t e = (int64_t)ps.b[s] * P * ps.b[s + 1];
+      ps.a[s] = dnew(e, st);
+      const cplx* src = is_top ? ref + ref_off[s] : d_init + (int64_t)s * P;  // bottom: bond-1 start
+      TN_CUDA(cudaMemcpyAsync(ps.a[s], src, e * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
     }
     for (size_t li = 0; li < sp.steps.size(); ++li) {
-      if (store) snapshot(st, P, sp.o_snap[li]);
+      if (store) snapshot(st, ps, sp.o_snap[li]);
       if (on_snap) on_snap((int)li);
       for (const Step& s : sp.steps[li]) {
         Pool tmp(st);  // step temporaries
         if (s.type == MOVE_R) {
           const int c = s.site;
-          cplx* Q = store ? at(s.o_q) : tmp.c((int64_t)4 * s.b * s.kq);
+          cplx* Q = store ? at(s.o_q) : tmp.c((int64_t)P * s.b * s.kq);
           cplx* R = tmp.c((int64_t)s.kq * s.bp);
-          qr_right(st, so, tmp, P.a[c], 4 * s.b, s.bp, s.kq, Q, R, info);
-          cplx* nc_ = dnew((int64_t)4 * s.b * s.kq, st);
-          TN_CUDA(cudaMemcpyAsync(nc_, Q, (size_t)4 * s.b * s.kq * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-          cplx* nx = dnew((int64_t)s.kq * 4 * s.nb2, st);
-          nn(st, s.kq, 4 * s.nb2, s.bp, R, 0, P.a[c + 1], 0, nx, 0, 1);
-          dset(P.a[c], nc_, st);
-          dset(P.a[c + 1], nx, st);
-          P.b[c + 1] = s.kq;
+          qr_right(st, so, tmp, ps.a[c], P * s.b, s.bp, s.kq, Q, R, info);
+          cplx* nc_ = dnew((int64_t)P * s.b * s.kq, st);
+          TN_CUDA(cudaMemcpyAsync(nc_, Q, (size_t)P * s.b * s.kq * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+          cplx* nx = dnew((int64_t)s.kq * P * s.nb2, st);
+          nn(st, s.kq, P * s.nb2, s.bp, R, 0, ps.a[c + 1], 0, nx, 0, 1);
+          dset(ps.a[c], nc_, st);
+          dset(ps.a[c + 1], nx, st);
+          ps.b[c + 1] = s.kq;
         } else if (s.type == MOVE_L) {
           const int c = s.site;
-          cplx* Q = store ? at(s.o_q) : tmp.c((int64_t)s.kq * 4 * s.bp);
+          cplx* Q = store ? at(s.o_q) : tmp.c((int64_t)s.kq * P * s.bp);
           cplx* L = tmp.c((int64_t)s.b * s.kq);
-          lq_left(st, so, tmp, P.a[c], s.b, 4 * s.bp, s.kq, Q, L, info);
-          cplx* nc_ = dnew((int64_t)s.kq * 4 * s.bp, st);
-          TN_CUDA(cudaMemcpyAsync(nc_, Q, (size_t)s.kq * 4 * s.bp * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-          cplx* nx = dnew((int64_t)s.nb2 * 4 * s.kq, st);
-          nn(st, s.nb2 * 4, s.kq, s.b, P.a[c - 1], 0, L, 0, nx, 0, 1);
-          dset(P.a[c], nc_, st);
-          dset(P.a[c - 1], nx, st);
-          P.b[c] = s.kq;
+          lq_left(st, so, tmp, ps.a[c], s.b, P * s.bp, s.kq, Q, L, info);
+          cplx* nc_ = dnew((int64_t)s.kq * P * s.bp, st);
+          TN_CUDA(cudaMemcpyAsync(nc_, Q, (size_t)s.kq * P * s.bp * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+          cplx* nx = dnew((int64_t)s.nb2 * P * s.kq, st);
+          nn(st, s.nb2 * P, s.kq, s.b, ps.a[c - 1], 0, L, 0, nx, 0, 1);
+          dset(ps.a[c], nc_, st);
+          dset(ps.a[c - 1], nx, st);
+          ps.b[c] = s.kq;
         } else {
           const int i = s.site;
-          const int64_t nth = (int64_t)16 * s.bl * s.br;
+          const int64_t nth = (int64_t)PP * s.bl * s.br;
           cplx* theta = store ? at(s.o_theta) : tmp.c(nth);
-          nn(st, 4 * s.bl, 4 * s.br, s.m, P.a[i], 0, P.a[i + 1], 0, theta, 0, 1);
+          nn(st, P * s.bl, P * s.br, s.m, ps.a[i], 0, ps.a[i + 1], 0, theta, 0, 1);
           cplx* A = tmp.c(nth);
-          apply_gate(st, A, 0, theta, 0, G + (int64_t)s.k * 16, 0, s.bl, s.br, 1, ONE, false);
+          apply_gate(st, A, 0, theta, 0, G + (int64_t)s.k * 16, 0, s.bl, s.br, 1, ONE, false, NI);
           double* S = store ? at<double>(s.o_S) : (double*)tmp.raw((size_t)s.mn * sizeof(double));
-          cplx* uh = store ? at(s.o_uh) : tmp.c((int64_t)s.r * 4 * s.bl);
-          cplx* vh = store ? at(s.o_vh) : tmp.c((int64_t)s.r * 4 * s.br);
+          cplx* uh = store ? at(s.o_uh) : tmp.c((int64_t)s.r * P * s.bl);
+          cplx* vh = store ? at(s.o_vh) : tmp.c((int64_t)s.r * P * s.br);
           // Split: Gram heevd (fast) when the cut lies where it resolves the
           // spectrum (smallest kept sigma >= 1e-6 sigma_1 and a boundary gap in
           // sigma^2 >= 1e-12 sigma_1^2), else one-sided Jacobi (relative accuracy).
           int method = kGram;
-          int nbas = 4 * s.bl;
+          int nbas = P * s.bl;
           cplx* Acp = tmp.c(nth);
           TN_CUDA(cudaMemcpyAsync(Acp, A, nth * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-          cplx* uhf = tmp.c((int64_t)4 * s.bl * 4 * s.bl);
-          double* Sf = (double*)tmp.raw((size_t)4 * s.bl * sizeof(double));
-          svd_rowmajor(st, so, tmp, Acp, 4 * s.bl, 4 * s.br, Sf, uhf, info + 1, method);
+          cplx* uhf = tmp.c((int64_t)P * s.bl * P * s.bl);
+          double* Sf = (double*)tmp.raw((size_t)P * s.bl * sizeof(double));
+          svd_rowmajor(st, so, tmp, Acp, P * s.bl, P * s.br, Sf, uhf, info + 1, method);
           int iters = 0;
-          if (s.r < 4 * s.bl) {  // something (discarded or null) is excluded
+          if (s.r < P * s.bl) {  // something (discarded or null) is excluded
             // kept/excluded mixing of a Gram basis ~ eps sigma_top^2 / (sigma_{r-1}^2 - sigma_r^2)
             // (sigma_r = 0 for a null direction); first-order refinement converges
             // quadratically from delta <~ 1e-2.  Otherwise a second Gram level on the
             // low block (resolves relative to its own scale), else QR-iteration SVD.
-            const int R = 4 * s.bl;
+            const int R = P * s.bl;
             std::vector<double> hS(R);
             TN_CUDA(cudaMemcpyAsync(hS.data(), Sf, R * sizeof(double), cudaMemcpyDeviceToHost, st));
             TN_CUDA(cudaStreamSynchronize(st));
@@ -829,8 +849,8 @@ struct Engine {
               int n_hi = top_i;
               while (n_hi < R && hS[n_hi] >= 1e-4 * hS[top_i]) ++n_hi;
               if (!(n_hi > top_i && n_hi < s.r)) break;
-              refine_kept(st, tmp, uhf, Sf, A, R, 4 * s.br, R, n_hi, 2);
-              deflate_low(st, so, tmp, uhf, Sf, A, R, 4 * s.br, n_hi, info + 1);
+              refine_kept(st, tmp, uhf, Sf, A, R, P * s.br, R, n_hi, 2);
+              deflate_low(st, so, tmp, uhf, Sf, A, R, P * s.br, n_hi, info + 1);
               TN_CUDA(cudaMemcpyAsync(hS.data(), Sf, R * sizeof(double), cudaMemcpyDeviceToHost, st));
               TN_CUDA(cudaStreamSynchronize(st));
               delta = mixing(hS[n_hi]);
@@ -850,7 +870,7 @@ struct Engine {
               nbas = s.mn;
               iters = 2;
               TN_CUDA(cudaMemcpyAsync(Acp, A, nth * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-              svd_rowmajor(st, so, tmp, Acp, 4 * s.bl, 4 * s.br, Sf, uhf, info + 1, method);
+              svd_rowmajor(st, so, tmp, Acp, P * s.bl, P * s.br, Sf, uhf, info + 1, method);
               ++n_fallback;
             } else {
               iters = delta < 1e-8 ? 1 : delta < 1e-4 ? 2 : 4;
@@ -858,44 +878,44 @@ struct Engine {
           }
           TN_CUDA(cudaMemcpyAsync(S, Sf, (size_t)s.mn * sizeof(double), cudaMemcpyDeviceToDevice, st));
           double* sc = store ? at<double>(s.o_s) : (double*)tmp.raw(sizeof(double));
-          refine_kept(st, tmp, uhf, Sf, A, 4 * s.bl, 4 * s.br, nbas, s.r, iters);
-          TN_CUDA(cudaMemcpyAsync(uh, uhf, (size_t)s.r * 4 * s.bl * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+          refine_kept(st, tmp, uhf, Sf, A, P * s.bl, P * s.br, nbas, s.r, iters);
+          TN_CUDA(cudaMemcpyAsync(uh, uhf, (size_t)s.r * P * s.bl * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
           // Y = U_r^H A (= S_r W_r^H up to a kept-space rotation); LQ gives W_r^H
-          cplx* Y = tmp.c((int64_t)s.r * 4 * s.br);
-          nn(st, s.r, 4 * s.br, 4 * s.bl, uh, 0, A, 0, Y, 0, 1);
+          cplx* Y = tmp.c((int64_t)s.r * P * s.br);
+          nn(st, s.r, P * s.br, P * s.bl, uh, 0, A, 0, Y, 0, 1);
           {  // frozen s = ||A|| / ||U_r^H A|| and diagnostics
             double* nrm = (double*)tmp.raw(2 * sizeof(double));
             tangent_dot(st, nth, 1, A, A, nrm);
-            tangent_dot(st, (int64_t)s.r * 4 * s.br, 1, Y, Y, nrm + 1);
+            tangent_dot(st, (int64_t)s.r * P * s.br, 1, Y, Y, nrm + 1);
             s_from_norms(st, nrm, S, s.mn, s.r, sc, diag);
           }
           cplx* Lq = tmp.c((int64_t)s.r * s.r);
-          lq_left(st, so, tmp, Y, s.r, 4 * s.br, s.r, vh, Lq, info);
-          cplx* ni = dnew((int64_t)4 * s.bl * s.r, st);
-          cplx* nj = dnew((int64_t)s.r * 4 * s.br, st);
+          lq_left(st, so, tmp, Y, s.r, P * s.br, s.r, vh, Lq, info);
+          cplx* ni = dnew((int64_t)P * s.bl * s.r, st);
+          cplx* nj = dnew((int64_t)s.r * P * s.br, st);
           if (s.lr) {  // (U_r, s U_r^H A), centre -> i+1
-            conjT_scale_cols(st, ni, uh, s.r, 4 * s.bl, nullptr, nullptr);
-            TN_CUDA(cudaMemcpyAsync(nj, Y, (size_t)s.r * 4 * s.br * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-            scale_by(st, nj, sc, 1.0, (int64_t)s.r * 4 * s.br);
+            conjT_scale_cols(st, ni, uh, s.r, P * s.bl, nullptr, nullptr);
+            TN_CUDA(cudaMemcpyAsync(nj, Y, (size_t)s.r * P * s.br * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+            scale_by(st, nj, sc, 1.0, (int64_t)s.r * P * s.br);
           } else {     // (s U_r L, W_r^H), centre -> i
-            cn(st, 4 * s.bl, s.r, s.r, uh, 0, Lq, 0, ni, 0, 1);
-            scale_by(st, ni, sc, 1.0, (int64_t)4 * s.bl * s.r);
-            TN_CUDA(cudaMemcpyAsync(nj, vh, (size_t)s.r * 4 * s.br * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+            cn(st, P * s.bl, s.r, s.r, uh, 0, Lq, 0, ni, 0, 1);
+            scale_by(st, ni, sc, 1.0, (int64_t)P * s.bl * s.r);
+            TN_CUDA(cudaMemcpyAsync(nj, vh, (size_t)s.r * P * s.br * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
           }
-          dset(P.a[i], ni, st);
-          dset(P.a[i + 1], nj, st);
-          P.b[i + 1] = s.r;
+          dset(ps.a[i], ni, st);
+          dset(ps.a[i + 1], nj, st);
+          ps.b[i + 1] = s.r;
         }
       }
     }
-    if (store) snapshot(st, P, sp.o_snap.back());
+    if (store) snapshot(st, ps, sp.o_snap.back());
     if (on_snap) on_snap((int)sp.steps.size());
-    return P;
+    return ps;
   }
 
-  void snapshot(cudaStream_t st, const Mps& P, const std::vector<size_t>& offs) {
+  void snapshot(cudaStream_t st, const Mps& ps, const std::vector<size_t>& offs) {
     for (int s = 0; s < n; ++s)
-      TN_CUDA(cudaMemcpyAsync(at(offs[s]), P.a[s], (size_t)P.b[s] * 4 * P.b[s + 1] * sizeof(cplx),
+      TN_CUDA(cudaMemcpyAsync(at(offs[s]), ps.a[s], (size_t)ps.b[s] * P * ps.b[s + 1] * sizeof(cplx),
                               cudaMemcpyDeviceToDevice, st));
   }
 
@@ -905,10 +925,10 @@ struct Engine {
     cplx* L = pool.c(1);
     TN_CUDA(cudaMemcpyAsync(L, &ONE, sizeof(cplx), cudaMemcpyHostToDevice, st));
     for (int s = 0; s < n; ++s) {
-      cplx* Y = pool.c((int64_t)tb[s] * 4 * bb[s + 1]);
-      nn(st, tb[s], 4 * bb[s + 1], bb[s], L, 0, bp[s], 0, Y, 0, 1);
+      cplx* Y = pool.c((int64_t)tb[s] * P * bb[s + 1]);
+      nn(st, tb[s], P * bb[s + 1], bb[s], L, 0, bp[s], 0, Y, 0, 1);
       cplx* L2 = pool.c((int64_t)tb[s + 1] * bb[s + 1]);
-      cn(st, tb[s + 1], bb[s + 1], 4 * tb[s], tp[s], 0, Y, 0, L2, 0, 1);
+      cn(st, tb[s + 1], bb[s + 1], P * tb[s], tp[s], 0, Y, 0, L2, 0, 1);
       L = L2;
     }
     return L;
@@ -1215,7 +1235,7 @@ struct Engine {
   // Two-site block of site tensors a (x,4,m), b (m,4,y): out (x,4,4,y)
   void pair(cudaStream_t st, cplx* out, const cplx* a, int64_t sa, const cplx* b, int64_t sb, int x, int m, int y,
             int batch) {
-    nn(st, 4 * x, 4 * y, m, a, sa, b, sb, out, (int64_t)16 * x * y, batch);
+    nn(st, P * x, P * y, m, a, sa, b, sb, out, (int64_t)PP * x * y, batch);
   }
 
   // a4: per layer right sweep, left sweep with E_k (primal envs stored for apply)
@@ -1242,19 +1262,19 @@ struct Engine {
       const int s = blks[j].first, k = blks[j].second;
       Pool pool(st);  // block temporaries
       if (k < 0) {
-        cplx* Y = pool.c((int64_t)bb[s] * 4 * tb[s + 1]);
-        nn(st, 4 * bb[s], tb[s + 1], bb[s + 1], bp[s], 0, at(o_R[ell][s + 1]), 0, Y, 0, 1);
-        nc(st, bb[s], tb[s], 4 * tb[s + 1], Y, 0, tp[s], 0, at(o_R[ell][s]), 0, 1);
+        cplx* Y = pool.c((int64_t)bb[s] * P * tb[s + 1]);
+        nn(st, P * bb[s], tb[s + 1], bb[s + 1], bp[s], 0, at(o_R[ell][s + 1]), 0, Y, 0, 1);
+        nc(st, bb[s], tb[s], P * tb[s + 1], Y, 0, tp[s], 0, at(o_R[ell][s]), 0, 1);
       } else {
-        cplx* TB = TBs[s] = lp.c((int64_t)16 * bb[s] * bb[s + 2]);
+        cplx* TB = TBs[s] = lp.c((int64_t)PP * bb[s] * bb[s + 2]);
         pair(st, TB, bp[s], 0, bp[s + 1], 0, bb[s], bb[s + 1], bb[s + 2], 1);
-        cplx* TT = TTs[s] = lp.c((int64_t)16 * tb[s] * tb[s + 2]);
+        cplx* TT = TTs[s] = lp.c((int64_t)PP * tb[s] * tb[s + 2]);
         pair(st, TT, tp[s], 0, tp[s + 1], 0, tb[s], tb[s + 1], tb[s + 2], 1);
-        cplx* TTg = pool.c((int64_t)16 * tb[s] * tb[s + 2]);
-        apply_gate(st, TTg, 0, TT, 0, at(o_gdag) + (int64_t)k * 16, 0, tb[s], tb[s + 2], 1, ONE, false);
-        cplx* Y = pool.c((int64_t)16 * bb[s] * tb[s + 2]);
-        nn(st, 16 * bb[s], tb[s + 2], bb[s + 2], TB, 0, at(o_R[ell][s + 2]), 0, Y, 0, 1);
-        nc(st, bb[s], tb[s], 16 * tb[s + 2], Y, 0, TTg, 0, at(o_R[ell][s]), 0, 1);
+        cplx* TTg = pool.c((int64_t)PP * tb[s] * tb[s + 2]);
+        apply_gate(st, TTg, 0, TT, 0, at(o_gdag) + (int64_t)k * 16, 0, tb[s], tb[s + 2], 1, ONE, false, NI);
+        cplx* Y = pool.c((int64_t)PP * bb[s] * tb[s + 2]);
+        nn(st, PP * bb[s], tb[s + 2], bb[s + 2], TB, 0, at(o_R[ell][s + 2]), 0, Y, 0, 1);
+        nc(st, bb[s], tb[s], PP * tb[s + 2], Y, 0, TTg, 0, at(o_R[ell][s]), 0, 1);
       }
     }
     // left sweep + extraction
@@ -1262,19 +1282,19 @@ struct Engine {
       const int s = blks[j].first, k = blks[j].second;
       Pool pool(st);  // block temporaries
       if (k < 0) {
-        cplx* Y = pool.c((int64_t)tb[s] * 4 * bb[s + 1]);
-        nn(st, tb[s], 4 * bb[s + 1], bb[s], at(o_L[ell][s]), 0, bp[s], 0, Y, 0, 1);
-        cn(st, tb[s + 1], bb[s + 1], 4 * tb[s], tp[s], 0, Y, 0, at(o_L[ell][s + 1]), 0, 1);
+        cplx* Y = pool.c((int64_t)tb[s] * P * bb[s + 1]);
+        nn(st, tb[s], P * bb[s + 1], bb[s], at(o_L[ell][s]), 0, bp[s], 0, Y, 0, 1);
+        cn(st, tb[s + 1], bb[s + 1], P * tb[s], tp[s], 0, Y, 0, at(o_L[ell][s + 1]), 0, 1);
       } else {
         cplx* TB = TBs[s];
         cplx* TT = TTs[s];
-        cplx* Y = pool.c((int64_t)16 * tb[s] * bb[s + 2]);
-        nn(st, tb[s], 16 * bb[s + 2], bb[s], at(o_L[ell][s]), 0, TB, 0, Y, 0, 1);
-        cplx* Z = pool.c((int64_t)16 * tb[s] * tb[s + 2]);
-        nn(st, 16 * tb[s], tb[s + 2], bb[s + 2], Y, 0, at(o_R[ell][s + 2]), 0, Z, 0, 1);
-        extract_env(st, at(o_E) + (int64_t)k * 16, 0, TT, 0, Z, 0, tb[s], tb[s + 2], 1, ONE);
-        apply_gate(st, TT, 0, TT, 0, at(o_gdag) + (int64_t)k * 16, 0, tb[s], tb[s + 2], 1, ONE, false);
-        cn(st, tb[s + 2], bb[s + 2], 16 * tb[s], TT, 0, Y, 0, at(o_L[ell][s + 2]), 0, 1);
+        cplx* Y = pool.c((int64_t)PP * tb[s] * bb[s + 2]);
+        nn(st, tb[s], PP * bb[s + 2], bb[s], at(o_L[ell][s]), 0, TB, 0, Y, 0, 1);
+        cplx* Z = pool.c((int64_t)PP * tb[s] * tb[s + 2]);
+        nn(st, PP * tb[s], tb[s + 2], bb[s + 2], Y, 0, at(o_R[ell][s + 2]), 0, Z, 0, 1);
+        extract_env(st, at(o_E) + (int64_t)k * 16, 0, TT, 0, Z, 0, tb[s], tb[s + 2], 1, ONE, NI);
+        apply_gate(st, TT, 0, TT, 0, at(o_gdag) + (int64_t)k * 16, 0, tb[s], tb[s + 2], 1, ONE, false, NI);
+        cn(st, tb[s + 2], bb[s + 2], PP * tb[s], TT, 0, Y, 0, at(o_L[ell][s + 2]), 0, 1);
       }
     }
   }
@@ -1294,10 +1314,7 @@ struct Engine {
     std::vector<const cplx*> tp(T0.a.begin(), T0.a.end());
     std::vector<int> ones(n + 1, 1);
     std::vector<const cplx*> bp(n);
-    cplx* id = pool.c(4);
-    const double h = 1.0 / std::sqrt(2.0);
-    set_small(st, id, 4, {h, 0.0}, ZERO, ZERO, {h, 0.0});
-    for (int s = 0; s < n; ++s) bp[s] = id;
+    for (int s = 0; s < n; ++s) bp[s] = d_init + (int64_t)s * P;  // B_0: the bond-1 bottom start
     cplx* T11 = overlap(st, pool, tp, T0.b, bp, ones);
     for (cplx*& p : T0.a) ddel(p, st);
     double* sc = (double*)pool.raw(8 * sizeof(double));
@@ -1316,7 +1333,7 @@ struct Engine {
 
   // ---------------------------------------------------- tangent pass --
 
-  int64_t bsize(const Bonds& b, int s) const { return (int64_t)b.ab[s] * 4 * b.aa[s + 1]; }
+  int64_t bsize(const Bonds& b, int s) const { return (int64_t)b.ab[s] * P * b.aa[s + 1]; }
 
   void tangent_init(cudaStream_t st, Tangent& t, const SidePlan& sp, bool is_top, int nb,
                     ChainCache* cache = nullptr) {
@@ -1333,7 +1350,7 @@ struct Engine {
       cache->init_Aa.assign(n, nullptr);
     }
     for (int s = 0; s < n; ++s) {
-      const int64_t e = (int64_t)t.bd.p[s] * 4 * t.bd.p[s + 1];
+      const int64_t e = (int64_t)t.bd.p[s] * P * t.bd.p[s + 1];
       t.B[s] = dnew(e * nb, st);
       TN_CUDA(cudaMemsetAsync(t.B[s], 0, (size_t)e * nb * sizeof(cplx), st));
       if (t.mode == CHAIN_REPLAY) {
@@ -1343,16 +1360,9 @@ struct Engine {
       }
       t.Ab[s] = dnew(e, st);
       t.Aa[s] = dnew(e, st);
-      const cplx* src = is_top ? ref + ref_off[s] : nullptr;
-      if (is_top) {
-        TN_CUDA(cudaMemcpyAsync(t.Ab[s], src, e * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-        TN_CUDA(cudaMemcpyAsync(t.Aa[s], src, e * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-      } else {
-        const double h = 1.0 / std::sqrt(2.0);
-        cplx id[4] = {{h, 0}, {0, 0}, {0, 0}, {h, 0}};
-        set_small(st, t.Ab[s], 4, id[0], id[1], id[2], id[3]);
-        set_small(st, t.Aa[s], 4, id[0], id[1], id[2], id[3]);
-      }
+      const cplx* src = is_top ? ref + ref_off[s] : d_init + (int64_t)s * P;
+      TN_CUDA(cudaMemcpyAsync(t.Ab[s], src, e * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+      TN_CUDA(cudaMemcpyAsync(t.Aa[s], src, e * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
       if (t.mode == CHAIN_RECORD) {
         cache->init_Ab[s] = t.Ab[s];
         cache->init_Aa[s] = t.Aa[s];
@@ -1392,12 +1402,12 @@ struct Engine {
 
   int64_t chain_cache_elems(const SidePlan& sp) const {
     int64_t e = 0;
-    for (int s = 0; s < n; ++s) e += 2LL * sp.init.p[s] * 4 * sp.init.p[s + 1];
+    for (int s = 0; s < n; ++s) e += 2LL * sp.init.p[s] * P * sp.init.p[s + 1];
     for (auto& ls : sp.steps)
       for (const Step& x : ls) {
-        if (x.type == MOVE_R) e += (int64_t)x.kq * x.ab1 + 4LL * x.b * x.kq + (int64_t)x.kq * 4 * x.ab2;
-        else if (x.type == MOVE_L) e += (int64_t)x.aa0 * x.kq + (int64_t)x.kq * 4 * x.bp + (int64_t)x.aam * 4 * x.kq;
-        else e += 4LL * x.aa0 * x.r + (int64_t)x.r * 4 * x.br + 4LL * x.bl * x.r + (int64_t)x.r * 4 * x.ab2;
+        if (x.type == MOVE_R) e += (int64_t)x.kq * x.ab1 + (int64_t)P * x.b * x.kq + (int64_t)x.kq * P * x.ab2;
+        else if (x.type == MOVE_L) e += (int64_t)x.aa0 * x.kq + (int64_t)x.kq * P * x.bp + (int64_t)x.aam * P * x.kq;
+        else e += (int64_t)P * x.aa0 * x.r + (int64_t)x.r * P * x.br + (int64_t)P * x.bl * x.r + (int64_t)x.r * P * x.ab2;
       }
     return e;
   }
@@ -1479,21 +1489,21 @@ struct Engine {
         X = cc[0], nAbc = cc[1], nAb1 = cc[2];
       } else {
         X = t.mode == CHAIN_RECORD ? dnew((int64_t)kq * ab1, st) : pool.c((int64_t)kq * ab1);
-        cn(st, kq, ab1, 4 * b, Q, 0, t.Ab[c], 0, X, 0, 1);
-        nAbc = dnew((int64_t)4 * b * kq, st);
-        TN_CUDA(cudaMemcpyAsync(nAbc, Q, (size_t)4 * b * kq * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-        nAb1 = dnew((int64_t)kq * 4 * ab2, st);
-        nn(st, kq, 4 * ab2, ab1, X, 0, t.Ab[c + 1], 0, nAb1, 0, 1);
+        cn(st, kq, ab1, P * b, Q, 0, t.Ab[c], 0, X, 0, 1);
+        nAbc = dnew((int64_t)P * b * kq, st);
+        TN_CUDA(cudaMemcpyAsync(nAbc, Q, (size_t)P * b * kq * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+        nAb1 = dnew((int64_t)kq * P * ab2, st);
+        nn(st, kq, P * ab2, ab1, X, 0, t.Ab[c + 1], 0, nAb1, 0, 1);
         if (t.mode == CHAIN_RECORD) record(t, {X, nAbc, nAb1, nullptr});
       }
       // blocks: B_c (b,4,aa1), B_{c+1} (ab1,4,aa2)
-      const int64_t sc0 = (int64_t)4 * b * aa1, sc1o = (int64_t)ab1 * 4 * aa2, sc1n = (int64_t)kq * 4 * aa2;
+      const int64_t sc0 = (int64_t)P * b * aa1, sc1o = (int64_t)ab1 * P * aa2, sc1n = (int64_t)kq * P * aa2;
       cplx* Y = pool.c((int64_t)kq * aa1 * nb);
-      cn(st, kq, aa1, 4 * b, Q, 0, t.B[c], sc0, Y, (int64_t)kq * aa1, nb);
-      nn(st, 4 * b, aa1, kq, Q, 0, Y, (int64_t)kq * aa1, t.B[c], sc0, nb, MONE, ONE);
+      cn(st, kq, aa1, P * b, Q, 0, t.B[c], sc0, Y, (int64_t)kq * aa1, nb);
+      nn(st, P * b, aa1, kq, Q, 0, Y, (int64_t)kq * aa1, t.B[c], sc0, nb, MONE, ONE);
       cplx* nB1 = dnew(sc1n * nb, st);
-      nn(st, kq, 4 * aa2, ab1, X, 0, t.B[c + 1], sc1o, nB1, sc1n, nb);
-      nn(st, kq, 4 * aa2, aa1, Y, (int64_t)kq * aa1, t.Aa[c + 1], 0, nB1, sc1n, nb, ONE, ONE);
+      nn(st, kq, P * aa2, ab1, X, 0, t.B[c + 1], sc1o, nB1, sc1n, nb);
+      nn(st, kq, P * aa2, aa1, Y, (int64_t)kq * aa1, t.Aa[c + 1], 0, nB1, sc1n, nb, ONE, ONE);
       chain_set(t, t.Ab[c], nAbc, st);
       chain_set(t, t.Ab[c + 1], nAb1, st);
       dset(t.B[c + 1], nB1, st);
@@ -1509,21 +1519,21 @@ struct Engine {
         X = cc[0], nAac = cc[1], nAam = cc[2];
       } else {
         X = t.mode == CHAIN_RECORD ? dnew((int64_t)aa0 * kq, st) : pool.c((int64_t)aa0 * kq);
-        nc(st, aa0, kq, 4 * bp, t.Aa[c], 0, Q, 0, X, 0, 1);
-        nAac = dnew((int64_t)kq * 4 * bp, st);
-        TN_CUDA(cudaMemcpyAsync(nAac, Q, (size_t)kq * 4 * bp * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-        nAam = dnew((int64_t)aam * 4 * kq, st);
-        nn(st, aam * 4, kq, aa0, t.Aa[c - 1], 0, X, 0, nAam, 0, 1);
+        nc(st, aa0, kq, P * bp, t.Aa[c], 0, Q, 0, X, 0, 1);
+        nAac = dnew((int64_t)kq * P * bp, st);
+        TN_CUDA(cudaMemcpyAsync(nAac, Q, (size_t)kq * P * bp * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+        nAam = dnew((int64_t)aam * P * kq, st);
+        nn(st, aam * P, kq, aa0, t.Aa[c - 1], 0, X, 0, nAam, 0, 1);
         if (t.mode == CHAIN_RECORD) record(t, {X, nAac, nAam, nullptr});
       }
       // blocks: B_c (ab0,4,bp), B_{c-1} (abm,4,aa0)
-      const int64_t sc0 = (int64_t)ab0 * 4 * bp, sm_o = (int64_t)abm * 4 * aa0, sm_n = (int64_t)abm * 4 * kq;
+      const int64_t sc0 = (int64_t)ab0 * P * bp, sm_o = (int64_t)abm * P * aa0, sm_n = (int64_t)abm * P * kq;
       cplx* Y = pool.c((int64_t)ab0 * kq * nb);
-      nc(st, ab0, kq, 4 * bp, t.B[c], sc0, Q, 0, Y, (int64_t)ab0 * kq, nb);
-      nn(st, ab0, 4 * bp, kq, Y, (int64_t)ab0 * kq, Q, 0, t.B[c], sc0, nb, MONE, ONE);
+      nc(st, ab0, kq, P * bp, t.B[c], sc0, Q, 0, Y, (int64_t)ab0 * kq, nb);
+      nn(st, ab0, P * bp, kq, Y, (int64_t)ab0 * kq, Q, 0, t.B[c], sc0, nb, MONE, ONE);
       cplx* nBm = dnew(sm_n * nb, st);
-      nn(st, abm * 4, kq, aa0, t.B[c - 1], sm_o, X, 0, nBm, sm_n, nb);
-      nn(st, abm * 4, kq, ab0, t.Ab[c - 1], 0, Y, (int64_t)ab0 * kq, nBm, sm_n, nb, ONE, ONE);
+      nn(st, abm * P, kq, aa0, t.B[c - 1], sm_o, X, 0, nBm, sm_n, nb);
+      nn(st, abm * P, kq, ab0, t.Ab[c - 1], 0, Y, (int64_t)ab0 * kq, nBm, sm_n, nb, ONE, ONE);
       chain_set(t, t.Aa[c], nAac, st);
       chain_set(t, t.Aa[c - 1], nAam, st);
       dset(t.B[c - 1], nBm, st);
@@ -1538,33 +1548,33 @@ struct Engine {
       const cplx* uh = at(s.o_uh);  // (r x 4bl)
       const cplx* vh = at(s.o_vh);  // (r x 4br)
       const cplx* Mk = M + (int64_t)s.k * 16;
-      const int64_t nD = (int64_t)16 * bl * br;
+      const int64_t nD = (int64_t)PP * bl * br;
       // DTheta = M (B_i Aa_{i+1} + Ab_i B_{i+1}) + V_M Theta
       cplx* Dt = pool.c(nD * nb);
-      nn(st, 4 * bl, 4 * br, aa1, t.B[i], (int64_t)4 * bl * aa1, t.Aa[i + 1], 0, Dt, nD, nb);
-      nn(st, 4 * bl, 4 * br, ab1, t.Ab[i], 0, t.B[i + 1], (int64_t)ab1 * 4 * br, Dt, nD, nb, ONE, ONE);
-      apply_gate(st, Dt, nD, Dt, nD, Mk, 0, bl, br, nb, ONE, false);
-      apply_gate(st, Dt, nD, theta, 0, VM + (int64_t)s.k * 16, KK, bl, br, nb, ONE, true);
-      const int64_t sUD = (int64_t)r * 4 * br, sZ = (int64_t)4 * bl * r, sRR = (int64_t)r * r;
+      nn(st, P * bl, P * br, aa1, t.B[i], (int64_t)P * bl * aa1, t.Aa[i + 1], 0, Dt, nD, nb);
+      nn(st, P * bl, P * br, ab1, t.Ab[i], 0, t.B[i + 1], (int64_t)ab1 * P * br, Dt, nD, nb, ONE, ONE);
+      apply_gate(st, Dt, nD, Dt, nD, Mk, 0, bl, br, nb, ONE, false, NI);
+      apply_gate(st, Dt, nD, theta, 0, VM + (int64_t)s.k * 16, KK, bl, br, nb, ONE, true, NI);
+      const int64_t sUD = (int64_t)r * P * br, sZ = (int64_t)P * bl * r, sRR = (int64_t)r * r;
       cplx* UD = pool.c(sUD * nb);
-      nn(st, r, 4 * br, 4 * bl, uh, 0, Dt, nD, UD, sUD, nb);  // U^H D (uh is U^H, r x 4bl)
+      nn(st, r, P * br, P * bl, uh, 0, Dt, nD, UD, sUD, nb);  // U^H D (uh is U^H, r x 4bl)
       cplx* Z = pool.c(sZ * nb);
-      nc(st, 4 * bl, r, 4 * br, Dt, nD, vh, 0, Z, sZ, nb);  // D W = D vh^H
+      nc(st, P * bl, r, P * br, Dt, nD, vh, 0, Z, sZ, nb);  // D W = D vh^H
       cplx* nBi = dnew(sZ * nb, st);
       cplx* nBj = dnew(sUD * nb, st);
       if (s.lr) {
         // B_{i+1} = s U^H D ; B_i = s (D W - U (U^H D W))
         cplx* UDW = pool.c(sRR * nb);
-        nc(st, r, r, 4 * br, UD, sUD, vh, 0, UDW, sRR, nb);
+        nc(st, r, r, P * br, UD, sUD, vh, 0, UDW, sRR, nb);
         TN_CUDA(cudaMemcpyAsync(nBi, Z, (size_t)sZ * nb * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-        cn(st, 4 * bl, r, r, uh, 0, UDW, sRR, nBi, sZ, nb, cmsc, csc);
+        cn(st, P * bl, r, r, uh, 0, UDW, sRR, nBi, sZ, nb, cmsc, csc);
         axpby(st, nBj, UD, csc, ZERO, sUD * nb);
       } else {
         // B_i = s D W ; B_{i+1} = s (U^H D - (U^H D W) W^H)
         cplx* UDW = pool.c(sRR * nb);
-        nn(st, r, r, 4 * bl, uh, 0, Z, sZ, UDW, sRR, nb);
+        nn(st, r, r, P * bl, uh, 0, Z, sZ, UDW, sRR, nb);
         TN_CUDA(cudaMemcpyAsync(nBj, UD, (size_t)sUD * nb * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-        nn(st, r, 4 * br, r, UDW, sRR, vh, 0, nBj, sUD, nb, cmsc, csc);
+        nn(st, r, P * br, r, UDW, sRR, vh, 0, nBj, sUD, nb, cmsc, csc);
         axpby(st, nBi, Z, csc, ZERO, sZ * nb);
       }
       // chains (direction-independent; recorded / replayed per point)
@@ -1573,20 +1583,20 @@ struct Engine {
         const auto& cc = t.cache->step.at(sn);
         nAai = cc[0], nAaj = cc[1], nAbi = cc[2], nAbj = cc[3];
       } else {
-        cplx* aa2t = pool.c((int64_t)16 * aa0 * br);
-        nn(st, 4 * aa0, 4 * br, aa1, t.Aa[i], 0, t.Aa[i + 1], 0, aa2t, 0, 1);
-        apply_gate(st, aa2t, 0, aa2t, 0, Mk, 0, aa0, br, 1, ONE, false);
-        nAai = dnew((int64_t)4 * aa0 * r, st);
-        nc(st, 4 * aa0, r, 4 * br, aa2t, 0, vh, 0, nAai, 0, 1, csc);
-        nAaj = dnew((int64_t)r * 4 * br, st);
-        TN_CUDA(cudaMemcpyAsync(nAaj, vh, (size_t)r * 4 * br * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-        cplx* ab2t = pool.c((int64_t)16 * bl * ab2);
-        nn(st, 4 * bl, 4 * ab2, ab1, t.Ab[i], 0, t.Ab[i + 1], 0, ab2t, 0, 1);
-        apply_gate(st, ab2t, 0, ab2t, 0, Mk, 0, bl, ab2, 1, ONE, false);
-        nAbj = dnew((int64_t)r * 4 * ab2, st);
-        nn(st, r, 4 * ab2, 4 * bl, uh, 0, ab2t, 0, nAbj, 0, 1, csc);
-        nAbi = dnew((int64_t)4 * bl * r, st);
-        conjT_scale_cols(st, nAbi, uh, r, 4 * bl, nullptr, nullptr);
+        cplx* aa2t = pool.c((int64_t)PP * aa0 * br);
+        nn(st, P * aa0, P * br, aa1, t.Aa[i], 0, t.Aa[i + 1], 0, aa2t, 0, 1);
+        apply_gate(st, aa2t, 0, aa2t, 0, Mk, 0, aa0, br, 1, ONE, false, NI);
+        nAai = dnew((int64_t)P * aa0 * r, st);
+        nc(st, P * aa0, r, P * br, aa2t, 0, vh, 0, nAai, 0, 1, csc);
+        nAaj = dnew((int64_t)r * P * br, st);
+        TN_CUDA(cudaMemcpyAsync(nAaj, vh, (size_t)r * P * br * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+        cplx* ab2t = pool.c((int64_t)PP * bl * ab2);
+        nn(st, P * bl, P * ab2, ab1, t.Ab[i], 0, t.Ab[i + 1], 0, ab2t, 0, 1);
+        apply_gate(st, ab2t, 0, ab2t, 0, Mk, 0, bl, ab2, 1, ONE, false, NI);
+        nAbj = dnew((int64_t)r * P * ab2, st);
+        nn(st, r, P * ab2, P * bl, uh, 0, ab2t, 0, nAbj, 0, 1, csc);
+        nAbi = dnew((int64_t)P * bl * r, st);
+        conjT_scale_cols(st, nAbi, uh, r, P * bl, nullptr, nullptr);
         if (t.mode == CHAIN_RECORD) record(t, {nAai, nAaj, nAbi, nAbj});
       }
       chain_set(t, t.Aa[i], nAai, st);
@@ -1620,8 +1630,8 @@ struct Engine {
       return sn;
     }
     for (int s = 0; s < n; ++s) {
-      const int64_t eb = (int64_t)t.bd.ab[s] * 4 * t.bd.ab[s + 1];
-      const int64_t ea = (int64_t)t.bd.aa[s] * 4 * t.bd.aa[s + 1];
+      const int64_t eb = (int64_t)t.bd.ab[s] * P * t.bd.ab[s + 1];
+      const int64_t ea = (int64_t)t.bd.aa[s] * P * t.bd.aa[s + 1];
       const int64_t e = bsize(t.bd, s) * nb;
       sn.Ab[s] = dnew(eb, st);
       sn.Aa[s] = dnew(ea, st);
@@ -1644,7 +1654,7 @@ struct Engine {
     L.assign(n + 1, nullptr);
     L[0] = memo(st, pool, ell, 0, tag, 1, [&](cplx* o) { set_small(st, o, 1, ONE); });
     for (auto [s, k] : blocks(ell)) {
-      const int w = k < 0 ? 4 : 16, e = k < 0 ? s + 1 : s + 2;
+      const int w = k < 0 ? P : PP, e = k < 0 ? s + 1 : s + 2;
       L[e] = memo(st, pool, ell, e, tag, (int64_t)tb[e] * bb[e], [&](cplx* o) {
         Pool tmp(st);
         cplx* Y = tmp.c((int64_t)tb[s] * w * bb[e]);
@@ -1662,7 +1672,7 @@ struct Engine {
     auto blks = blocks(ell);
     for (int j = (int)blks.size() - 1; j >= 0; --j) {
       const int s = blks[j].first, k = blks[j].second;
-      const int w = k < 0 ? 4 : 16, e = k < 0 ? s + 1 : s + 2;
+      const int w = k < 0 ? P : PP, e = k < 0 ? s + 1 : s + 2;
       R[s] = memo(st, pool, ell, s, tag, (int64_t)bb[s] * tb[s], [&](cplx* o) {
         Pool tmp(st);
         cplx* Y = tmp.c((int64_t)bb[s] * w * tb[e]);
@@ -1709,23 +1719,23 @@ struct Engine {
     for (auto [s, k] : blks) {
       Blk& q = bk[s];
       const int e = k < 0 ? s + 1 : s + 2;
-      const int w = k < 0 ? 4 : 16;
+      const int w = k < 0 ? P : PP;
       auto mk2 = [&](int tag, const std::vector<const cplx*>& a, const std::vector<int>& bd) -> cplx* {
         if (k < 0) return const_cast<cplx*>(a[s]);
-        return memo(st, pool, ell, s, tag, (int64_t)16 * bd[s] * bd[e],
+        return memo(st, pool, ell, s, tag, (int64_t)PP * bd[s] * bd[e],
                     [&](cplx* o) { pair(st, o, a[s], 0, a[s + 1], 0, bd[s], bd[s + 1], bd[e], 1); });
       };
       auto gated = [&](int tag, const cplx* x, int X, int Y) -> cplx* {
         if (k < 0) return const_cast<cplx*>(x);
-        return memo(st, pool, ell, s, tag, (int64_t)16 * X * Y, [&](cplx* o) {
-          apply_gate(st, o, 0, x, 0, at(o_gdag) + (int64_t)k * 16, 0, X, Y, 1, ONE, false);
+        return memo(st, pool, ell, s, tag, (int64_t)PP * X * Y, [&](cplx* o) {
+          apply_gate(st, o, 0, x, 0, at(o_gdag) + (int64_t)k * 16, 0, X, Y, 1, ONE, false, NI);
         });
       };
       q.TT = mk2(1, tpv, tb);
       q.TTg = gated(2, q.TT, tb[s], tb[e]);
       if (k >= 0)
-        q.TTp = memo(st, pool, ell, s, 3, (int64_t)16 * tb[s] * tb[e],
-                     [&](cplx* o) { out_leg_split(st, o, q.TT, tb[s], tb[e]); });
+        q.TTp = memo(st, pool, ell, s, 3, (int64_t)PP * tb[s] * tb[e],
+                     [&](cplx* o) { out_leg_split(st, o, q.TT, tb[s], tb[e], NI); });
       q.BB = mk2(4, bpv, bb);
       if (!skipB) {
         q.BAaB = mk2(5, BAa, ya);
@@ -1735,8 +1745,8 @@ struct Engine {
         if (k < 0) {
           TN_CUDA(cudaMemcpyAsync(q.BBd, DBs.B[s], sz * nb * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
         } else {
-          nn(st, 4 * xb[s], 4 * ya[e], ya[s + 1], DBs.B[s], bsize(DBs.bd, s), BAa[s + 1], 0, q.BBd, sz, nb);
-          nn(st, 4 * xb[s], 4 * ya[e], xb[s + 1], BAb[s], 0, DBs.B[s + 1], bsize(DBs.bd, s + 1), q.BBd, sz, nb,
+          nn(st, P * xb[s], P * ya[e], ya[s + 1], DBs.B[s], bsize(DBs.bd, s), BAa[s + 1], 0, q.BBd, sz, nb);
+          nn(st, P * xb[s], P * ya[e], xb[s + 1], BAb[s], 0, DBs.B[s + 1], bsize(DBs.bd, s + 1), q.BBd, sz, nb,
              ONE, ONE);
         }
       }
@@ -1751,11 +1761,11 @@ struct Engine {
           TN_CUDA(cudaMemcpyAsync(q.TBd, DT.B[s], sz * nb * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
           q.TBdG = q.TBd;
         } else {
-          nn(st, 4 * ub[s], 4 * va[e], va[s + 1], DT.B[s], bsize(DT.bd, s), TAa[s + 1], 0, q.TBd, sz, nb);
-          nn(st, 4 * ub[s], 4 * va[e], ub[s + 1], TAb[s], 0, DT.B[s + 1], bsize(DT.bd, s + 1), q.TBd, sz, nb, ONE,
+          nn(st, P * ub[s], P * va[e], va[s + 1], DT.B[s], bsize(DT.bd, s), TAa[s + 1], 0, q.TBd, sz, nb);
+          nn(st, P * ub[s], P * va[e], ub[s + 1], TAb[s], 0, DT.B[s + 1], bsize(DT.bd, s + 1), q.TBd, sz, nb, ONE,
              ONE);
           q.TBdG = pool.c(sz * nb);
-          apply_gate(st, q.TBdG, sz, q.TBd, sz, at(o_gdag) + (int64_t)k * 16, 0, ub[s], va[e], nb, ONE, false);
+          apply_gate(st, q.TBdG, sz, q.TBd, sz, at(o_gdag) + (int64_t)k * 16, 0, ub[s], va[e], nb, ONE, false, NI);
         }
       }
     }
@@ -1784,7 +1794,7 @@ struct Engine {
     // ---------------- right sweep (per direction)
     for (int j = (int)blks.size() - 1; j >= 0; --j) {
       const int s = blks[j].first, k = blks[j].second;
-      const int w = k < 0 ? 4 : 16, e = k < 0 ? s + 1 : s + 2;
+      const int w = k < 0 ? P : PP, e = k < 0 ? s + 1 : s + 2;
       Blk& q = bk[s];
       const cplx* R0e = at(o_R[ell][e]);
       Pool rp(st);  // block temporaries
@@ -1796,15 +1806,15 @@ struct Engine {
         dRV[s] = pool.c((int64_t)bb[s] * tb[s] * nb);
         nc(st, bb[s], tb[s], w * tb[e], Y, sY, q.TTg, 0, dRV[s], (int64_t)bb[s] * tb[s], nb);
         if (k >= 0) {  // (V Y0) TT^H = sum_ac V[a,c] Y0_c TT_a^H: 16 shared products, one K=16 GEMM
-          const int64_t sq = (int64_t)bb[s] * tb[s], sy = (int64_t)bb[s] * 4 * tb[e], stt = (int64_t)tb[s] * 4 * tb[e];
+          const int64_t sq = (int64_t)bb[s] * tb[s], sy = (int64_t)bb[s] * NI2 * tb[e], stt = (int64_t)tb[s] * NI2 * tb[e];
           cplx* Q = memo(st, rp, ell, s, 60, 16 * sq, [&](cplx* o) {
             Pool tmp(st);
             cplx* Y0 = tmp.c(sY);
             nn(st, w * bb[s], tb[e], bb[e], q.BB, 0, R0e, 0, Y0, 0, 1);
             cplx* Y0p = tmp.c(sY);
-            out_leg_split(st, Y0p, Y0, bb[s], tb[e]);
+            out_leg_split(st, Y0p, Y0, bb[s], tb[e], NI);
             for (int a = 0; a < 4; ++a)  // Q[a*4+c] = Y0p[c] TTp[a]^H
-              nc(st, bb[s], tb[s], 4 * tb[e], Y0p, sy, q.TTp + a * stt, 0, o + (int64_t)a * 4 * sq, sq, 4);
+              nc(st, bb[s], tb[s], NI2 * tb[e], Y0p, sy, q.TTp + a * stt, 0, o + (int64_t)a * 4 * sq, sq, 4);
           });
           mm(st, 'N', 'N', nb, (int)sq, 16, ONE, Vd + (int64_t)k * 16, KK, 0, Q, sq, 0, ONE, dRV[s], sq, 0, 1);
         }
@@ -1840,7 +1850,7 @@ struct Engine {
     cplx* dLB = skipB ? nullptr : zero_owned(1);
     cplx* dLT = skipT ? nullptr : zero_owned(1);
     for (auto [s, k] : blks) {
-      const int w = k < 0 ? 4 : 16, e = k < 0 ? s + 1 : s + 2;
+      const int w = k < 0 ? P : PP, e = k < 0 ? s + 1 : s + 2;
       Blk& q = bk[s];
       Pool bpool(st);  // block temporaries
       const cplx* L0s = at(o_L[ell][s]);
@@ -1875,42 +1885,42 @@ struct Engine {
         // directions use Wt = Theta_top R^H (once per block) so that
         // sum conj(top) (Y R) = sum conj(Wt) Y  -- no per-direction Y R product.
         {
-          cplx* Wt = memo(st, bpool, ell, s, 72, (int64_t)16 * tb[s] * bb[e],   // TT R0^H
-                          [&](cplx* o) { nc(st, 16 * tb[s], bb[e], tb[e], q.TT, 0, R0e, 0, o, 0, 1); });
-          extract_env(st, HT + (int64_t)k * 16, KK, Wt, 0, YV, sYV, tb[s], bb[e], nb, ONE);
+          cplx* Wt = memo(st, bpool, ell, s, 72, (int64_t)PP * tb[s] * bb[e],   // TT R0^H
+                          [&](cplx* o) { nc(st, PP * tb[s], bb[e], tb[e], q.TT, 0, R0e, 0, o, 0, 1); });
+          extract_env(st, HT + (int64_t)k * 16, KK, Wt, 0, YV, sYV, tb[s], bb[e], nb, ONE, NI);
         }
         {  // per-direction right environments: Z = Y0 dRV (+ LBb BAbB dRB)
-          const int64_t sZ = (int64_t)16 * tb[s] * tb[e];
+          const int64_t sZ = (int64_t)PP * tb[s] * tb[e];
           cplx* Z = bpool.c(sZ * nb);
-          nn(st, 16 * tb[s], tb[e], bb[e], Y0, 0, dRV[e], (int64_t)bb[e] * tb[e], Z, sZ, nb);
+          nn(st, PP * tb[s], tb[e], bb[e], Y0, 0, dRV[e], (int64_t)bb[e] * tb[e], Z, sZ, nb);
           if (!skipB) {
-            cplx* LBA = memo(st, bpool, ell, s, 73, (int64_t)16 * tb[s] * xb[e],
-                             [&](cplx* o) { nn(st, tb[s], 16 * xb[e], xb[s], LBb[s], 0, q.BAbB, 0, o, 0, 1); });
-            nn(st, 16 * tb[s], tb[e], xb[e], LBA, 0, dRB[e], (int64_t)xb[e] * tb[e], Z, sZ, nb, ONE, ONE);
+            cplx* LBA = memo(st, bpool, ell, s, 73, (int64_t)PP * tb[s] * xb[e],
+                             [&](cplx* o) { nn(st, tb[s], PP * xb[e], xb[s], LBb[s], 0, q.BAbB, 0, o, 0, 1); });
+            nn(st, PP * tb[s], tb[e], xb[e], LBA, 0, dRB[e], (int64_t)xb[e] * tb[e], Z, sZ, nb, ONE, ONE);
           }
-          extract_env(st, HT + (int64_t)k * 16, KK, q.TT, 0, Z, sZ, tb[s], tb[e], nb, ONE);
+          extract_env(st, HT + (int64_t)k * 16, KK, q.TT, 0, Z, sZ, tb[s], tb[e], nb, ONE, NI);
         }
         if (!skipB) {  // (dLB BAaB + LBb BBd) RBa  ->  Wt = TT RBa^H
-          cplx* Wt = memo(st, bpool, ell, s, 74, (int64_t)16 * tb[s] * ya[e],
-                          [&](cplx* o) { nc(st, 16 * tb[s], ya[e], tb[e], q.TT, 0, RBa[e], 0, o, 0, 1); });
-          extract_env(st, HT + (int64_t)k * 16, KK, Wt, 0, YB, sYB, tb[s], ya[e], nb, ONE);
+          cplx* Wt = memo(st, bpool, ell, s, 74, (int64_t)PP * tb[s] * ya[e],
+                          [&](cplx* o) { nc(st, PP * tb[s], ya[e], tb[e], q.TT, 0, RBa[e], 0, o, 0, 1); });
+          extract_env(st, HT + (int64_t)k * 16, KK, Wt, 0, YB, sYB, tb[s], ya[e], nb, ONE, NI);
         }
         if (!skipT) {
           {  // top TAaB with (dLT BB) RTa  ->  Wt = TAaB RTa^H
-            cplx* Wt = memo(st, bpool, ell, s, 75, (int64_t)16 * va[s] * bb[e],
-                            [&](cplx* o) { nc(st, 16 * va[s], bb[e], va[e], q.TAaB, 0, RTa[e], 0, o, 0, 1); });
-            extract_env(st, HT + (int64_t)k * 16, KK, Wt, 0, YT, sYT, va[s], bb[e], nb, ONE);
+            cplx* Wt = memo(st, bpool, ell, s, 75, (int64_t)PP * va[s] * bb[e],
+                            [&](cplx* o) { nc(st, PP * va[s], bb[e], va[e], q.TAaB, 0, RTa[e], 0, o, 0, 1); });
+            extract_env(st, HT + (int64_t)k * 16, KK, Wt, 0, YT, sYT, va[s], bb[e], nb, ONE, NI);
           }
           // per-dir top TBd with shared (LTb BB) RTa
-          const int64_t sZ3 = (int64_t)16 * ub[s] * va[e];
+          const int64_t sZ3 = (int64_t)PP * ub[s] * va[e];
           cplx* Z3 = memo(st, bpool, ell, s, 76, sZ3,
-                          [&](cplx* o) { nn(st, 16 * ub[s], va[e], bb[e], YT0, 0, RTa[e], 0, o, 0, 1); });
-          extract_env(st, HT + (int64_t)k * 16, KK, q.TBd, sZ3, Z3, 0, ub[s], va[e], nb, ONE);
+                          [&](cplx* o) { nn(st, PP * ub[s], va[e], bb[e], YT0, 0, RTa[e], 0, o, 0, 1); });
+          extract_env(st, HT + (int64_t)k * 16, KK, q.TBd, sZ3, Z3, 0, ub[s], va[e], nb, ONE, NI);
           // top TAbB with (LTb BB) dRT
-          const int64_t sZ4 = (int64_t)16 * ub[s] * ub[e];
+          const int64_t sZ4 = (int64_t)PP * ub[s] * ub[e];
           cplx* Z4 = bpool.c(sZ4 * nb);
-          nn(st, 16 * ub[s], ub[e], bb[e], YT0, 0, dRT[e], (int64_t)bb[e] * ub[e], Z4, sZ4, nb);
-          extract_env(st, HT + (int64_t)k * 16, KK, q.TAbB, 0, Z4, sZ4, ub[s], ub[e], nb, ONE);
+          nn(st, PP * ub[s], ub[e], bb[e], YT0, 0, dRT[e], (int64_t)bb[e] * ub[e], Z4, sZ4, nb);
+          extract_env(st, HT + (int64_t)k * 16, KK, q.TAbB, 0, Z4, sZ4, ub[s], ub[e], nb, ONE, NI);
         }
       }
       // ---- left updates
@@ -1918,13 +1928,13 @@ struct Engine {
         cplx* nL = dnew((int64_t)tb[e] * bb[e] * nb, st);
         cn(st, tb[e], bb[e], w * tb[s], q.TTg, 0, YV, sYV, nL, (int64_t)tb[e] * bb[e], nb);
         if (k >= 0) {  // TT^H (V Y0) = sum_ac V[a,c] TT_a^H Y0_c: 16 shared products, one K=16 GEMM
-          const int64_t sp = (int64_t)tb[e] * bb[e], sy = (int64_t)tb[s] * 4 * bb[e], stt = (int64_t)tb[s] * 4 * tb[e];
+          const int64_t sp = (int64_t)tb[e] * bb[e], sy = (int64_t)tb[s] * NI2 * bb[e], stt = (int64_t)tb[s] * NI2 * tb[e];
           cplx* Pm = memo(st, bpool, ell, s, 77, 16 * sp, [&](cplx* o) {
             Pool tmp(st);
             cplx* Y0p = tmp.c(sYV);
-            out_leg_split(st, Y0p, Y0, tb[s], bb[e]);
+            out_leg_split(st, Y0p, Y0, tb[s], bb[e], NI);
             for (int a = 0; a < 4; ++a)  // P[a*4+c] = TTp[a]^H Y0p[c]
-              cn(st, tb[e], bb[e], 4 * tb[s], q.TTp + a * stt, 0, Y0p, sy, o + (int64_t)a * 4 * sp, sp, 4);
+              cn(st, tb[e], bb[e], NI2 * tb[s], q.TTp + a * stt, 0, Y0p, sy, o + (int64_t)a * 4 * sp, sp, 4);
           });
           mm(st, 'N', 'N', nb, (int)sp, 16, ONE, Vd + (int64_t)k * 16, KK, 0, Pm, sp, 0, ONE, nL, sp, 0, 1);
         }
@@ -2050,6 +2060,14 @@ struct Engine {
     }
     graphs.clear();
     cudaDeviceGraphMemTrim(device);
+  }
+
+  // The inputs of the stored point change: nothing of it may be reused.
+  void invalidate(cudaStream_t st) {
+    primal_valid = false;
+    ti_valid = false;
+    drop_graphs(st);
+    drop_chain_cache(st);
   }
 
   // tn_hvp_trim_memory: drop the per-point caches and graphs (rebuilt by the
@@ -2250,6 +2268,21 @@ void engine_primal_copy(tn_hvp_ctx* ctx, void* buf, size_t bytes, int into_ctx, 
     if (!e.primal_valid) throw StateError("tn_hvp_primal_copy: no valid primal pass to export");
     TN_CUDA(cudaMemcpyAsync(buf, e.arena, bytes, cudaMemcpyDeviceToDevice, st));
   }
+}
+void engine_set_product_state(tn_hvp_ctx* ctx, const cplx* psi, cudaStream_t st) {
+  Engine& e = ctx->e;
+  if (e.P != 2) throw std::invalid_argument("tn_hvp_set_product_state: the context is in operator mode (site_dim 4)");
+  TN_CUDA(cudaSetDevice(e.device));
+  e.invalidate(st);
+  TN_CUDA(cudaMemcpyAsync(e.d_init, psi, sizeof(cplx) * 2 * e.n, cudaMemcpyDeviceToDevice, st));
+}
+void engine_set_reference(tn_hvp_ctx* ctx, const cplx* ref, cudaStream_t st) {
+  Engine& e = ctx->e;
+  TN_CUDA(cudaSetDevice(e.device));
+  e.invalidate(st);
+  size_t el = 0;
+  for (int s = 0; s < e.n; ++s) el += (size_t)e.ref_bonds[s] * e.P * e.ref_bonds[s + 1];
+  TN_CUDA(cudaMemcpyAsync(e.ref, ref, sizeof(cplx) * el, cudaMemcpyDeviceToDevice, st));
 }
 void engine_trim_memory(tn_hvp_ctx* ctx, cudaStream_t st) {
   TN_CUDA(cudaSetDevice(ctx->e.device));

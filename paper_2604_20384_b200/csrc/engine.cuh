@@ -25,6 +25,8 @@ void engine_primal_blob(tn_hvp_ctx* ctx, void** ptr, size_t* bytes);
 void engine_primal_imported(tn_hvp_ctx* ctx, const cplx* gates, cudaStream_t st);
 void engine_primal_copy(tn_hvp_ctx* ctx, void* buf, size_t bytes, int into_ctx, cudaStream_t st);
 void engine_trim_memory(tn_hvp_ctx* ctx, cudaStream_t st);
+void engine_set_product_state(tn_hvp_ctx* ctx, const cplx* psi, cudaStream_t st);
+void engine_set_reference(tn_hvp_ctx* ctx, const cplx* ref, cudaStream_t st);
 void engine_work(tn_hvp_ctx* ctx, double* per_dir, double* primal);
 void engine_query(const tn_hvp_config& cfg, const int32_t* ref_bonds, size_t* primal_bytes, size_t* work_bytes,
                   size_t* per_dir_bytes);

@@ -20,12 +20,16 @@ inline int nblocks(int64_t n, int per = TPB) {
 }
 
 // ---------------------------------------------------------------- gates --
-// x: [batch][X][4][4][Y] viewed as [X][o1][i1][o2][i2][Y]; out[b] = gate[b] x[b]
+// Site physical index p = out * NI + in: NI = 2 for operators (MPO sites,
+// p = 2 out + in), NI = 1 for states (MPS sites, p = out).
+// x: [batch][X][2NI][2NI][Y] viewed as [X][o1][i1][o2][i2][Y]; out[b] = gate[b] x[b]
 // on the out legs (o1 o2); gate stride sg in complex elements (0 = shared).
+template <int NI>
 __global__ void apply_gate_kernel(cplx* out, int64_t sout, const cplx* x, int64_t sx,
                                   const cplx* __restrict__ gate, int64_t sg, int X, int Y, int batch,
                                   cplx alpha, int accumulate) {
-  const int64_t per = (int64_t)X * 4 * Y;  // (x, i1, i2, y) combos per batch entry
+  constexpr int P = 2 * NI;
+  const int64_t per = (int64_t)X * NI * NI * Y;  // (x, i1, i2, y) combos per batch entry
   const int64_t total = per * batch;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
@@ -33,18 +37,18 @@ __global__ void apply_gate_kernel(cplx* out, int64_t sout, const cplx* x, int64_
     int64_t r = idx % per;
     const int y = (int)(r % Y);
     r /= Y;
-    const int i12 = (int)(r % 4);
-    const int xx = (int)(r / 4);
-    const int i1 = i12 >> 1, i2 = i12 & 1;
-    const cplx* xb = x + b * sx + (int64_t)xx * 16 * Y;
+    const int i12 = (int)(r % (NI * NI));
+    const int xx = (int)(r / (NI * NI));
+    const int i1 = i12 / NI, i2 = i12 % NI;
+    const cplx* xb = x + b * sx + (int64_t)xx * P * P * Y;
     const cplx* g = gate + b * sg;
     cplx in[4];
 #pragma unroll
     for (int o = 0; o < 4; ++o) {
       const int o1 = o >> 1, o2 = o & 1;
-      in[o] = xb[((int64_t)((o1 * 2 + i1) * 4 + (o2 * 2 + i2))) * Y + y];
+      in[o] = xb[((int64_t)((o1 * NI + i1) * P + (o2 * NI + i2))) * Y + y];
     }
-    cplx* ob = out + b * sout + (int64_t)xx * 16 * Y;
+    cplx* ob = out + b * sout + (int64_t)xx * P * P * Y;
 #pragma unroll
     for (int o = 0; o < 4; ++o) {
       cplx acc = make_double2(0, 0);
@@ -52,13 +56,12 @@ __global__ void apply_gate_kernel(cplx* out, int64_t sout, const cplx* x, int64_
       for (int c = 0; c < 4; ++c) acc = cadd(acc, cmul(g[o * 4 + c], in[c]));
       acc = cmul(alpha, acc);
       const int o1 = o >> 1, o2 = o & 1;
-      cplx* d = ob + ((int64_t)((o1 * 2 + i1) * 4 + (o2 * 2 + i2))) * Y + y;
+      cplx* d = ob + ((int64_t)((o1 * NI + i1) * P + (o2 * NI + i2))) * Y + y;
       *d = accumulate ? cadd(*d, acc) : acc;
     }
   }
 }
 
-// b == 0: y is write-only (BLAS convention; y may be uninitialised, 0 * NaN = NaN)
 __global__ void axpby_kernel(cplx* __restrict__ y, const cplx* __restrict__ x, cplx a, cplx b, int64_t n) {
   const bool read_y = b.x != 0.0 || b.y != 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -74,26 +77,28 @@ __global__ void scale_kernel(cplx* __restrict__ y, const double* __restrict__ s,
 // Gate-environment extraction:
 // E[b][(o1 o2),(c1 c2)] += alpha * sum_{t,i1,i2,u} conj(top[t,o1 i1,o2 i2,u]) z[b][t,c1 i1,c2 i2,u]
 // top: [T][4][4][U] (shared, stride stop per batch, 0 allowed); z: [batch][T][4][4][U].
+template <int NI>
 __global__ void extract_env_kernel(double* __restrict__ part, const cplx* __restrict__ top, int64_t stop,
                                    const cplx* __restrict__ z, int64_t sz, int T, int U) {
+  constexpr int P = 2 * NI;
   const int b = blockIdx.y;
   const cplx* tp = top + b * stop;
   const cplx* zb = z + b * sz;
   double acc[16][2];
 #pragma unroll
   for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = 0.0;
-  const int64_t pairs = (int64_t)T * U * 4;  // (t, u, i1, i2)
+  const int64_t pairs = (int64_t)T * U * NI * NI;  // (t, u, i1, i2)
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < pairs;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    const int i12 = (int)(idx & 3);
-    const int64_t tu = idx >> 2;
+    const int i12 = (int)(idx % (NI * NI));
+    const int64_t tu = idx / (NI * NI);
     const int u = (int)(tu % U), t = (int)(tu / U);
-    const int i1 = i12 >> 1, i2 = i12 & 1;
+    const int i1 = i12 / NI, i2 = i12 % NI;
     cplx tv[4], zv[4];
 #pragma unroll
     for (int o = 0; o < 4; ++o) {
       const int o1 = o >> 1, o2 = o & 1;
-      const int64_t off = (((int64_t)t * 4 + (o1 * 2 + i1)) * 4 + (o2 * 2 + i2)) * U + u;
+      const int64_t off = (((int64_t)t * P + (o1 * NI + i1)) * P + (o2 * NI + i2)) * U + u;
       tv[o] = tp[off];
       zv[o] = zb[off];
     }
@@ -279,11 +284,15 @@ __global__ void hessian_kernel(int K, int batch, const cplx* __restrict__ G, con
 }  // namespace
 
 void apply_gate(cudaStream_t st, cplx* out, int64_t sout, const cplx* x, int64_t sx, const cplx* gate, int64_t sg,
-                int X, int Y, int batch, cplx alpha, bool accumulate) {
-  const int64_t total = (int64_t)X * 4 * Y * batch;
+                int X, int Y, int batch, cplx alpha, bool accumulate, int ni) {
+  const int64_t total = (int64_t)X * ni * ni * Y * batch;
   if (total == 0) return;
-  apply_gate_kernel<<<nblocks(total), TPB, 0, st>>>(out, sout, x, sx, gate, sg, X, Y, batch, alpha,
-                                                    accumulate ? 1 : 0);
+  if (ni == 2)
+    apply_gate_kernel<2><<<nblocks(total), TPB, 0, st>>>(out, sout, x, sx, gate, sg, X, Y, batch, alpha,
+                                                         accumulate ? 1 : 0);
+  else
+    apply_gate_kernel<1><<<nblocks(total), TPB, 0, st>>>(out, sout, x, sx, gate, sg, X, Y, batch, alpha,
+                                                         accumulate ? 1 : 0);
   TN_CUDA(cudaGetLastError());
   count_launch();
 }
@@ -303,8 +312,8 @@ void scale_by(cudaStream_t st, cplx* y, const double* s, double pw, int64_t n) {
 }
 
 void extract_env(cudaStream_t st, cplx* E, int64_t sE, const cplx* top, int64_t stop, const cplx* z, int64_t sz,
-                 int T, int U, int batch, cplx alpha) {
-  const int64_t pairs = (int64_t)T * U * 4;
+                 int T, int U, int batch, cplx alpha, int ni) {
+  const int64_t pairs = (int64_t)T * U * ni * ni;
   int bx = (int)((pairs + TPB * 8 - 1) / (TPB * 8));
   if (bx < 1) bx = 1;
   if (bx > 64) bx = 64;
@@ -312,7 +321,10 @@ void extract_env(cudaStream_t st, cplx* E, int64_t sE, const cplx* top, int64_t 
   part = (double*)dalloc(sizeof(double) * 32 * bx * (size_t)batch, st);
   if (std::getenv("TN_POISON")) TN_CUDA(cudaMemsetAsync(part, 0xFF, sizeof(double) * 32 * bx * (size_t)batch, st));
   dim3 grid(bx, batch);
-  extract_env_kernel<<<grid, TPB, 0, st>>>(part, top, stop, z, sz, T, U);
+  if (ni == 2)
+    extract_env_kernel<2><<<grid, TPB, 0, st>>>(part, top, stop, z, sz, T, U);
+  else
+    extract_env_kernel<1><<<grid, TPB, 0, st>>>(part, top, stop, z, sz, T, U);
   TN_CUDA(cudaGetLastError());
   count_launch();
   extract_finish_kernel<<<batch, 32, 0, st>>>(E, sE, part, bx, alpha);
@@ -458,17 +470,19 @@ __global__ void s_from_norms_kernel(const double* __restrict__ nrm, const double
 }
 
 // dst[(o1 o2)][x][i1][i2][y] = src[x][(o1 i1)][(o2 i2)][y]  (split off the out legs)
+template <int NI>
 __global__ void out_leg_split_kernel(cplx* __restrict__ dst, const cplx* __restrict__ src, int X, int Y) {
-  const int64_t n = (int64_t)X * 16 * Y;
+  constexpr int P = 2 * NI;
+  const int64_t n = (int64_t)X * 4 * NI * NI * Y;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
     const int y = (int)(idx % Y);
     int64_t r = idx / Y;
-    const int i12 = (int)(r % 4);
-    r /= 4;
+    const int i12 = (int)(r % (NI * NI));
+    r /= NI * NI;
     const int x = (int)(r % X);
     const int a = (int)(r / X);
-    const int o1 = a >> 1, o2 = a & 1, i1 = i12 >> 1, i2 = i12 & 1;
-    dst[idx] = src[(((int64_t)x * 4 + (o1 * 2 + i1)) * 4 + (o2 * 2 + i2)) * Y + y];
+    const int o1 = a >> 1, o2 = a & 1, i1 = i12 / NI, i2 = i12 % NI;
+    dst[idx] = src[(((int64_t)x * P + (o1 * NI + i1)) * P + (o2 * NI + i2)) * Y + y];
   }
 }
 
@@ -638,10 +652,13 @@ void s_from_norms(cudaStream_t st, const double* nrm, const double* S, int mn, i
   count_launch();
 }
 
-void out_leg_split(cudaStream_t st, cplx* dst, const cplx* src, int X, int Y) {
-  const int64_t n = (int64_t)X * 16 * Y;
+void out_leg_split(cudaStream_t st, cplx* dst, const cplx* src, int X, int Y, int ni) {
+  const int64_t n = (int64_t)X * 4 * ni * ni * Y;
   if (!n) return;
-  out_leg_split_kernel<<<nblocks(n), TPB, 0, st>>>(dst, src, X, Y);
+  if (ni == 2)
+    out_leg_split_kernel<2><<<nblocks(n), TPB, 0, st>>>(dst, src, X, Y);
+  else
+    out_leg_split_kernel<1><<<nblocks(n), TPB, 0, st>>>(dst, src, X, Y);
   TN_CUDA(cudaGetLastError());
   count_launch();
 }
@@ -804,3 +821,4 @@ void check_tangent(cudaStream_t st, int K, int batch, const cplx* G, const cplx*
   count_launch();
 }
 }  // namespace tn
+

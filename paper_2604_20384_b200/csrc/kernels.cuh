@@ -3,15 +3,17 @@
 #include "common.cuh"
 
 namespace tn {
+// Site physical index p = out * ni + in: ni = 2 for operator (MPO) sites,
+// ni = 1 for state (MPS) sites.
 // out[b] = alpha * gate[b] (x) I_in applied to the out legs of x[b] viewed as
-// [X][4][4][Y] (p = 2 out + in); accumulate adds to out.  In-place allowed.
+// [X][2ni][2ni][Y]; accumulate adds to out.  In-place allowed.
 void apply_gate(cudaStream_t st, cplx* out, int64_t sout, const cplx* x, int64_t sx, const cplx* gate, int64_t sg,
-                int X, int Y, int batch, cplx alpha, bool accumulate);
+                int X, int Y, int batch, cplx alpha, bool accumulate, int ni = 2);
 void axpby(cudaStream_t st, cplx* y, const cplx* x, cplx a, cplx b, int64_t n);   // y = a x + b y
 void scale_by(cudaStream_t st, cplx* y, const double* s, double pw, int64_t n);    // y *= s^pw (device s)
 // E[b] += alpha * sum conj(top[t,(o1 i1),(o2 i2),u]) z[b][t,(c1 i1),(c2 i2),u]
 void extract_env(cudaStream_t st, cplx* E, int64_t sE, const cplx* top, int64_t stop, const cplx* z, int64_t sz,
-                 int T, int U, int batch, cplx alpha);
+                 int T, int U, int batch, cplx alpha, int ni = 2);
 void project(cudaStream_t st, int K, int batch, const cplx* G, const cplx* in, cplx* out);
 void gradient_post(cudaStream_t st, int K, const cplx* G, const cplx* E, const double* scal, cplx* grad_f,
                    cplx* grad_R);
@@ -42,7 +44,7 @@ void eig_to_svd(cudaStream_t st, cplx* uhf, double* S, const cplx* W, const doub
 // diag[1] = min(diag[1], relative gap (S[r-1]-S[r])/S[0]), diag[2] = max(diag[2], |log10 s|)
 void s_from_norms(cudaStream_t st, const double* nrm, const double* S, int mn, int r, double* s_out, double* diag);
 // dst[(o1 o2)][x][i1 i2][y] = src[x][(o1 i1)][(o2 i2)][y]
-void out_leg_split(cudaStream_t st, cplx* dst, const cplx* src, int X, int Y);
+void out_leg_split(cudaStream_t st, cplx* dst, const cplx* src, int X, int Y, int ni = 2);
 // *acc = max(*acc, |*info|)  (cuSOLVER status accumulation)
 void info_accum(cudaStream_t st, int* acc, const int* info);
 // dst = conj(src), n elements
@@ -85,3 +87,4 @@ namespace tn {
 void check_unitary(cudaStream_t st, int K, const cplx* G, double* res);
 void check_tangent(cudaStream_t st, int K, int batch, const cplx* G, const cplx* V, double* res);
 }  // namespace tn
+
