@@ -348,7 +348,13 @@ def main():
     B = args.batch or cfg.batch                       # directions per step (all ranks together)
     mb = args.max_batch or SUB_BATCH[cfg.cid]
     K = C.num_gates(cfg.n, cfg.depth, cfg.first_offset)
-    ref = C.reference_mpo(cfg, device=dev)
+    # N4: the reference MPO is built on the GPU by the library's TEBD (tn_mpo_tebd)
+    from paper_2604_20384_b200.api import mpo_tebd
+    torch.cuda.synchronize()
+    t_ref0 = time.time()
+    ref = mpo_tebd(cfg.n, C.reference_layers(cfg), cfg.chi)
+    torch.cuda.synchronize()
+    t_ref = time.time() - t_ref0
     Gnp = C.haar_gates(cfg.cid, K)
     Vnp = C.tangent_directions(cfg.cid, Gnp, B)
     G = torch.tensor(Gnp, device=dev)
@@ -488,7 +494,9 @@ def main():
                    "step": ("parallel.sharded_step" if world > 1 else
                             "tn_hvp_environments + tn_hvp_apply" if args.unfused else
                             "tn_hvp_step (fused: first sub-batch's forward tangents overlap the primal pass)"),
-                   "l2": "working set (primal store, tangent caches: GBs) > 126 MB L2; no flush"},
+                   "l2": "working set (primal store, tangent caches: GBs) > 126 MB L2; no flush",
+                   "reference": f"tn_mpo_tebd (library TEBD of the {cfg.order}-order Trotter circuit, N4), "
+                                f"built in {t_ref:.1f} s before timing"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "traffic_algorithmic_bytes_per_launch": traffic_alg,

@@ -209,6 +209,28 @@ tn_status tn_hvp_primal_imported(tn_hvp_ctx* ctx, const void* gates, void* strea
 tn_status tn_hvp_set_product_state(tn_hvp_ctx* ctx, const void* psi, void* stream);
 tn_status tn_hvp_set_reference(tn_hvp_ctx* ctx, const void* ref, void* stream);
 
+/* ---- N4: GPU-side reference construction (PAPER.md:589,
+ * :601; reading X11) ------------------------------------------------------------
+ * TEBD of a gate sequence (e.g. a 1st/2nd/4th-order Trotter circuit) on the
+ * operator I/2^{n/2} with the library's primal kernels: gate g (DEVICE
+ * complex128 gates[g][4][4]) acts on the OUT legs of sites (sites[g],
+ * sites[g]+1) (HOST int32), each split keeps r = min(chi, #{sigma_j >
+ * max(tol, 1e-7) sigma_1}) singular values rescaled to the pre-truncation norm;
+ * the result is right-canonical, centre at site 0, unit Frobenius norm -- the
+ * reference MPO U_ref / 2^{n/2} that tn_hvp_setup takes.  bonds_out: HOST
+ * int32[n+1]; out: DEVICE, capacity out_capacity complex128 elements (n 16 chi^2
+ * always suffices), site tensors [b][4][b'] packed.  Synchronises the stream
+ * once per gate (data-dependent split sizes).  TN_EINVAL on a bad site or too
+ * small a capacity. */
+tn_status tn_mpo_tebd(int32_t n_sites, int32_t n_gates, const int32_t* sites, const void* gates, int32_t chi,
+                      double tol, int32_t device, int32_t* bonds_out, void* out, size_t out_capacity, void* stream);
+
+/* Cap, in bytes, on the per-point caches (tangent chains + layer-HVP memo)
+ * of this context; 0 (default) = automatic (chains within half, memo within a
+ * third of the free memory at the first apply).  For several contexts sharing
+ * one device (N1 samples).  Takes effect at the next primal pass. */
+tn_status tn_hvp_set_cache_budget(tn_hvp_ctx* ctx, size_t bytes);
+
 /* Release the per-point caches and CUDA graphs (the next apply rebuilds them)
  * and return the library pool's unused device memory to the device, e.g.
  * before the caller allocates large buffers of its own.  Synchronises. */

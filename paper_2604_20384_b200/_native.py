@@ -19,7 +19,8 @@ EXPORTS = ["tn_hvp_num_gates", "tn_hvp_setup", "tn_hvp_environments", "tn_hvp_ap
            "tn_hvp_work", "tn_retract", "tn_tangent_dot", "tn_tangent_axpby", "tn_hvp_primal_copy",
            "tn_hvp_launch_count", "tn_gemm_profile", "tn_pauli_basis", "tn_pauli_coords", "tn_sym_eig",
            "tn_hvp_ti_environments", "tn_hvp_ti_apply", "tn_hvp_step", "tn_hvp_query", "tn_hvp_trim_memory",
-           "tn_hvp_set_product_state", "tn_hvp_set_reference",
+           "tn_hvp_set_product_state", "tn_hvp_set_reference", "tn_mpo_tebd",
+           "tn_hvp_set_cache_budget",
            "tn_hvp_destroy", "tn_hvp_last_error"]
 TN_C128, TN_C64 = 0, 1
 TN_CHECK_UNITARY, TN_CHECK_TANGENT = 1, 2
@@ -62,6 +63,9 @@ def lib():
         L.tn_hvp_trim_memory.argtypes = [vp, vp]
         L.tn_hvp_set_product_state.argtypes = [vp, vp, vp]
         L.tn_hvp_set_reference.argtypes = [vp, vp, vp]
+        L.tn_hvp_set_cache_budget.argtypes = [vp, C.c_size_t]
+        L.tn_mpo_tebd.argtypes = [i32, i32, C.POINTER(i32), vp, i32, C.c_double, i32, C.POINTER(i32), vp,
+                                  C.c_size_t, vp]
         L.tn_hvp_environments.argtypes = [vp, vp, vp, vp, vp]
         L.tn_hvp_apply.argtypes = [vp, i32, vp, vp, vp, vp]
         L.tn_hvp_gradient_T.argtypes = [vp, vp, vp]
@@ -85,7 +89,7 @@ def lib():
         for name in ("tn_retract", "tn_tangent_dot", "tn_tangent_axpby", "tn_hvp_primal_copy", "tn_pauli_basis",
                      "tn_pauli_coords", "tn_sym_eig", "tn_hvp_ti_environments", "tn_hvp_ti_apply",
                      "tn_hvp_step", "tn_hvp_query", "tn_hvp_trim_memory", "tn_hvp_set_product_state",
-                     "tn_hvp_set_reference"):
+                     "tn_hvp_set_reference", "tn_mpo_tebd", "tn_hvp_set_cache_budget"):
             getattr(L, name).restype = C.c_int
         L.tn_hvp_launch_count.argtypes = []
         L.tn_hvp_launch_count.restype = C.c_int64
@@ -247,3 +251,16 @@ def tn_hvp_ti_apply(ctx, batch, v_ptr, hess_ptr, stream):
 def tn_hvp_step(ctx, gates_ptr, scalars_ptr, grad_R_ptr, batch, dirs_ptr, hess_ptr, aux_ptr, stream):
     check(lib().tn_hvp_step(ctx, C.c_void_p(gates_ptr), C.c_void_p(scalars_ptr), C.c_void_p(grad_R_ptr), batch,
                             C.c_void_p(dirs_ptr), C.c_void_p(hess_ptr), C.c_void_p(aux_ptr), C.c_void_p(stream)), ctx)
+
+
+def tn_mpo_tebd(n, sites, gates_ptr, chi, tol, device, out_ptr, capacity, stream):
+    """-> bonds (list of n+1)."""
+    sarr = (C.c_int32 * max(len(sites), 1))(*sites)
+    barr = (C.c_int32 * (n + 1))()
+    check(lib().tn_mpo_tebd(n, len(sites), sarr, C.c_void_p(gates_ptr), chi, tol, device, barr,
+                            C.c_void_p(out_ptr), C.c_size_t(capacity), C.c_void_p(stream)))
+    return list(barr)
+
+
+def tn_hvp_set_cache_budget(ctx, nbytes):
+    check(lib().tn_hvp_set_cache_budget(ctx, C.c_size_t(int(nbytes))), ctx)

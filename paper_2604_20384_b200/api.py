@@ -69,6 +69,10 @@ class HVPEngine:
         N.tn_hvp_set_reference(self.ctx, packed.data_ptr(), _stream())
         torch.cuda.current_stream().synchronize()      # packed is a temporary
 
+    def set_cache_budget(self, nbytes: int):
+        """Cap on this context's per-point caches (0 = automatic)."""
+        N.tn_hvp_set_cache_budget(self.ctx, nbytes)
+
     def trim_memory(self):
         """Drop per-point caches / graphs and return the library pool's unused memory."""
         N.tn_hvp_trim_memory(self.ctx, _stream())
@@ -152,6 +156,27 @@ class HVPEngine:
     def work(self):
         """(complex MACs per direction of the last apply, complex MACs of the last primal pass)."""
         return N.tn_hvp_work(self.ctx)
+
+
+def mpo_tebd(n: int, layers, chi: int, tol: float = 1e-14, device=None):
+    """N4: the reference MPO U_ref/2^{n/2} of a gate sequence built on the GPU by
+    tn_mpo_tebd.  layers: list of layers, each a list of (left site, 4x4 gate)
+    applied in order (tn_inputs.models.trotter_layers).  -> list of n device
+    tensors [b][4][b'] (right-canonical, centre at site 0, unit norm)."""
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    sites = [int(i) for ly in layers for i, _ in ly]
+    g = torch.tensor([[list(r) for r in gg] for ly in layers for _, gg in ly], dtype=torch.complex128,
+                     device=dev) if sites else torch.zeros(1, 4, 4, dtype=torch.complex128, device=dev)
+    cap = n * 16 * chi * chi
+    out = torch.empty(cap, dtype=torch.complex128, device=dev)
+    with torch.cuda.device(dev):
+        bonds = N.tn_mpo_tebd(n, sites, g.data_ptr(), chi, tol, dev.index, out.data_ptr(), cap, _stream())
+    res, o = [], 0
+    for s in range(n):
+        e = bonds[s] * 4 * bonds[s + 1]
+        res.append(out[o:o + e].view(bonds[s], 4, bonds[s + 1]).clone())
+        o += e
+    return res
 
 
 def riemannian_project(gates: torch.Tensor, Z: torch.Tensor) -> torch.Tensor:

@@ -126,6 +126,23 @@ tn_status tn_hvp_set_reference(tn_hvp_ctx* ctx, const void* ref, void* stream) {
   return guarded(ctx, [&] { tn::engine_set_reference(ctx, (const tn::cplx*)ref, (cudaStream_t)stream); });
 }
 
+tn_status tn_mpo_tebd(int32_t n, int32_t ngates, const int32_t* sites, const void* gates, int32_t chi, double tol,
+                      int32_t device, int32_t* bonds_out, void* out, size_t cap, void* stream) {
+  if (n < 2 || ngates < 0 || chi < 1 || device < 0 || !bonds_out || !out || (ngates && (!sites || !gates)) ||
+      !(tol >= 0.0))
+    return fail(nullptr, TN_EINVAL, "tn_mpo_tebd: bad argument");
+  return guarded(nullptr, [&] {
+    TN_CUDA(cudaSetDevice(device));
+    tn::engine_tebd(n, ngates, sites, (const tn::cplx*)gates, chi, tol, device, bonds_out, (tn::cplx*)out, cap,
+                    (cudaStream_t)stream);
+  });
+}
+
+tn_status tn_hvp_set_cache_budget(tn_hvp_ctx* ctx, size_t bytes) {
+  if (!ctx) return fail(nullptr, TN_EINVAL, "tn_hvp_set_cache_budget: null context");
+  return guarded(ctx, [&] { tn::engine_set_cache_budget(ctx, bytes); });
+}
+
 tn_status tn_hvp_trim_memory(tn_hvp_ctx* ctx, void* stream) {
   if (!ctx) return fail(nullptr, TN_EINVAL, "tn_hvp_trim_memory: null context");
   return guarded(ctx, [&] { tn::engine_trim_memory(ctx, (cudaStream_t)stream); });

@@ -206,6 +206,10 @@ struct Engine {
   std::vector<cplx*> memo_owned;
   size_t memo_bytes = 0, memo_budget = 0;
   bool memo_budget_set = false;
+  // tn_hvp_set_cache_budget: 0 = automatic (chain caches within half, memo
+  // within a third of the free memory at the first apply); else a cap in bytes
+  // on chain caches + memo together (several contexts sharing a device).
+  size_t cache_budget = 0;
   // CUDA-graph replay of tn_hvp_apply: a (batch, aux) key seen a second time
   // since the last primal pass is captured once (engine-owned I/O buffers) and
   // replayed; host scalars baked into the graph (frozen s) are per point, so
@@ -607,6 +611,131 @@ struct Engine {
     if (ref) cudaFree(ref);
     pool_trim(device);
     cudaDeviceGraphMemTrim(device);
+  }
+
+  // ------------------------------------------- N4: reference construction --
+  // TEBD of a gate sequence on the operator I/2^{n/2} with the primal pass's
+  // own kernels (reading X11): gates on the OUT legs, the
+  // centre moved by QR / LQ, every two-site split through the Gram
+  // eigendecomposition (DMMA GEMM + heevd), keep r = min(chi, #{sigma_j >
+  // tol sigma_1}) (tol >= 1e-7: the Gram split resolves sigma to ~1e-8 sigma_1),
+  // U_r^H A rescaled to the pre-truncation norm; finally right-canonical with
+  // the centre at site 0 and unit Frobenius norm.  Data-dependent shapes: the
+  // split sizes are read on the host (one stream synchronisation per gate).
+  // out: DEVICE, capacity cap complex elements; bonds: n+1 on return.
+  void tebd(cudaStream_t st, int nn_, int ngates, const int32_t* gsite, const cplx* G, int chi_, double tol,
+            std::vector<int>& bonds, cplx* out, size_t cap) {
+    n = nn_;
+    chi = chi_;
+    TN_CUDA(cudaSetDevice(device));
+    Solver& so = sol[0];
+    TN_SOLVER(cusolverDnCreate(&so.h));
+    TN_SOLVER(cusolverDnSetStream(so.h, st));
+    {
+      const int R = 4 * chi;  // largest two-site row / column count
+      TN_SOLVER(cusolverDnZheevd_bufferSize(so.h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, R, nullptr, R,
+                                            nullptr, &lwork_heevd));
+      TN_SOLVER(cusolverDnZgeqrf_bufferSize(so.h, R, R, nullptr, R, &lwork_geqrf));
+      TN_SOLVER(cusolverDnZungqr_bufferSize(so.h, R, R, R, nullptr, R, nullptr, &lwork_ungqr));
+    }
+    const double tolg = std::max(tol, 1e-7);
+    std::vector<cplx*> a(n, nullptr);
+    bonds.assign(n + 1, 1);
+    const double h = 1.0 / std::sqrt(2.0);
+    for (int s = 0; s < n; ++s) {
+      a[s] = dnew(4, st);
+      set_small(st, a[s], 4, {h, 0.0}, ZERO, ZERO, {h, 0.0});
+    }
+    Pool keep_alive(st);
+    int* info = (int*)keep_alive.raw(sizeof(int));
+    TN_CUDA(cudaMemsetAsync(info, 0, sizeof(int), st));
+    int c = 0;
+    auto move_right = [&]() {
+      Pool tmp(st);
+      const int b = bonds[c], bp = bonds[c + 1], kq = std::min(4 * b, bp), nb2 = bonds[c + 2];
+      cplx* Q = dnew((int64_t)4 * b * kq, st);
+      cplx* Rm = tmp.c((int64_t)kq * bp);
+      qr_right(st, so, tmp, a[c], 4 * b, bp, kq, Q, Rm, info);
+      cplx* nx = dnew((int64_t)kq * 4 * nb2, st);
+      nn(st, kq, 4 * nb2, bp, Rm, 0, a[c + 1], 0, nx, 0, 1);
+      dset(a[c], Q, st);
+      dset(a[c + 1], nx, st);
+      bonds[c + 1] = kq;
+      ++c;
+    };
+    auto move_left = [&]() {
+      Pool tmp(st);
+      const int b = bonds[c], bp = bonds[c + 1], kq = std::min(b, 4 * bp), nb2 = bonds[c - 1];
+      cplx* Q = dnew((int64_t)kq * 4 * bp, st);
+      cplx* L = tmp.c((int64_t)b * kq);
+      lq_left(st, so, tmp, a[c], b, 4 * bp, kq, Q, L, info);
+      cplx* nx = dnew((int64_t)nb2 * 4 * kq, st);
+      nn(st, nb2 * 4, kq, b, a[c - 1], 0, L, 0, nx, 0, 1);
+      dset(a[c], Q, st);
+      dset(a[c - 1], nx, st);
+      bonds[c] = kq;
+      --c;
+    };
+    for (int g = 0; g < ngates; ++g) {
+      const int i = gsite[g];
+      if (i < 0 || i + 1 >= n) throw std::invalid_argument("tn_mpo_tebd: gate site out of range");
+      while (c < i) move_right();
+      while (c > i) move_left();
+      Pool tmp(st);
+      const int bl = bonds[i], m = bonds[i + 1], br = bonds[i + 2], R = 4 * bl, Cc = 4 * br;
+      cplx* th = tmp.c((int64_t)R * Cc);
+      nn(st, R, Cc, m, a[i], 0, a[i + 1], 0, th, 0, 1);
+      cplx* A = tmp.c((int64_t)R * Cc);
+      apply_gate(st, A, 0, th, 0, G + (int64_t)g * 16, 0, bl, br, 1, ONE, false, 2);
+      double* nrm = (double*)tmp.raw(2 * sizeof(double));
+      tangent_dot(st, (int64_t)R * Cc, 1, A, A, nrm);
+      cplx* uhf = tmp.c((int64_t)R * R);
+      double* S = (double*)tmp.raw((size_t)R * sizeof(double));
+      cplx* Acp = tmp.c((int64_t)R * Cc);
+      TN_CUDA(cudaMemcpyAsync(Acp, A, (size_t)R * Cc * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+      svd_rowmajor(st, so, tmp, Acp, R, Cc, S, uhf, info, kGram);
+      std::vector<double> hS(R);
+      TN_CUDA(cudaMemcpyAsync(hS.data(), S, R * sizeof(double), cudaMemcpyDeviceToHost, st));
+      TN_CUDA(cudaStreamSynchronize(st));
+      int r = 0;
+      while (r < R && hS[r] > tolg * hS[0]) ++r;
+      r = std::max(1, std::min(chi, r));
+      cplx* ni = dnew((int64_t)R * r, st);
+      conjT_scale_cols(st, ni, uhf, r, R, nullptr, nullptr);       // U_r (4bl x r)
+      cplx* nj = dnew((int64_t)r * Cc, st);
+      nn(st, r, Cc, R, uhf, 0, A, 0, nj, 0, 1);                     // U_r^H A
+      tangent_dot(st, (int64_t)r * Cc, 1, nj, nj, nrm + 1);
+      scale_by_norm_ratio(st, nj, nrm, (int64_t)r * Cc);            // x sqrt(nrm[0] / nrm[1])
+      dset(a[i], ni, st);
+      dset(a[i + 1], nj, st);
+      bonds[i + 1] = r;
+      c = i + 1;
+    }
+    while (c > 0) move_left();
+    {  // unit Frobenius norm (site 0 is the centre)
+      Pool tmp(st);
+      double* nrm = (double*)tmp.raw(2 * sizeof(double));
+      const int64_t e0 = (int64_t)4 * bonds[1];
+      set_small(st, reinterpret_cast<cplx*>(nrm), 1, ONE);   // nrm[0] = 1
+      tangent_dot(st, e0, 1, a[0], a[0], nrm + 1);
+      scale_by_norm_ratio(st, a[0], nrm, e0);
+      TN_CUDA(cudaStreamSynchronize(st));
+    }
+    size_t tot = 0;
+    for (int s = 0; s < n; ++s) tot += (size_t)bonds[s] * 4 * bonds[s + 1];
+    if (tot > cap) throw std::invalid_argument("tn_mpo_tebd: output capacity " + std::to_string(cap) +
+                                               " < " + std::to_string(tot) + " elements");
+    size_t o = 0;
+    for (int s = 0; s < n; ++s) {
+      const size_t e = (size_t)bonds[s] * 4 * bonds[s + 1];
+      TN_CUDA(cudaMemcpyAsync(out + o, a[s], e * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+      o += e;
+      ddel(a[s], st);
+    }
+    int hinfo = 0;
+    TN_CUDA(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, st));
+    TN_CUDA(cudaStreamSynchronize(st));
+    if (hinfo) throw NumericError("tn_mpo_tebd: cuSOLVER info nonzero");
   }
 
   // ------------------------------------------------------ primal pass --
@@ -1424,6 +1553,11 @@ struct Engine {
     size_t fr = 0, tot = 0;
     TN_CUDA(cudaMemGetInfo(&fr, &tot));
     const size_t need = sizeof(cplx) * (size_t)chain_cache_elems(side ? top : bot);
+    if (cache_budget) {
+      const size_t used = sizeof(cplx) * (size_t)((chain_cache[0].built ? chain_cache_elems(bot) : 0) +
+                                                  (chain_cache[1].built ? chain_cache_elems(top) : 0));
+      return used + need <= cache_budget && need < fr / 2 ? &c : nullptr;
+    }
     return need < fr / 2 ? &c : nullptr;
   }
   // Release the per-point caches, stream-ordered on st: every use of them was
@@ -1455,6 +1589,12 @@ struct Engine {
           size_t fr = 0, tot = 0;
           TN_CUDA(cudaMemGetInfo(&fr, &tot));
           memo_budget = fr / 3;
+          if (cache_budget) {
+            const size_t chains =
+                sizeof(cplx) * (size_t)((chain_cache[0].built ? chain_cache_elems(bot) : 0) +
+                                        (chain_cache[1].built ? chain_cache_elems(top) : 0));
+            memo_budget = std::min(memo_budget, cache_budget > chains ? cache_budget - chains : 0);
+          }
           memo_budget_set = true;
         }
         const size_t bytes = (size_t)std::max<int64_t>(elems, 1) * sizeof(cplx);
@@ -2284,9 +2424,22 @@ void engine_set_reference(tn_hvp_ctx* ctx, const cplx* ref, cudaStream_t st) {
   for (int s = 0; s < e.n; ++s) el += (size_t)e.ref_bonds[s] * e.P * e.ref_bonds[s + 1];
   TN_CUDA(cudaMemcpyAsync(e.ref, ref, sizeof(cplx) * el, cudaMemcpyDeviceToDevice, st));
 }
+void engine_set_cache_budget(tn_hvp_ctx* ctx, size_t bytes) { ctx->e.cache_budget = bytes; }
 void engine_trim_memory(tn_hvp_ctx* ctx, cudaStream_t st) {
   TN_CUDA(cudaSetDevice(ctx->e.device));
   ctx->e.trim_memory(st);
+}
+void engine_tebd(int n, int ngates, const int32_t* sites, const cplx* gates, int chi, double tol, int device,
+                 int32_t* bonds_out, cplx* out, size_t cap, cudaStream_t st) {
+  Engine e;
+  e.device = device;
+  std::vector<int> b;
+  e.tebd(st, n, ngates, sites, gates, chi, tol, b, out, cap);
+  for (int s = 0; s <= n; ++s) bonds_out[s] = b[s];
+  if (e.sol[0].h) {
+    cusolverDnDestroy(e.sol[0].h);
+    e.sol[0].h = nullptr;
+  }
 }
 void engine_query(const tn_hvp_config& cfg, const int32_t* ref_bonds, size_t* primal_bytes, size_t* work_bytes,
                   size_t* per_dir_bytes) {

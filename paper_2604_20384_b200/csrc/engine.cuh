@@ -25,6 +25,9 @@ void engine_primal_blob(tn_hvp_ctx* ctx, void** ptr, size_t* bytes);
 void engine_primal_imported(tn_hvp_ctx* ctx, const cplx* gates, cudaStream_t st);
 void engine_primal_copy(tn_hvp_ctx* ctx, void* buf, size_t bytes, int into_ctx, cudaStream_t st);
 void engine_trim_memory(tn_hvp_ctx* ctx, cudaStream_t st);
+void engine_set_cache_budget(tn_hvp_ctx* ctx, size_t bytes);
+void engine_tebd(int n, int ngates, const int32_t* sites, const cplx* gates, int chi, double tol, int device,
+                 int32_t* bonds_out, cplx* out, size_t cap, cudaStream_t st);
 void engine_set_product_state(tn_hvp_ctx* ctx, const cplx* psi, cudaStream_t st);
 void engine_set_reference(tn_hvp_ctx* ctx, const cplx* ref, cudaStream_t st);
 void engine_work(tn_hvp_ctx* ctx, double* per_dir, double* primal);

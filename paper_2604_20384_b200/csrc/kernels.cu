@@ -822,3 +822,20 @@ void check_tangent(cudaStream_t st, int K, int batch, const cplx* G, const cplx*
 }
 }  // namespace tn
 
+
+namespace tn {
+namespace {
+__global__ void norm_ratio_kernel(cplx* __restrict__ y, const double* __restrict__ nrm, int64_t n) {
+  const double f = sqrt(nrm[0] / nrm[1]);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = cscale(y[i], f);
+}
+}  // namespace
+
+void scale_by_norm_ratio(cudaStream_t st, cplx* y, const double* nrm, int64_t n) {
+  if (n <= 0) return;
+  norm_ratio_kernel<<<nblocks(n), TPB, 0, st>>>(y, nrm, n);
+  TN_CUDA(cudaGetLastError());
+  count_launch();
+}
+}  // namespace tn

@@ -88,3 +88,8 @@ void check_unitary(cudaStream_t st, int K, const cplx* G, double* res);
 void check_tangent(cudaStream_t st, int K, int batch, const cplx* G, const cplx* V, double* res);
 }  // namespace tn
 
+
+namespace tn {
+// y *= sqrt(nrm[0] / nrm[1]) (device scalars; norm-restoring rescale)
+void scale_by_norm_ratio(cudaStream_t st, cplx* y, const double* nrm, int64_t n);
+}  // namespace tn

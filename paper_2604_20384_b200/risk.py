@@ -47,6 +47,14 @@ class EmpiricalRisk:
         # own host thread, so their latency-bound primal sweeps overlap on the
         # GPU (ctypes releases the GIL inside the library calls)
         self.streams = [torch.cuda.Stream(device=self.device) for _ in self.engines]
+        # the engines share the device: split the per-point cache memory
+        # (chains + memo) evenly, keeping room for each sample's tangent state
+        if self.engines:
+            free, _ = torch.cuda.mem_get_info(self.device)
+            work = sum(e.per_direction_bytes * e.max_batch for e in self.engines)
+            share = max(0, int(0.8 * (free - work))) // len(self.engines)
+            for e in self.engines:
+                e.set_cache_budget(max(share, 1))
         self.pool = ThreadPoolExecutor(max_workers=max(1, len(self.engines)))
 
     def _each(self, fn):

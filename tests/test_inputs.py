@@ -65,7 +65,7 @@ def test_trotter_gate_closed_form_zz():
     assert np.allclose(g, np.diag(np.exp(1j * 0.3 * np.array([1, -1, -1, 1]))), atol=1e-15)
 
 
-@pytest.mark.parametrize("order,slope", [(1, 2.0), (2, 4.0)])
+@pytest.mark.parametrize("order,slope", [(1, 2.0), (2, 4.0), (4, 16.0)])
 def test_trotter_order(order, slope):
     n, t = 5, 0.5
     m = Model("tfim", {"J": 1.0, "h": 0.9, "g": 0.4})

@@ -91,6 +91,23 @@ def trotter_layers(model: Model, n: int, t: float, steps: int, order: int):
         for s in range(steps):
             layers.append(layer(1, d))
             layers.append(layer(0, d if s + 1 < steps else d / 2))
+    elif order == 4:
+        # Suzuki's fourth-order fractal (PAPER.md:589, :601 use a 4th-order
+        # reference): S4(d) = S2(p d)^2 S2((1 - 4p) d) S2(p d)^2, p = 1/(4 - 4^{1/3}),
+        # S2(x) = e^{-i x H_A/2} e^{-i x H_B} e^{-i x H_A/2}; adjacent H_A half
+        # steps are merged into one layer (as for order 2)
+        p = 1.0 / (4.0 - 4.0 ** (1.0 / 3.0))
+        seq = []                                   # (offset, dt) factors, applied in order
+        for _ in range(steps):
+            for x in (p, p, 1 - 4 * p, p, p):
+                seq += [(0, x * d / 2), (1, x * d), (0, x * d / 2)]
+        merged = []
+        for off, dt in seq:
+            if merged and merged[-1][0] == off:
+                merged[-1] = (off, merged[-1][1] + dt)
+            else:
+                merged.append((off, dt))
+        layers = [layer(off, dt) for off, dt in merged]
     else:
-        raise ValueError("order must be 1 or 2")
+        raise ValueError("order must be 1, 2 or 4")
     return [ly for ly in layers if ly]

@@ -104,9 +104,13 @@ def mpo_bonds(sites):
 def mpo_to_dense_operator(sites) -> np.ndarray:
     """Contract an MPO (n <= 10) into its 2^n x 2^n operator (times 1, no rescale)."""
     n = len(sites)
-    t = sites[0].detach().resolve_conj().cpu().numpy()           # [1][4][b]
+
+    def host(x):
+        return x if isinstance(x, np.ndarray) else x.detach().resolve_conj().cpu().numpy()
+
+    t = host(sites[0])                                           # [1][4][b]
     for s in range(1, n):
-        a = sites[s].detach().resolve_conj().cpu().numpy()
+        a = host(sites[s])
         t = np.tensordot(t, a, axes=([t.ndim - 1], [0]))
     t = t.reshape((4,) * n)                         # drop boundary bonds
     t = t.reshape((2, 2) * n)                       # o0 i0 o1 i1 ...
