@@ -1,13 +1,12 @@
 // Batched complex128 GEMM on the FP64 tensor cores of sm_100a.
 //
 // tcgen05.mma has no f64 kind (ptxas rejects .kind::f64), so the FP64 tensor
-// path on B200 is the warp-level mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).  A
-// complex product is four real DMMAs on planar fragments:
-//   C_re += A_re B_re + (-A_im) B_im,   C_im += A_re B_im + A_im B_re.
-// Tiles: CTA 64x64 (complex) x BK=16, 4 warps in 2x2, warp tile 32x32 =
-// 4x4 DMMA tiles; operands staged global->shared with cp.async (16 B per
-// complex element, zero-filled outside the matrix), double-buffered; shared
-// strides padded so every fragment load (one LDS.128 = one complex) is
+// path on B200 is the warp-level mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).  The
+// complex product uses the 3M (Gauss) form -- three real DMMAs per complex
+// k-step on planar fragments (zgemm3m_kernel below).  CTA tile 64x64 (complex)
+// x BK=16; operands staged global->shared with cp.async (16 B per complex
+// element, zero-filled outside the matrix), double-buffered, two CTAs per SM;
+// shared strides padded so every fragment load (one LDS.128 = one complex) is
 // bank-conflict free.  op(A), op(B) in {N, T, C}; conjugation is folded into
 // the fragment sign.  Row-major everywhere; batch strides may be 0 (shared).
 #include <algorithm>
@@ -33,12 +32,11 @@ struct Prof {
 };
 Prof g_prof;
 std::mutex g_prof_mu;
-constexpr int BM = 64, BN = 64, BK = 16, NT = 128;
+constexpr int BM = 64, BN = 64, BK = 16;
 constexpr int LDN = BK + 4;    // [rows][BK] tiles: row stride = 20 complex (= 4 mod 8 slots)
 constexpr int LDT = BM + 2;    // [BK][cols] tiles: row stride = 66 complex (= 2 mod 8 slots)
 constexpr int TILE = BM * LDN; // 1280 >= BK * LDT = 1056
 constexpr int STAGE = 2 * TILE;
-constexpr int SMEM_BYTES = 2 * STAGE * (int)sizeof(cplx);
 
 struct Params {
   int M, N, K;
@@ -68,118 +66,6 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
 }
-
-template <char OPA, char OPB>
-__global__ void __launch_bounds__(NT, 2) zgemm_kernel(Params p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  cplx* smem = reinterpret_cast<cplx*>(smem_raw);
-  const int64_t bz = blockIdx.z;
-  const cplx* __restrict__ A = p.A + bz * p.sA;
-  const cplx* __restrict__ B = p.B + bz * p.sB;
-  cplx* __restrict__ C = p.C + bz * p.sC;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 1, wn = warp & 1;
-  const int g = lane >> 2, q = lane & 3;
-
-  auto load_stage = [&](int stage, int k0) {
-    cplx* sA = smem + stage * STAGE;
-    cplx* sB = sA + TILE;
-#pragma unroll
-    for (int j = 0; j < (BM * BK) / NT; ++j) {
-      const int e = tid + j * NT;
-      if (OPA == 'N') {
-        const int m = e / BK, k = e % BK, gm = m0 + m, gk = k0 + k;
-        const bool ok = gm < p.M && gk < p.K;
-        cp_async16(sA + m * LDN + k, ok ? (const void*)(A + (int64_t)gm * p.lda + gk) : (const void*)A, ok);
-      } else {
-        const int k = e / BM, m = e % BM, gm = m0 + m, gk = k0 + k;
-        const bool ok = gm < p.M && gk < p.K;
-        cp_async16(sA + k * LDT + m, ok ? (const void*)(A + (int64_t)gk * p.lda + gm) : (const void*)A, ok);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < (BN * BK) / NT; ++j) {
-      const int e = tid + j * NT;
-      if (OPB == 'N') {
-        const int k = e / BN, n = e % BN, gn = n0 + n, gk = k0 + k;
-        const bool ok = gn < p.N && gk < p.K;
-        cp_async16(sB + k * LDT + n, ok ? (const void*)(B + (int64_t)gk * p.ldb + gn) : (const void*)B, ok);
-      } else {
-        const int n = e / BK, k = e % BK, gn = n0 + n, gk = k0 + k;
-        const bool ok = gn < p.N && gk < p.K;
-        cp_async16(sB + n * LDN + k, ok ? (const void*)(B + (int64_t)gn * p.ldb + gk) : (const void*)B, ok);
-      }
-    }
-  };
-
-  double acc_re[4][4][2], acc_im[4][4][2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc_re[i][j][0] = acc_re[i][j][1] = acc_im[i][j][0] = acc_im[i][j][1] = 0.0;
-
-  const int nk = (p.K + BK - 1) / BK;
-  load_stage(0, 0);
-  cp_commit();
-  for (int kt = 0; kt < nk; ++kt) {
-    if (kt + 1 < nk) load_stage((kt + 1) & 1, (kt + 1) * BK);
-    cp_commit();
-    cp_wait<1>();
-    __syncthreads();
-    const cplx* sA = smem + (kt & 1) * STAGE;
-    const cplx* sB = sA + TILE;
-#pragma unroll
-    for (int kk = 0; kk < BK / 4; ++kk) {
-      double ar[4], ai[4], an[4], br[4], bi[4];
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi) {
-        const int row = wm * 32 + mi * 8 + g, col = kk * 4 + q;
-        const cplx a = (OPA == 'N') ? sA[row * LDN + col] : sA[col * LDT + row];
-        ar[mi] = a.x;
-        ai[mi] = (OPA == 'C') ? -a.y : a.y;
-        an[mi] = -ai[mi];
-      }
-#pragma unroll
-      for (int ni = 0; ni < 4; ++ni) {
-        const int krow = kk * 4 + q, ncol = wn * 32 + ni * 8 + g;
-        const cplx b = (OPB == 'N') ? sB[krow * LDT + ncol] : sB[ncol * LDN + krow];
-        br[ni] = b.x;
-        bi[ni] = (OPB == 'C') ? -b.y : b.y;
-      }
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni) {
-          dmma(acc_re[mi][ni], ar[mi], br[ni]);
-          dmma(acc_im[mi][ni], ar[mi], bi[ni]);
-          dmma(acc_re[mi][ni], an[mi], bi[ni]);
-          dmma(acc_im[mi][ni], ai[mi], br[ni]);
-        }
-    }
-    __syncthreads();
-  }
-
-#pragma unroll
-  for (int mi = 0; mi < 4; ++mi) {
-    const int row = m0 + wm * 32 + mi * 8 + g;
-    if (row >= p.M) continue;
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni) {
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int col = n0 + wn * 32 + ni * 8 + 2 * q + j;
-        if (col < p.N) {
-          cplx v = cmul(p.alpha, make_double2(acc_re[mi][ni][j], acc_im[mi][ni][j]));
-          cplx* dst = C + (int64_t)row * p.ldc + col;
-          if (p.has_beta) v = cadd(v, cmul(p.beta, *dst));
-          *dst = v;
-        }
-      }
-    }
-  }
-}
-
 
 // 3M (Gauss) variant: (a + ib)(c + id) = ac - bd + i[(a + b)(c + d) - ac - bd],
 // three real DMMAs per complex k-step: P1 += Ar Br, P2 += Ai Bi,
@@ -333,22 +219,12 @@ __global__ void zreduce_kernel(Params p, int batch) {
   }
 }
 
-int g_variant = -1;  // 0 = 4M (4 warps, 2 stages), 1 = 3M (8 warps, 4 stages, 1 CTA/SM), 2 = 3M (2 stages, 2 CTAs/SM, default)
-int variant() {
-  if (g_variant < 0) {
-    const char* v = std::getenv("TN_GEMM");
-    g_variant = (v && std::string(v) == "4m") ? 0 : (v && std::string(v) == "3m4") ? 1 : 2;
-  }
-  return g_variant;
-}
-constexpr int SMEM3_4 = 4 * STAGE * (int)sizeof(cplx), SMEM3_2 = 2 * STAGE * (int)sizeof(cplx);
+constexpr int SMEM3_2 = 2 * STAGE * (int)sizeof(cplx);
 
 template <char OPA, char OPB>
 void launch(const Params& p, int batch, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    TN_CUDA(cudaFuncSetAttribute(zgemm_kernel<OPA, OPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    TN_CUDA(cudaFuncSetAttribute(zgemm3m_kernel<OPA, OPB, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM3_4));
     TN_CUDA(cudaFuncSetAttribute(zgemm3m_kernel<OPA, OPB, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM3_2));
     attr = true;
   }
@@ -358,7 +234,7 @@ void launch(const Params& p, int batch, cudaStream_t st) {
   q.part = nullptr;
   const int64_t ctas = (int64_t)grid.x * grid.y * batch;
   const int nk = (p.K + BK - 1) / BK;
-  if (variant() >= 1 && ctas < 148 && nk >= 16) {  // split K to fill the SMs (>= 8 k-tiles per split)
+  if (ctas < 148 && nk >= 16) {  // split K to fill the SMs (>= 8 k-tiles per split)
     int ks = (int)std::min<int64_t>((296 + ctas - 1) / ctas, nk / 8);
     if (ks > 1) {
       q.ksplit = ks;
@@ -373,12 +249,7 @@ void launch(const Params& p, int batch, cudaStream_t st) {
     TN_CUDA(cudaEventCreate(&e1));
     TN_CUDA(cudaEventRecord(e0, st));
   }
-  if (variant() == 1)
-    zgemm3m_kernel<OPA, OPB, 4, 1><<<grid, NT3, SMEM3_4, st>>>(q);
-  else if (variant() == 2)
-    zgemm3m_kernel<OPA, OPB, 2, 2><<<grid, NT3, SMEM3_2, st>>>(q);
-  else
-    zgemm_kernel<OPA, OPB><<<grid, NT, SMEM_BYTES, st>>>(p);
+  zgemm3m_kernel<OPA, OPB, 2, 2><<<grid, NT3, SMEM3_2, st>>>(q);
   TN_CUDA(cudaGetLastError());
   count_launch();
   if (q.ksplit > 1) {
@@ -415,10 +286,10 @@ void count_launch(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed
 // Library-private stream-ordered memory: one cudaMemPool per device, created on
 // first use, never the device's default pool (so torch's and other libraries'
 // allocations are not affected by its policies).  Cached blocks are kept
-// (release threshold max) and not reused across streams through implicit
-// dependencies (the two primal sweeps run on two streams and must not be
-// serialised through recycled blocks).  Inside a stream capture the allocation
-// becomes a graph memory node (cudaMallocAsync).
+// (release threshold max); the pool never inserts a dependency to reuse a
+// block across streams (the two primal sweeps run on two streams and must not
+// be serialised through recycled blocks).  Inside a stream capture the
+// allocation becomes a graph memory node (cudaMallocAsync).
 namespace {
 std::mutex g_pool_mu;
 cudaMemPool_t g_pools[64] = {};
@@ -433,10 +304,12 @@ cudaMemPool_t device_pool(int dev) {
     cudaMemPool_t p = nullptr;
     TN_CUDA(cudaMemPoolCreate(&p, &props));
     uint64_t thr = UINT64_MAX;
-    int off = 0;
+    int off = 0, on = 1;
     TN_CUDA(cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr));
-    TN_CUDA(cudaMemPoolSetAttribute(p, cudaMemPoolReuseFollowEventDependencies, &off));
-    TN_CUDA(cudaMemPoolSetAttribute(p, cudaMemPoolReuseAllowOpportunistic, &off));
+    // a block freed on one stream may serve another stream only when that
+    // costs no new dependency (already ordered, or the free has completed)
+    TN_CUDA(cudaMemPoolSetAttribute(p, cudaMemPoolReuseFollowEventDependencies, &on));
+    TN_CUDA(cudaMemPoolSetAttribute(p, cudaMemPoolReuseAllowOpportunistic, &on));
     TN_CUDA(cudaMemPoolSetAttribute(p, cudaMemPoolReuseAllowInternalDependencies, &off));
     g_pools[dev] = p;
   }

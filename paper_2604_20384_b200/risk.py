@@ -27,7 +27,8 @@ class EmpiricalRisk:
     """labels: S label MPS (lists of [b][2][b'] tensors, right-canonical, the
     same bonds for every sample); psis: [S, n, 2] product states."""
 
-    def __init__(self, n, depth, chi, labels, psis, first_offset=0, max_batch=64, device=None, group=None):
+    def __init__(self, n, depth, chi, labels, psis, first_offset=0, max_batch=64, device=None, group=None,
+                 concurrency=4):
         self.group = group
         S = len(labels)
         if group is not None:
@@ -51,11 +52,14 @@ class EmpiricalRisk:
         # (chains + memo) evenly, keeping room for each sample's tangent state
         if self.engines:
             free, _ = torch.cuda.mem_get_info(self.device)
-            work = sum(e.per_direction_bytes * e.max_batch for e in self.engines)
+            work = 2 * min(concurrency, len(self.engines)) * max(e.per_direction_bytes * e.max_batch
+                                                                for e in self.engines)
             share = max(0, int(0.8 * (free - work))) // len(self.engines)
             for e in self.engines:
                 e.set_cache_budget(max(share, 1))
-        self.pool = ThreadPoolExecutor(max_workers=max(1, len(self.engines)))
+        # at most `concurrency` samples in flight (their transient tangent and
+        # environment buffers must fit beside all samples' primal stores)
+        self.pool = ThreadPoolExecutor(max_workers=max(1, min(concurrency, len(self.engines))))
 
     def _each(self, fn):
         """fn(engine) for every local sample, concurrently on per-sample
