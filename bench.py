@@ -54,7 +54,8 @@ def parse():
     ap.add_argument("--workload", default="config", choices=["config", "n1"],
                     help="config: the BASELINE.json config (default); n1: the sampled-state empirical risk "
                          "(SURVEY.md 8(f) N1) at the config's width")
-    ap.add_argument("--samples", type=int, default=8, help="N1: product states S")
+    ap.add_argument("--samples", type=int, default=4, help="N1: product states S")
+    ap.add_argument("--concurrency", type=int, default=2, help="N1: samples in flight per GPU")
     return ap.parse_args()
 
 
@@ -269,7 +270,7 @@ def run_n1(args, cfg, rank, world, local):
     G = torch.tensor(Gnp, device=dev)
     V = torch.tensor(C.tangent_directions(cfg.cid, Gnp, B), device=dev)
     er = EmpiricalRisk(cfg.n, cfg.depth, cfg.chi, labels, psis, cfg.first_offset, max_batch=B,
-                       group=dist.group.WORLD if world > 1 else None)
+                       group=dist.group.WORLD if world > 1 else None, concurrency=args.concurrency)
 
     def step():
         er.environments(G)

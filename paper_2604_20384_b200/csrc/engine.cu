@@ -700,6 +700,9 @@ struct Engine {
       int r = 0;
       while (r < R && hS[r] > tolg * hS[0]) ++r;
       r = std::max(1, std::min(chi, r));
+      // kept-subspace refinement across the cut (as in the primal pass): the
+      // Gram basis mixes kept and discarded directions by ~eps s_1^2 / gap
+      refine_kept(st, tmp, uhf, S, A, R, Cc, R, r, 2);
       cplx* ni = dnew((int64_t)R * r, st);
       conjT_scale_cols(st, ni, uhf, r, R, nullptr, nullptr);       // U_r (4bl x r)
       cplx* nj = dnew((int64_t)r * Cc, st);
