@@ -354,6 +354,10 @@ def main():
     torch.cuda.synchronize()
     t_ref0 = time.time()
     ref = mpo_tebd(cfg.n, C.reference_layers(cfg), cfg.chi)
+    if world > 1:   # every rank uses rank 0's reference bits (the imported primal store was built on it)
+        import torch.distributed as dist
+        for a in ref:
+            dist.broadcast(a, src=0)
     torch.cuda.synchronize()
     t_ref = time.time() - t_ref0
     Gnp = C.haar_gates(cfg.cid, K)

@@ -74,11 +74,10 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 // pipeline, one CTA per SM (<= 255 registers).
 constexpr int NT3 = 256;
 
-template <char OPA, char OPB, int NSTAGE3, int MINB, bool BSUM>
+template <char OPA, char OPB, int NSTAGE3, int MINB>
 __global__ void __launch_bounds__(NT3, MINB) zgemm3m_kernel(Params p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cplx* smem = reinterpret_cast<cplx*>(smem_raw);
-  double* sBsum = reinterpret_cast<double*>(smem + NSTAGE3 * STAGE);  // BSUM: [stage][TILE] Br + Bi
   const int ks = p.ksplit > 1 ? p.ksplit : 1;
   const int64_t bz = blockIdx.z / ks;
   const int split = blockIdx.z % ks;
@@ -147,17 +146,6 @@ __global__ void __launch_bounds__(NT3, MINB) zgemm3m_kernel(Params p) {
     }
     const cplx* sA = smem + (kt % NSTAGE3) * STAGE;
     const cplx* sB = sA + TILE;
-    double* sBs = sBsum + (kt % NSTAGE3) * TILE;
-    if (BSUM) {  // the 3M sums of the B tile once per CTA, off the DMMA dependency chains
-#pragma unroll
-      for (int j = 0; j < (BN * BK) / NT3; ++j) {
-        const int e = tid + j * NT3;
-        const int idx = (OPB == 'N') ? (e / BN) * LDT + (e % BN) : (e / BK) * LDN + (e % BK);
-        const cplx b = sB[idx];
-        sBs[idx] = b.x + ((OPB == 'C') ? -b.y : b.y);
-      }
-      __syncthreads();
-    }
 #pragma unroll
     for (int kk = 0; kk < BK / 4; ++kk) {
       double ar[2], ai[2], as[2], br[4], bi[4], bs[4];
@@ -172,11 +160,10 @@ __global__ void __launch_bounds__(NT3, MINB) zgemm3m_kernel(Params p) {
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni) {
         const int krow = kk * 4 + q, ncol = wn * 32 + ni * 8 + g;
-        const int bidx = (OPB == 'N') ? krow * LDT + ncol : ncol * LDN + krow;
-        const cplx b = sB[bidx];
+        const cplx b = (OPB == 'N') ? sB[krow * LDT + ncol] : sB[ncol * LDN + krow];
         br[ni] = b.x;
         bi[ni] = (OPB == 'C') ? -b.y : b.y;
-        bs[ni] = BSUM ? sBs[bidx] : br[ni] + bi[ni];
+        bs[ni] = br[ni] + bi[ni];
       }
 #pragma unroll
       for (int mi = 0; mi < 2; ++mi)
@@ -233,20 +220,12 @@ __global__ void zreduce_kernel(Params p, int batch) {
 }
 
 constexpr int SMEM3_2 = 2 * STAGE * (int)sizeof(cplx);
-constexpr int SMEM3_2S = SMEM3_2 + 2 * TILE * (int)sizeof(double);
-bool bsum_variant() {  // experiment switch (TN_GEMM_BSUM=1)
-  static const bool v = std::getenv("TN_GEMM_BSUM") != nullptr;
-  return v;
-}
 
 template <char OPA, char OPB>
 void launch(const Params& p, int batch, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    TN_CUDA(cudaFuncSetAttribute(zgemm3m_kernel<OPA, OPB, 2, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 SMEM3_2));
-    TN_CUDA(cudaFuncSetAttribute(zgemm3m_kernel<OPA, OPB, 2, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 SMEM3_2S));
+    TN_CUDA(cudaFuncSetAttribute(zgemm3m_kernel<OPA, OPB, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM3_2));
     attr = true;
   }
   dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, batch);
@@ -270,10 +249,7 @@ void launch(const Params& p, int batch, cudaStream_t st) {
     TN_CUDA(cudaEventCreate(&e1));
     TN_CUDA(cudaEventRecord(e0, st));
   }
-  if (bsum_variant())
-    zgemm3m_kernel<OPA, OPB, 2, 2, true><<<grid, NT3, SMEM3_2S, st>>>(q);
-  else
-    zgemm3m_kernel<OPA, OPB, 2, 2, false><<<grid, NT3, SMEM3_2, st>>>(q);
+  zgemm3m_kernel<OPA, OPB, 2, 2><<<grid, NT3, SMEM3_2, st>>>(q);
   TN_CUDA(cudaGetLastError());
   count_launch();
   if (q.ksplit > 1) {
