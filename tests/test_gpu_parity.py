@@ -38,13 +38,29 @@ CASES = [
 ]
 
 
+def cpp_outputs(cfg, ref, G, V):
+    """The plain C++ complex128 oracle (oracle/cpp): the dense truncated
+    definition with its own Jacobi SVD, Alg. 2 / App. E postprocessing."""
+    from oracle import cpp_oracle as X
+    from oracle import dense as O
+    from tn_inputs.reference import mpo_bonds, mpo_to_dense_operator
+    n = cfg.n
+    x0 = O.op_to_vec(np.eye(2 ** n) / 2 ** (n / 2), n)
+    top0 = O.op_to_vec(mpo_to_dense_operator(ref), n)
+    T, E, H = X.dense_truncated(n, cfg.depth, cfg.chi, G, x0, top0, mpo_bonds(ref), V, cfg.first_offset)
+    f, gR, HR = X.postprocess(G, T, E, H, V)
+    return {"T": T, "f": f, "E": E, "grad_R": gR, "HR": HR, "HT": H,
+            "OM": np.array([np.sum(E * V[b]) for b in range(V.shape[0])])}
+
+
 @pytest.mark.parametrize("cfg", CASES, ids=lambda c: c.name)
 def test_parity_small(cfg):
-    """Against O3 (MPO sweeps) AND O2 (the dense plain definition with explicit
-    Schmidt projectors, n <= 8), whole-output and per gate."""
+    """Against O3 (MPO sweeps), O2 (the dense plain definition with explicit
+    Schmidt projectors, n <= 8) AND the plain C++ oracle, whole-output and per
+    gate."""
     ref, G, V = workload(cfg, ref_chi=max(cfg.chi, 4))
     g = gpu_outputs(cfg, ref, G, V)
-    for o in (oracle_outputs(cfg, ref, G, V), o2_outputs(cfg, ref, G, V)):
+    for o in (oracle_outputs(cfg, ref, G, V), o2_outputs(cfg, ref, G, V), cpp_outputs(cfg, ref, G, V)):
         assert abs(g["T"] - o["T"]) <= TOL * abs(o["T"])
         assert abs(g["f"] - o["f"]) <= TOL * abs(o["f"])
         assert rel(g["E"], o["E"]) < TOL
