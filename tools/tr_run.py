@@ -20,6 +20,8 @@ ap.add_argument("--config", type=int, default=5)
 ap.add_argument("--problems", type=int, default=None)
 ap.add_argument("--outer", type=int, default=None)
 ap.add_argument("--max-hvp", type=int, default=None)
+ap.add_argument("--concurrent", type=int, default=1,
+                help="problems in flight per GPU (one engine, stream and host thread each; memory permitting)")
 a = ap.parse_args()
 cfg = C.CONFIGS[a.config]
 P = a.problems or cfg.extra.get("problems", 1)
@@ -34,17 +36,35 @@ if world > 1:
 dev = torch.device("cuda", torch.cuda.current_device())
 t0 = time.time()
 ref = C.reference_mpo(cfg, device=dev)
-eng = HVPEngine(cfg.n, cfg.depth, cfg.chi, ref, max_batch=1)
 start, count = shard(P, rank, world)
+mine = list(range(start, start + count))
+lanes = max(1, min(a.concurrent, len(mine)))
+engines = [HVPEngine(cfg.n, cfg.depth, cfg.chi, ref, max_batch=1) for _ in range(lanes)]
+streams = [torch.cuda.Stream() for _ in range(lanes)]
+
+
+def solve(p, lane):
+    with torch.cuda.stream(streams[lane]):
+        x0 = torch.tensor(C.trotter_init_gates(cfg, p), device=dev)
+        tp = time.time()
+        x, f, tr = TrustRegion(engines[lane], TRParams(outer=outer, max_hvp=max_hvp)).run(x0)
+        torch.cuda.current_stream().synchronize()
+    return {"problem": p, "f0": tr.records[0]["f"], "f": f, "hvps": tr.hvps, "grads": tr.grads,
+            "seconds": time.time() - tp, "lane": lane,
+            "trace": [{k: v for k, v in r.items() if k in ("iter", "f", "rho", "accepted", "n_hvp", "delta",
+                                                             "tcg_stop")} for r in tr.records]}
+
+
 results = []
-for p in range(start, start + count):
-    x0 = torch.tensor(C.trotter_init_gates(cfg, p), device=dev)
-    tp = time.time()
-    x, f, tr = TrustRegion(eng, TRParams(outer=outer, max_hvp=max_hvp)).run(x0)
-    results.append({"problem": p, "f0": tr.records[0]["f"], "f": f, "hvps": tr.hvps, "grads": tr.grads,
-                    "seconds": time.time() - tp,
-                    "trace": [{k: v for k, v in r.items() if k in ("iter", "f", "rho", "accepted", "n_hvp", "delta",
-                                                                     "tcg_stop")} for r in tr.records]})
+if lanes == 1:
+    results = [solve(p, 0) for p in mine]
+else:   # problems are independent: interleave them over lanes (ctypes releases the GIL in the library)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=lanes) as ex:
+        futs = []
+        for i in range(0, len(mine), lanes):
+            futs = [ex.submit(solve, p, j) for j, p in enumerate(mine[i:i + lanes])]
+            results += [f.result() for f in futs]
 if world > 1:
     fs = torch.zeros(P, dtype=torch.float64, device=dev)
     for r in results:
@@ -55,6 +75,7 @@ else:
     gathered = [r["f"] for r in results]
 if rank == 0:
     print(json.dumps({"config": cfg.name, "problems": P, "world": world, "outer": outer, "max_hvp": max_hvp,
-                      "final_f": gathered, "rank0_runs": results, "wall_s": time.time() - t0}))
+                      "concurrent": lanes, "final_f": gathered, "rank0_runs": results,
+                      "wall_s": time.time() - t0}))
 if world > 1:
     dist.destroy_process_group()
