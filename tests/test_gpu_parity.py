@@ -198,3 +198,39 @@ def test_fused_step_equals_environments_plus_apply(cid, max_batch):
     H3 = eng.apply(V)                                  # state after the fused step is the same
     assert torch.equal(H3, H1)
     eng.close()
+
+
+EDGE = [
+    C.small_case(231, 2, 3, 4, batch=2),                  # n = 2: layer 2 has no gate (K = 2)
+    C.small_case(232, 2, 2, 4, batch=1, first_offset=1),  # n = 2, offset 1: layer 1 empty (K = 1)
+    C.small_case(233, 3, 1, 16, batch=2),                 # depth 1
+    C.small_case(234, 3, 2, 2, batch=3, first_offset=1),  # odd n, chi = 2 (heavy truncation)
+]
+
+
+@pytest.mark.parametrize("cfg", EDGE, ids=lambda c: c.name)
+def test_parity_edge_cases(cfg):
+    """Degenerate layouts (empty layers, a single gate, depth 1, chi = 2)
+    against O3 and the plain C++ oracle, whole output and per gate."""
+    ref, G, V = workload(cfg, ref_chi=max(cfg.chi, 4))
+    g = gpu_outputs(cfg, ref, G, V, max_batch=2)           # ragged sub-batches for batch 3
+    for o in (oracle_outputs(cfg, ref, G, V), cpp_outputs(cfg, ref, G, V)):
+        assert abs(g["f"] - o["f"]) <= TOL * abs(o["f"])
+        gatewise(g["grad_R"], o["grad_R"], TOL)
+        for b in range(V.shape[0]):
+            gatewise(g["HR"][b], o["HR"][b], TOL)
+
+
+def test_empty_batch_and_zero_direction():
+    """batch 0 is a no-op; the zero direction gives a zero Hessian (V = 0 closed form)."""
+    from paper_2604_20384_b200.api import HVPEngine
+    cfg = C.small_case(235, 4, 3, 8, batch=1)
+    ref, G, V = workload(cfg)
+    dev = torch.device("cuda")
+    eng = HVPEngine(cfg.n, cfg.depth, cfg.chi, [a.to(dev) for a in ref], max_batch=2)
+    eng.environments(torch.tensor(G, device=dev))
+    H0 = eng.apply(torch.zeros((0,) + V.shape[1:], dtype=torch.complex128, device=dev))
+    assert H0.shape[0] == 0
+    Hz = eng.apply(torch.zeros_like(torch.tensor(V, device=dev)))
+    assert float(Hz.abs().max()) == 0.0
+    eng.close()
