@@ -343,7 +343,7 @@ def main():
         return
     from paper_2604_20384_b200 import _native as N
     from paper_2604_20384_b200.api import SUB_BATCH, HVPEngine
-    from paper_2604_20384_b200.parallel import broadcast_primal, gather_rows, shard, sharded_step
+    from paper_2604_20384_b200.parallel import broadcast_primal, gather_rows, shard, sharded_step, split_primal
 
     dev = torch.device("cuda", torch.cuda.current_device())
     B = args.batch or cfg.batch                       # directions per step (all ranks together)
@@ -386,14 +386,10 @@ def main():
     # apply phase's GEMMs run alone on one stream: per-launch GEMM time (CUDA
     # events around every GEMM) and exact complex MACs of each phase
     barrier(world)
-    env_gemm_ms = env_gemm_cmac = 0.0
-    if rank == 0:
-        N.tn_gemm_profile(1)
-        eng.environments(G)
-        torch.cuda.synchronize()
-        env_gemm_ms, env_gemm_cmac = N.tn_gemm_profile(0)
-    if world > 1:
-        broadcast_primal(eng, G)
+    N.tn_gemm_profile(1)
+    split_primal(eng, G)                       # one GPU: tn_hvp_environments
+    torch.cuda.synchronize()
+    env_gemm_ms, env_gemm_cmac = N.tn_gemm_profile(0)
     N.tn_gemm_profile(1)
     if cnt:
         eng.apply(Vmine)
@@ -448,12 +444,13 @@ def main():
                "h2d_bytes_per_step": int(Gh.numel() * 16 + Vh.numel() * 16),
                "d2h_bytes_per_step": int(Hh.numel() * 16 + 8 * 8)}
 
-    # phases of one (untimed) step, each bracketed by a barrier: primal pass on
-    # rank 0, broadcast of the store, apply of this rank's share, all_gather
+    # phases of one (untimed) step, each bracketed by a barrier: the primal
+    # pass (N > 1: split over ranks 0 / 1 with the region exchange and every
+    # rank's finish), the alternative whole-store broadcast from rank 0, the
+    # apply of this rank's share, the all_gather
     barrier(world)
     with Phase() as p_env:
-        if rank == 0:
-            eng.environments(G)
+        split_primal(eng, G)
     t_env = max_over_ranks(p_env.ms, world)
     barrier(world)
     with Phase() as p_bc:
@@ -469,8 +466,15 @@ def main():
         if world > 1:
             gather_rows(local_H, B)
     t_ga = max_over_ranks(p_ga.ms, world)
-    phases = {"primal_ms": t_env, "broadcast_ms": t_bc if world > 1 else 0.0,
-              "broadcast_bytes": int(eng.primal_bytes) if world > 1 else 0, "apply_ms": t_ap,
+    xbytes = sum(eng.primal_region(p)[1] for p in (0, 1))
+    phases = {"primal_ms": t_env,
+              "primal": ("split over ranks 0/1 (bottom | top sweep), both store regions broadcast "
+                         f"({xbytes} bytes), environments finished on every rank") if world > 1 else
+                        "tn_hvp_environments",
+              "broadcast_ms": t_bc if world > 1 else 0.0,
+              "broadcast_bytes": int(eng.primal_bytes) if world > 1 else 0,
+              "broadcast": "whole-store NCCL broadcast from rank 0 (the unsplit alternative), timed for reference",
+              "apply_ms": t_ap,
               "gather_ms": t_ga if world > 1 else 0.0, "directions_per_rank": cnt,
               "apply_only_hvps_per_s": B / (t_ap / 1e3),
               "apply_only": "SURVEY.md §8(d) HVPs/s: B directions / max-over-ranks apply time of the rank shares, "
@@ -493,8 +497,9 @@ def main():
         "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": cfg.name, "n": cfg.n, "depth": cfg.depth, "chi": cfg.chi, "gates": K,
                    "directions_per_step": B, "sub_batch": mb,
-                   "parallelism": ("strong: primal once on rank 0 + NCCL broadcast of the store, "
-                                   f"{B}/{world} directions per rank, NCCL all_gather of Hess_R") if world > 1
+                   "parallelism": ("strong: primal once, its two sweeps split over ranks 0/1 with an NCCL "
+                                   f"exchange of the store regions, {B}/{world} directions per rank, NCCL "
+                                   "all_gather of Hess_R") if world > 1
                                   else "1 GPU",
                    "step": ("parallel.sharded_step" if world > 1 else
                             "tn_hvp_environments + tn_hvp_apply" if args.unfused else

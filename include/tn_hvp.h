@@ -231,6 +231,25 @@ tn_status tn_mpo_tebd(int32_t n_sites, int32_t n_gates, const int32_t* sites, co
  * one device (N1 samples).  Takes effect at the next primal pass. */
 tn_status tn_hvp_set_cache_budget(tn_hvp_ctx* ctx, size_t bytes);
 
+/* ---- split primal pass (a10, multi-GPU) ------------------------
+ * The two primal sweeps are independent (a2 bottom, a3 top), so two ranks can
+ * run one each and exchange their halves of the store:
+ * tn_hvp_environments_part(part 0 | 1): the bottom (0) or top (1) sweep at
+ *   gates (DEVICE [K][4][4]) on `stream`, writing only that side's region of the
+ *   store (tn_hvp_primal_region) and its diagnostics; invalidates the point;
+ *   synchronises (solver status).
+ * tn_hvp_primal_region(part): byte offset and size of that side's region inside
+ *   the primal store (for a collective on a slice of the caller-owned buffer).
+ * tn_hvp_environments_finish: once both regions hold the sweeps at `gates`
+ *   (computed here or received), the layer environments, E_k, T, f and grad_R
+ *   as tn_hvp_environments would produce them (scalars_out as there, with the
+ *   fallback / deflation counts left 0); the point is then valid for apply.
+ *   Synchronises. */
+tn_status tn_hvp_environments_part(tn_hvp_ctx* ctx, const void* gates, int32_t part, void* stream);
+tn_status tn_hvp_primal_region(tn_hvp_ctx* ctx, int32_t part, size_t* offset, size_t* bytes);
+tn_status tn_hvp_environments_finish(tn_hvp_ctx* ctx, const void* gates, void* scalars_out, void* grad_R_out,
+                                     void* stream);
+
 /* Release the per-point caches and CUDA graphs (the next apply rebuilds them)
  * and return the library pool's unused device memory to the device, e.g.
  * before the caller allocates large buffers of its own.  Synchronises. */

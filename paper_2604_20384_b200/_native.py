@@ -20,7 +20,8 @@ EXPORTS = ["tn_hvp_num_gates", "tn_hvp_setup", "tn_hvp_environments", "tn_hvp_ap
            "tn_hvp_launch_count", "tn_gemm_profile", "tn_pauli_basis", "tn_pauli_coords", "tn_sym_eig",
            "tn_hvp_ti_environments", "tn_hvp_ti_apply", "tn_hvp_step", "tn_hvp_query", "tn_hvp_trim_memory",
            "tn_hvp_set_product_state", "tn_hvp_set_reference", "tn_mpo_tebd",
-           "tn_hvp_set_cache_budget",
+           "tn_hvp_set_cache_budget", "tn_hvp_environments_part", "tn_hvp_environments_finish",
+           "tn_hvp_primal_region",
            "tn_hvp_destroy", "tn_hvp_last_error"]
 TN_C128, TN_C64 = 0, 1
 TN_CHECK_UNITARY, TN_CHECK_TANGENT = 1, 2
@@ -64,6 +65,9 @@ def lib():
         L.tn_hvp_set_product_state.argtypes = [vp, vp, vp]
         L.tn_hvp_set_reference.argtypes = [vp, vp, vp]
         L.tn_hvp_set_cache_budget.argtypes = [vp, C.c_size_t]
+        L.tn_hvp_environments_part.argtypes = [vp, vp, i32, vp]
+        L.tn_hvp_environments_finish.argtypes = [vp, vp, vp, vp, vp]
+        L.tn_hvp_primal_region.argtypes = [vp, i32, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]
         L.tn_mpo_tebd.argtypes = [i32, i32, C.POINTER(i32), vp, i32, C.c_double, i32, C.POINTER(i32), vp,
                                   C.c_size_t, vp]
         L.tn_hvp_environments.argtypes = [vp, vp, vp, vp, vp]
@@ -89,7 +93,8 @@ def lib():
         for name in ("tn_retract", "tn_tangent_dot", "tn_tangent_axpby", "tn_hvp_primal_copy", "tn_pauli_basis",
                      "tn_pauli_coords", "tn_sym_eig", "tn_hvp_ti_environments", "tn_hvp_ti_apply",
                      "tn_hvp_step", "tn_hvp_query", "tn_hvp_trim_memory", "tn_hvp_set_product_state",
-                     "tn_hvp_set_reference", "tn_mpo_tebd", "tn_hvp_set_cache_budget"):
+                     "tn_hvp_set_reference", "tn_mpo_tebd", "tn_hvp_set_cache_budget",
+                     "tn_hvp_environments_part", "tn_hvp_environments_finish", "tn_hvp_primal_region"):
             getattr(L, name).restype = C.c_int
         L.tn_hvp_launch_count.argtypes = []
         L.tn_hvp_launch_count.restype = C.c_int64
@@ -264,3 +269,19 @@ def tn_mpo_tebd(n, sites, gates_ptr, chi, tol, device, out_ptr, capacity, stream
 
 def tn_hvp_set_cache_budget(ctx, nbytes):
     check(lib().tn_hvp_set_cache_budget(ctx, C.c_size_t(int(nbytes))), ctx)
+
+
+def tn_hvp_environments_part(ctx, gates_ptr, part, stream):
+    check(lib().tn_hvp_environments_part(ctx, C.c_void_p(gates_ptr), part, C.c_void_p(stream)), ctx)
+
+
+def tn_hvp_environments_finish(ctx, gates_ptr, scalars_ptr, grad_R_ptr, stream):
+    check(lib().tn_hvp_environments_finish(ctx, C.c_void_p(gates_ptr), C.c_void_p(scalars_ptr),
+                                           C.c_void_p(grad_R_ptr), C.c_void_p(stream)), ctx)
+
+
+def tn_hvp_primal_region(ctx, part):
+    """-> (byte offset, bytes) of side `part` (0 bottom, 1 top) inside the primal store."""
+    o, b = C.c_size_t(), C.c_size_t()
+    check(lib().tn_hvp_primal_region(ctx, part, C.byref(o), C.byref(b)), ctx)
+    return o.value, b.value

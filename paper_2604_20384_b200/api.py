@@ -140,6 +140,22 @@ class HVPEngine:
     def primal_blob(self):
         return N.tn_hvp_primal_blob(self.ctx)
 
+    def environments_part(self, gates: torch.Tensor, part: int):
+        """Split primal: the bottom (0) or top (1) sweep only, into its store region."""
+        _require_cuda(gates, "gates")
+        N.tn_hvp_environments_part(self.ctx, gates.data_ptr(), part, _stream())
+
+    def primal_region(self, part: int):
+        """(byte offset, bytes) of side `part` inside the primal store."""
+        return N.tn_hvp_primal_region(self.ctx, part)
+
+    def environments_finish(self, gates: torch.Tensor):
+        """Split primal: layer environments, E, f, grad_R once both regions are in place."""
+        _require_cuda(gates, "gates")
+        gR = torch.empty(self.K, 4, 4, dtype=torch.complex128, device=self.device)
+        N.tn_hvp_environments_finish(self.ctx, gates.data_ptr(), self.scalars.data_ptr(), gR.data_ptr(), _stream())
+        return self.scalars, gR
+
     def primal_store(self) -> torch.Tensor:
         """The primal store itself (uint8, tn_hvp_primal_blob's bytes; no copy)."""
         return self.primal[: self.primal_bytes]

@@ -143,6 +143,26 @@ tn_status tn_hvp_set_cache_budget(tn_hvp_ctx* ctx, size_t bytes) {
   return guarded(ctx, [&] { tn::engine_set_cache_budget(ctx, bytes); });
 }
 
+tn_status tn_hvp_environments_part(tn_hvp_ctx* ctx, const void* gates, int32_t part, void* stream) {
+  if (!ctx || !gates || (part != 0 && part != 1)) return fail(ctx, TN_EINVAL, "tn_hvp_environments_part: bad argument");
+  return guarded(ctx, [&] { tn::engine_environments_part(ctx, (const tn::cplx*)gates, part, (cudaStream_t)stream); });
+}
+
+tn_status tn_hvp_environments_finish(tn_hvp_ctx* ctx, const void* gates, void* scalars_out, void* grad_R_out,
+                                     void* stream) {
+  if (!ctx || !gates || !scalars_out) return fail(ctx, TN_EINVAL, "tn_hvp_environments_finish: null argument");
+  return guarded(ctx, [&] {
+    tn::engine_environments_finish(ctx, (const tn::cplx*)gates, (double*)scalars_out, (tn::cplx*)grad_R_out,
+                                   (cudaStream_t)stream);
+  });
+}
+
+tn_status tn_hvp_primal_region(tn_hvp_ctx* ctx, int32_t part, size_t* offset, size_t* bytes) {
+  if (!ctx || !offset || !bytes || (part != 0 && part != 1))
+    return fail(ctx, TN_EINVAL, "tn_hvp_primal_region: bad argument");
+  return guarded(ctx, [&] { tn::engine_primal_region(ctx, part, offset, bytes); });
+}
+
 tn_status tn_hvp_trim_memory(tn_hvp_ctx* ctx, void* stream) {
   if (!ctx) return fail(nullptr, TN_EINVAL, "tn_hvp_trim_memory: null context");
   return guarded(ctx, [&] { tn::engine_trim_memory(ctx, (cudaStream_t)stream); });

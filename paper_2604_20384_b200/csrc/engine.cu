@@ -147,6 +147,9 @@ struct Engine {
   size_t arena_bytes = 0;
   bool own_arena = true;  // false: caller-owned primal_buf (tn_hvp_setup)
   size_t o_gates = 0, o_gdag = 0, o_E = 0, o_gradf = 0, o_scal = 0, o_diag = 0;
+  // side regions of the store (split primal over two ranks): [o_side[0], o_side[1])
+  // = bottom sweep (its diagnostics, snapshots, replay data), [o_side[1], o_side[2]) = top
+  size_t o_side[3] = {0, 0, 0}, o_sdiag[2] = {0, 0};
   std::vector<std::vector<size_t>> o_L, o_R;  // per layer, per cut
   std::vector<double> h_s;                    // host copy of the frozen factors
   cplx* ref = nullptr;                        // reference MPO copy (device)
@@ -379,6 +382,9 @@ struct Engine {
     o_diag = take(8 * sizeof(double));
     int s_index = 0;
     for (SidePlan* sp : {&bot, &top}) {
+      const int side = sp == &top;
+      o_side[side] = o;
+      o_sdiag[side] = take(8 * sizeof(double));
       sp->o_snap.clear();
       for (const Bonds& b : sp->snap) {
         std::vector<size_t> offs(n);
@@ -399,6 +405,7 @@ struct Engine {
           }
         }
     }
+    o_side[2] = o;
     // layer environments L0/R0: layer ell uses T_ell (top snapshot index D-ell) and B_{ell-1} (bottom index ell-1)
     o_L.assign(D + 1, std::vector<size_t>(n + 1, 0));
     o_R.assign(D + 1, std::vector<size_t>(n + 1, 0));
@@ -1331,6 +1338,8 @@ struct Engine {
       TN_CUDA(cudaStreamWaitEvent(st, ev_joing, 0));
     }
     combine_diag(st, at<double>(o_diag), dg);
+    TN_CUDA(cudaMemcpyAsync(at<double>(o_sdiag[0]), dg, 8 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    TN_CUDA(cudaMemcpyAsync(at<double>(o_sdiag[1]), dg + 8, 8 * sizeof(double), cudaMemcpyDeviceToDevice, st));
     // T = <<T_0|B_0>>  (Alg. 1)
     cplx* T11 = overlap(st, pool, snap_ptrs(top, D), top.snap[D].p, snap_ptrs(bot, 0), bot.snap[0].p);
     finish_cost(st, at<double>(o_scal), T11);
@@ -1361,6 +1370,63 @@ struct Engine {
     TN_CUDA(cudaMemcpyAsync(at<double>(o_scal), sc, 8 * sizeof(double), cudaMemcpyHostToDevice, st));
     TN_CUDA(cudaStreamSynchronize(st));
     work_primal = work_counter.load() - wc0;
+    primal_valid = true;
+  }
+
+  // ---- split primal (multi-GPU): one side's sweep per rank, then finish ----
+  // part 0: bottom sweep (a2), part 1: top sweep (a3), each on the caller's
+  // stream, writing only that side's region of the store and its diagnostics.
+  void environments_part(cudaStream_t st, const cplx* gates, int part) {
+    TN_CUDA(cudaSetDevice(device));
+    check_gates(st, gates, K);
+    invalidate(st);
+    TN_CUDA(cudaMemcpyAsync(at(o_gates), gates, (size_t)K * 16 * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+    dagger4(st, at(o_gdag), at(o_gates), K);
+    Pool pool(st);
+    int* info = (int*)pool.raw(2 * sizeof(int));
+    TN_CUDA(cudaMemsetAsync(info, 0, 2 * sizeof(int), st));
+    double* dg = at<double>(o_sdiag[part]);
+    double hdiag[8] = {0, 1.0, 0, 0, 0, 0, 0, 0};
+    TN_CUDA(cudaMemcpyAsync(dg, hdiag, sizeof(hdiag), cudaMemcpyHostToDevice, st));
+    Mps last = primal_side(st, sol[0], pool, part == 1, true, info, dg);
+    for (cplx*& p : last.a) ddel(p, st);
+    int hinfo[2];
+    TN_CUDA(cudaMemcpyAsync(hinfo, info, sizeof(hinfo), cudaMemcpyDeviceToHost, st));
+    TN_CUDA(cudaStreamSynchronize(st));
+    if (hinfo[0] || hinfo[1]) throw NumericError("cuSOLVER info nonzero in the split primal sweep");
+  }
+
+  // After both side regions hold this point's sweeps (local or received):
+  // layer environments, E, T, f, grad_R -- the rest of tn_hvp_environments.
+  void environments_finish(cudaStream_t st, const cplx* gates, double* scalars, cplx* grad_R) {
+    TN_CUDA(cudaSetDevice(device));
+    invalidate(st);
+    TN_CUDA(cudaMemcpyAsync(at(o_gates), gates, (size_t)K * 16 * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+    dagger4(st, at(o_gdag), at(o_gates), K);
+    Pool pool(st);
+    layer_gradients(st);
+    double* dg = (double*)pool.raw(16 * sizeof(double));
+    TN_CUDA(cudaMemcpyAsync(dg, at<double>(o_sdiag[0]), 8 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    TN_CUDA(cudaMemcpyAsync(dg + 8, at<double>(o_sdiag[1]), 8 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    combine_diag(st, at<double>(o_diag), dg);
+    cplx* T11 = overlap(st, pool, snap_ptrs(top, D), top.snap[D].p, snap_ptrs(bot, 0), bot.snap[0].p);
+    finish_cost(st, at<double>(o_scal), T11);
+    gradient_post(st, K, at(o_gates), at(o_E), at<double>(o_scal), at(o_gradf), grad_R);
+    for (SidePlan* sp : {&bot, &top})
+      for (auto& ls : sp->steps)
+        for (Step& x : ls)
+          if (x.type == PAIR)
+            TN_CUDA(cudaMemcpyAsync(&h_s[x.s_index], at<double>(x.o_s), sizeof(double), cudaMemcpyDeviceToHost, st));
+    double sc[8];
+    TN_CUDA(cudaMemcpyAsync(sc, at<double>(o_scal), 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    TN_CUDA(cudaMemcpyAsync(sc + 3, at<double>(o_diag), 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    TN_CUDA(cudaStreamSynchronize(st));
+    for (int j = 0; j < 6; ++j)
+      if (!std::isfinite(sc[j])) throw NumericError("non-finite primal scalar after the split primal");
+    sc[6] = sc[7] = 0.0;  // fallback / deflation counts stay with the ranks that swept
+    TN_CUDA(cudaMemcpyAsync(scalars, sc, 8 * sizeof(double), cudaMemcpyHostToDevice, st));
+    TN_CUDA(cudaMemcpyAsync(at<double>(o_scal), sc, 8 * sizeof(double), cudaMemcpyHostToDevice, st));
+    TN_CUDA(cudaStreamSynchronize(st));
     primal_valid = true;
   }
 
@@ -2428,6 +2494,17 @@ void engine_set_reference(tn_hvp_ctx* ctx, const cplx* ref, cudaStream_t st) {
   TN_CUDA(cudaMemcpyAsync(e.ref, ref, sizeof(cplx) * el, cudaMemcpyDeviceToDevice, st));
 }
 void engine_set_cache_budget(tn_hvp_ctx* ctx, size_t bytes) { ctx->e.cache_budget = bytes; }
+void engine_environments_part(tn_hvp_ctx* ctx, const cplx* gates, int part, cudaStream_t st) {
+  ctx->e.environments_part(st, gates, part);
+}
+void engine_environments_finish(tn_hvp_ctx* ctx, const cplx* gates, double* scalars, cplx* grad_R,
+                                cudaStream_t st) {
+  ctx->e.environments_finish(st, gates, scalars, grad_R);
+}
+void engine_primal_region(tn_hvp_ctx* ctx, int part, size_t* offset, size_t* bytes) {
+  *offset = ctx->e.o_side[part];
+  *bytes = ctx->e.o_side[part + 1] - ctx->e.o_side[part];
+}
 void engine_trim_memory(tn_hvp_ctx* ctx, cudaStream_t st) {
   TN_CUDA(cudaSetDevice(ctx->e.device));
   ctx->e.trim_memory(st);

@@ -26,6 +26,9 @@ void engine_primal_imported(tn_hvp_ctx* ctx, const cplx* gates, cudaStream_t st)
 void engine_primal_copy(tn_hvp_ctx* ctx, void* buf, size_t bytes, int into_ctx, cudaStream_t st);
 void engine_trim_memory(tn_hvp_ctx* ctx, cudaStream_t st);
 void engine_set_cache_budget(tn_hvp_ctx* ctx, size_t bytes);
+void engine_environments_part(tn_hvp_ctx* ctx, const cplx* gates, int part, cudaStream_t st);
+void engine_environments_finish(tn_hvp_ctx* ctx, const cplx* gates, double* scalars, cplx* grad_R, cudaStream_t st);
+void engine_primal_region(tn_hvp_ctx* ctx, int part, size_t* offset, size_t* bytes);
 void engine_tebd(int n, int ngates, const int32_t* sites, const cplx* gates, int chi, double tol, int device,
                  int32_t* bonds_out, cplx* out, size_t cap, cudaStream_t st);
 void engine_set_product_state(tn_hvp_ctx* ctx, const cplx* psi, cudaStream_t st);

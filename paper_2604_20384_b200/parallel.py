@@ -9,11 +9,15 @@ HVP is exchanged; the collectives here are outside the hot loop:
   * broadcast_primal(eng, gates, src) -- primal store of rank `src` to all
                                         ranks, in place (one primal pass, many
                                         ranks applying);
+  * split_primal(eng, gates)          -- bottom sweep on rank 0, top sweep on
+                                        rank 1, both store regions broadcast,
+                                        environments finished on every rank;
   * sharded_step(eng, gates, dirs)    -- the strong-scaling step bench.py
-                                        times for N > 1: primal once, broadcast,
+                                        times for N > 1: primal once (split),
                                         B/N directions per rank, all_gather.
 Every function only needs the engine's methods (environments, apply,
-primal_store, invalidate_primal, primal_imported, scalars), so the CPU tests
+primal_store, invalidate_primal, primal_imported, environments_part,
+primal_region, environments_finish, scalars), so the CPU tests
 drive the same choreography over gloo with a stand-in engine.
 """
 from __future__ import annotations
@@ -67,20 +71,48 @@ def broadcast_primal(eng, gates: torch.Tensor, src: int = 0, group=None):
     return buf
 
 
-def sharded_step(eng, gates: torch.Tensor, dirs: torch.Tensor, src: int = 0, group=None, out=None):
+def split_primal(eng, gates: torch.Tensor, group=None):
+    """The primal pass over two ranks: rank 0 runs the bottom
+    sweep and rank 1 the top sweep at the same time, each writing its side's
+    region of the primal store; both regions are broadcast in place (bottom
+    from rank 0, top from rank 1) to every rank, which then finishes the pass
+    (layer environments, E, f, grad_R) on its own GPU.  One GPU: the ordinary
+    primal pass.  Returns (scalars, grad_R)."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world < 2:
+        return eng.environments(gates)
+    rank = dist.get_rank(group)
+    if rank < 2:
+        eng.environments_part(gates, rank)
+    else:
+        eng.invalidate_primal()
+    store = eng.primal_store()
+    for part in (0, 1):
+        off, nbytes = eng.primal_region(part)
+        dist.broadcast(store[off:off + nbytes], src=part, group=group)
+    return eng.environments_finish(gates)
+
+
+def sharded_step(eng, gates: torch.Tensor, dirs: torch.Tensor, src: int = 0, group=None, out=None,
+                 split: bool = True):
     """One strong-scaling step of the hot path (north_star):
-    the primal pass once on rank `src` (eng.environments), its store broadcast
-    in place to every rank (broadcast_primal), each rank applying its
+    the primal pass once -- split over ranks 0 and 1 (split_primal: the two
+    sweeps at the same time, their store regions broadcast, every rank
+    finishing the environments), or with split=False on rank `src` with the
+    whole store broadcast in place (broadcast_primal) -- each rank applying its
     contiguous share of the B directions (shard), the Riemannian HVPs
     all-gathered in direction order (gather_rows).  Every rank passes the same
     gates and all B directions; returns (scalars [8], Hess_R [B, K, 4, 4]) on
     every rank (scalars broadcast from `src`).  `out`: optional [B,K,4,4]
     buffer for the gathered result."""
     rank, world = dist.get_rank(group), dist.get_world_size(group)
-    if rank == src:
-        eng.environments(gates)
-    broadcast_primal(eng, gates, src, group)
-    dist.broadcast(eng.scalars, src=src, group=group)
+    if split and world >= 2:
+        split_primal(eng, gates, group)          # every rank ends with the full store
+    else:
+        if rank == src:
+            eng.environments(gates)
+        broadcast_primal(eng, gates, src, group)
+        dist.broadcast(eng.scalars, src=src, group=group)
     B = dirs.shape[0]
     start, count = shard(B, rank, world)
     if count:

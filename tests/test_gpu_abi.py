@@ -116,3 +116,25 @@ def test_graph_replay_follows_new_directions():
         rel = (outs[j] - full[j:j + 1]).norm() / full[j].norm()
         assert rel < 1e-13, (j, float(rel))
     assert not torch.equal(outs[2], outs[3])
+
+
+def test_split_primal_two_contexts_equal_full_pass():
+    """The split primal of parallel.split_primal emulated with two contexts on
+    one GPU (no rank waits on another): context A sweeps the bottom side,
+    context B the top side, each copies the other's store region, both finish
+    -- f, grad_R and the HVPs equal one full tn_hvp_environments pass."""
+    eng, G, V = _setup(309, n=8, depth=5, chi=8, batch=2)
+    engB, _, _ = _setup(309, n=8, depth=5, chi=8, batch=2)
+    sc, gR = eng.environments(G)
+    sc, gR = sc.clone(), gR.clone()
+    H = eng.apply(V).clone()
+    A, Bc = _setup(309, n=8, depth=5, chi=8, batch=2)[0], engB
+    A.environments_part(G, 0)
+    Bc.environments_part(G, 1)
+    for src, dst, part in ((A, Bc, 0), (Bc, A, 1)):
+        off, nb = src.primal_region(part)
+        dst.primal_store()[off:off + nb].copy_(src.primal_store()[off:off + nb])
+    for e in (A, Bc):
+        s2, g2 = e.environments_finish(G)
+        assert torch.equal(s2[:6], sc[:6]) and torch.equal(g2, gR)
+        assert torch.equal(e.apply(V), H)

@@ -60,24 +60,41 @@ def test_gather_rows_world2_gloo(total):
 
 
 class _StandInEngine:
-    """Host-side stand-in of api.HVPEngine for the CPU choreography test: the
-    'primal store' is a function of the gates, apply needs a valid store."""
+    """Host-side stand-in of api.HVPEngine for the CPU choreography tests: the
+    'primal store' (uint8, like the real one) is a function of the gates, its
+    two halves are the bottom / top sweep regions, apply needs a valid store."""
 
     def __init__(self):
-        self.store = torch.zeros(8, dtype=torch.float64)
+        self.store = torch.zeros(64, dtype=torch.uint8)
         self.scalars = torch.zeros(8, dtype=torch.float64)
         self.valid = False
         self.calls = []
 
     @staticmethod
     def _primal(gates):
-        return gates.real.reshape(-1)[:8].clone() + 1.0
+        return (gates.real.reshape(-1)[:8].clone() + 1.0).view(torch.uint8)
 
     def environments(self, gates):
         self.calls.append("environments")
         self.store.copy_(self._primal(gates))
-        self.scalars.copy_(2 * self.store)
+        self.scalars.copy_(2 * self.store.view(torch.float64))
         self.valid = True
+
+    def environments_part(self, gates, part):
+        self.calls.append(f"part{part}")
+        self.valid = False
+        off, nb = self.primal_region(part)
+        self.store[off:off + nb] = self._primal(gates)[off:off + nb]
+
+    def primal_region(self, part):
+        return (0, 32) if part == 0 else (32, 32)
+
+    def environments_finish(self, gates):
+        self.calls.append("finish")
+        assert torch.equal(self.store, self._primal(gates)), "store regions do not match the point"
+        self.scalars.copy_(2 * self.store.view(torch.float64))
+        self.valid = True
+        return self.scalars, None
 
     def primal_store(self):
         return self.store
@@ -94,10 +111,10 @@ class _StandInEngine:
     def apply(self, dirs):
         assert self.valid
         self.calls.append(f"apply{dirs.shape[0]}")
-        return dirs * complex(float(self.store.sum()), 0.5)
+        return dirs * complex(float(self.store.view(torch.float64).sum()), 0.5)
 
 
-def _step_worker(rank, world, port, B, q):
+def _step_worker(rank, world, port, B, split, q):
     from paper_2604_20384_b200.parallel import sharded_step
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -105,32 +122,48 @@ def _step_worker(rank, world, port, B, q):
     gates = torch.randn(5, 4, 4, dtype=torch.complex128, generator=g)
     dirs = torch.randn(B, 5, 4, 4, dtype=torch.complex128, generator=g)
     eng = _StandInEngine()
-    sc, full = sharded_step(eng, gates, dirs)
-    want = dirs * complex(float(_StandInEngine._primal(gates).sum()), 0.5)
-    q.put((rank, bool(torch.equal(full, want)), bool(torch.equal(sc, 2 * _StandInEngine._primal(gates))),
-           eng.calls))
+    sc, full = sharded_step(eng, gates, dirs, split=split)
+    p = _StandInEngine._primal(gates).view(torch.float64)
+    want = dirs * complex(float(p.sum()), 0.5)
+    q.put((rank, bool(torch.equal(full, want)), bool(torch.equal(sc, 2 * p)), eng.calls))
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("B", [5, 1])
-def test_sharded_step_world2_gloo(B):
-    """primal once on rank 0 -> in-place broadcast of the store -> import
-    check on rank 1 -> B/2 directions per rank -> all_gather in order."""
+def _run(world, B, split):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_step_worker, args=(r, 2, port, B, q)) for r in range(2)]
+    procs = [ctx.Process(target=_step_worker, args=(r, world, port, B, split, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = sorted([q.get(timeout=120) for _ in range(2)])
+    res = sorted([q.get(timeout=120) for _ in range(world)])
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    (r0, ok0, sc0, calls0), (r1, ok1, sc1, calls1) = res
+    return res
+
+
+@pytest.mark.parametrize("B", [5, 1])
+def test_sharded_step_broadcast_world2_gloo(B):
+    """split=False: primal once on rank 0 -> in-place broadcast of the whole
+    store -> import check on rank 1 -> B/2 directions per rank -> all_gather."""
+    (r0, ok0, sc0, calls0), (r1, ok1, sc1, calls1) = _run(2, B, False)
     assert ok0 and ok1 and sc0 and sc1
     assert calls0[0] == "environments" and "imported" not in calls0
     assert calls1[:2] == ["invalidate", "imported"] and "environments" not in calls1
     n0 = (B + 1) // 2
     assert calls0[-1] == f"apply{n0}"
     assert (calls1[-1] == f"apply{B - n0}") if B - n0 else calls1[-1] == "imported"
+
+
+def test_sharded_step_split_primal_world3_gloo():
+    """split=True (the default): bottom sweep on rank 0, top sweep on rank 1,
+    both store regions broadcast, every rank finishes the environments itself
+    (rank 2 only receives), then 7 directions in shares 3/2/2 and all_gather."""
+    res = _run(3, 7, True)
+    for rank, ok, sc, calls in res:
+        assert ok and sc, rank
+        assert calls[-2] == "finish" and "environments" not in calls and "imported" not in calls
+    assert res[0][3][0] == "part0" and res[1][3][0] == "part1" and res[2][3][0] == "invalidate"
+    assert [c[-1] for _, _, _, c in res] == ["apply3", "apply2", "apply2"]
