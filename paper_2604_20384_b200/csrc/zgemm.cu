@@ -304,10 +304,11 @@ cudaMemPool_t device_pool(int dev) {
     cudaMemPool_t p = nullptr;
     TN_CUDA(cudaMemPoolCreate(&p, &props));
     uint64_t thr = UINT64_MAX;
-    int off = 0, on = 1;
+    int off = 0;
     TN_CUDA(cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr));
     // a block freed on one stream may serve another stream only when that
     // costs no new dependency (already ordered, or the free has completed)
+    int on = 1;  // measured at C3: 3.08 s per step with these two on, 3.20 s with them off
     TN_CUDA(cudaMemPoolSetAttribute(p, cudaMemPoolReuseFollowEventDependencies, &on));
     TN_CUDA(cudaMemPoolSetAttribute(p, cudaMemPoolReuseAllowOpportunistic, &on));
     TN_CUDA(cudaMemPoolSetAttribute(p, cudaMemPoolReuseAllowInternalDependencies, &off));
