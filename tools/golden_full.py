@@ -34,9 +34,13 @@ from tn_inputs import configs as C  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--case", default="c4", choices=sorted(C.FULL_PARITY_CASES))
 ap.add_argument("--dirs", type=int, default=2)
+ap.add_argument("--only", type=int, default=None,
+                help="compute just direction ONLY (its tangent alone in the sweeps) -> full_<case>_d<ONLY>.npz")
 a = ap.parse_args()
 
-cfg, G, V = C.full_parity_inputs(a.case, a.dirs)
+cfg, G, V = C.full_parity_inputs(a.case, a.dirs if a.only is None else a.only + 1)
+if a.only is not None:
+    V = V[a.only:a.only + 1]
 t0 = time.time()
 ref = [x.detach().resolve_conj().cpu().numpy() for x in C.reference_mpo(cfg, device="cpu")]
 t_ref = time.time() - t0
@@ -50,17 +54,20 @@ gR = cm.riemannian_gradient(G, gf)
 t_env = time.time() - t1
 print(json.dumps({"case": a.case, "t_primal_s": t_primal, "t_env_s": t_env, "f": f}), flush=True)
 HR, t_dirs = [], []
-for b in range(a.dirs):
+for b in range(V.shape[0]):
     tb = time.time()
     Hf, _ = cm.postprocess_hvp(o.T, E, o.hvp_T(b), V[b])
     HR.append(cm.riemannian_hvp(G, gf, Hf, V[b]))
     t_dirs.append(time.time() - tb)
     print(json.dumps({"case": a.case, "dir": b, "t_s": t_dirs[-1]}), flush=True)
-out = os.path.join(ROOT, "tests", "golden", f"full_{a.case}.npz")
-np.savez_compressed(out, f=f, T=o.T, grad_R=gR, HR=np.array(HR).reshape(a.dirs, -1, 4, 4),
+out = os.path.join(ROOT, "tests", "golden",
+                   f"full_{a.case}.npz" if a.only is None else f"full_{a.case}_d{a.only}.npz")
+np.savez_compressed(out, f=f, T=o.T, grad_R=gR, HR=np.array(HR).reshape(V.shape[0], -1, 4, 4),
                     ref_bonds=np.array(C.ref_fingerprint(ref)[0]), ref_norms=C.ref_fingerprint(ref)[1])
-meta = {"case": a.case, "config": cfg.name, "n": cfg.n, "depth": cfg.depth, "chi": cfg.chi, "dirs": a.dirs,
-        "command": f"python tools/golden_full.py --case {a.case} --dirs {a.dirs}",
+meta = {"case": a.case, "config": cfg.name, "n": cfg.n, "depth": cfg.depth, "chi": cfg.chi,
+        "dirs": V.shape[0], "first_dir": 0 if a.only is None else a.only,
+        "command": f"python tools/golden_full.py --case {a.case} " + (f"--dirs {a.dirs}" if a.only is None
+                                                                       else f"--only {a.only}"),
         "oracle": "oracle/mpo.py MPOOracle (O3), oracle/common.py postprocessing",
         "definition": "truncated fixed-projector HVP, SURVEY.md 8(c.2), readings X7-X9; PAPER.md:1019-1023",
         "t_reference_s": t_ref, "t_primal_s": t_primal, "t_env_s": t_env, "t_dir_s": t_dirs,
