@@ -131,14 +131,19 @@ tn_status tn_hvp_environments(tn_hvp_ctx* ctx, const void* gates, void* scalars_
  * hess_R_out: DEVICE [batch][K][4][4].
  * aux_out: DEVICE, nullable: [batch][K][4][4] H_T (Wirtinger HVP of T)
  *   followed by [batch] complex Omega.
- * Per-point reuse (results are bitwise those of a cold call): the first call
- * after a primal pass records the direction-independent tensors (tangent
- * chains; layer-HVP block tensors within a third of the then-free memory)
- * and later calls borrow them; a second call with the same (batch <= 8, aux
- * present or not) is captured into a CUDA graph and replayed from then on.
- * All of it is released by the next tn_hvp_environments / tn_hvp_step /
- * tn_hvp_primal_imported and by tn_hvp_destroy.  Environment switches read at
- * setup / load: TN_NO_CHAIN_CACHE=1, TN_NO_GRAPH=1. */
+ * Graphs and per-point reuse (results are bitwise those of a cold eager
+ * call): the first call at a point replays a point-free CUDA graph of the
+ * whole apply (captured once per (batch, aux) for the context's lifetime; the
+ * frozen truncation factors are read from the store on the device) when its
+ * graph-owned working memory is small (launch-bound configurations); the
+ * second call records the direction-independent tensors (tangent chains;
+ * layer-HVP block tensors within a third of the then-free memory, or the cap
+ * of tn_hvp_set_cache_budget) and later calls borrow them; a third call with
+ * the same (batch <= 8, aux) is captured into a point-specific graph that
+ * replays the cached tensors.  Point-specific state is released by the next
+ * primal pass; point-free graphs by tn_hvp_trim_memory and tn_hvp_destroy.
+ * Environment switches read at setup / load: TN_NO_CHAIN_CACHE=1,
+ * TN_NO_GRAPH=1. */
 tn_status tn_hvp_apply(tn_hvp_ctx* ctx, int32_t batch, const void* dirs, void* hess_R_out, void* aux_out,
                        void* stream);
 

@@ -54,8 +54,10 @@ void pool_trim(int device);
 // Batched row-major complex GEMM on DMMA (zgemm.cu).
 // C[b] = alpha * op(A[b]) * op(B[b]) + beta * C[b]; op(A): M x K, op(B): K x N.
 // opa/opb in {'N','T','C'}; strides in elements, 0 = operand shared.
+// dscale (nullable, DEVICE): alpha and beta are multiplied by *dscale in the
+// epilogue (a scalar known only on the device, e.g. a frozen truncation factor).
 void zgemm(cudaStream_t st, char opa, char opb, int M, int N, int K, cplx alpha, const cplx* A, int64_t lda,
            int64_t sA, const cplx* B, int64_t ldb, int64_t sB, cplx beta, cplx* C, int64_t ldc, int64_t sC,
-           int batch);
+           int batch, const double* dscale = nullptr);
 
 }  // namespace tn

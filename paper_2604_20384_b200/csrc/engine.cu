@@ -64,7 +64,7 @@ struct Step {
   int abm = 0, ab0 = 0, ab1 = 0, ab2 = 0;
   int aam = 0, aa0 = 0, aa1 = 0, aa2 = 0;
   size_t o_theta = 0, o_uh = 0, o_vh = 0, o_S = 0, o_s = 0, o_q = 0;  // primal-arena offsets (bytes)
-  int s_index = -1;                                                  // index into host copy of s
+  int s_index = -1;                                                  // ordinal of the pair step
 };
 
 struct Bonds {
@@ -151,7 +151,6 @@ struct Engine {
   // = bottom sweep (its diagnostics, snapshots, replay data), [o_side[1], o_side[2]) = top
   size_t o_side[3] = {0, 0, 0}, o_sdiag[2] = {0, 0};
   std::vector<std::vector<size_t>> o_L, o_R;  // per layer, per cut
-  std::vector<double> h_s;                    // host copy of the frozen factors
   cplx* ref = nullptr;                        // reference MPO copy (device)
   std::vector<size_t> ref_off;
   // solvers: one per concurrent primal sweep (bottom on the caller's stream,
@@ -168,7 +167,7 @@ struct Engine {
   int lwork_geqrf = 0, lwork_ungqr = 0;
   cudaStream_t st2 = nullptr, st1 = nullptr;  // top / bottom sweep streams (non-blocking)
   cudaStream_t stg = nullptr;                 // layer gradients, overlapped with the sweeps
-  cudaStream_t stf = nullptr, sth = nullptr;  // fused step: forward tangents; host reads of s
+  cudaStream_t stf = nullptr, sth = nullptr;  // fused step: forward tangents; spare side stream
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join1 = nullptr, ev_joing = nullptr, ev_joinf = nullptr;
   std::vector<cudaEvent_t> ev_snap[2];        // per side: layer snapshot idx is in the arena
   bool primal_valid = false;
@@ -220,6 +219,7 @@ struct Engine {
   struct ApplyGraph {
     int batch = 0;
     bool aux = false;
+    bool point_free = false;  // captured without per-point caches: valid across primal passes
     int calls = 0;
     bool failed = false;
     cudaGraphExec_t exec = nullptr;
@@ -230,6 +230,8 @@ struct Engine {
   std::vector<ApplyGraph> graphs;
   cudaStream_t stc = nullptr;  // capture stream
   const bool graphs_enabled = std::getenv("TN_NO_GRAPH") == nullptr;
+  int applies_at_point = 0;     // tn_hvp_apply calls since the last primal pass
+  bool no_cache = false;        // a point-free capture is running: no chain cache, no memo
   static constexpr int kGraphMaxBatch = 8;
   double work_primal = 0, work_apply = 0, work_fwd_first = 0;
   std::atomic<double> work_counter{0.0};
@@ -243,27 +245,29 @@ struct Engine {
   }
 
   // ------------------------------------------------------------ GEMMs --
+  // ds (nullable, DEVICE): a and b are scaled by *ds in the GEMM epilogue
   void mm(cudaStream_t st, char oa, char ob, int M, int N, int Kd, cplx a, const cplx* A, int64_t lda, int64_t sA,
-          const cplx* B, int64_t ldb, int64_t sB, cplx b, cplx* C, int64_t ldc, int64_t sC, int batch) {
+          const cplx* B, int64_t ldb, int64_t sB, cplx b, cplx* C, int64_t ldc, int64_t sC, int batch,
+          const double* ds = nullptr) {
     if (M <= 0 || N <= 0 || batch <= 0) return;
     (g_fwd_thread ? work_counter_fwd : work_counter)
         .fetch_add((double)M * N * std::max(Kd, 0) * batch, std::memory_order_relaxed);
-    zgemm(st, oa, ob, M, N, Kd, a, A, lda, sA, B, ldb, sB, b, C, ldc, sC, batch);
+    zgemm(st, oa, ob, M, N, Kd, a, A, lda, sA, B, ldb, sB, b, C, ldc, sC, batch, ds);
   }
   // C(MxN) = a A(MxK) B(KxN) + b C
   void nn(cudaStream_t st, int M, int N, int Kd, const cplx* A, int64_t sA, const cplx* B, int64_t sB, cplx* C,
-          int64_t sC, int batch, cplx a = ONE, cplx b = ZERO) {
-    mm(st, 'N', 'N', M, N, Kd, a, A, Kd, sA, B, N, sB, b, C, N, sC, batch);
+          int64_t sC, int batch, cplx a = ONE, cplx b = ZERO, const double* ds = nullptr) {
+    mm(st, 'N', 'N', M, N, Kd, a, A, Kd, sA, B, N, sB, b, C, N, sC, batch, ds);
   }
   // C(MxN) = a A^H B, A stored (K x M), B (K x N)
   void cn(cudaStream_t st, int M, int N, int Kd, const cplx* A, int64_t sA, const cplx* B, int64_t sB, cplx* C,
-          int64_t sC, int batch, cplx a = ONE, cplx b = ZERO) {
-    mm(st, 'C', 'N', M, N, Kd, a, A, M, sA, B, N, sB, b, C, N, sC, batch);
+          int64_t sC, int batch, cplx a = ONE, cplx b = ZERO, const double* ds = nullptr) {
+    mm(st, 'C', 'N', M, N, Kd, a, A, M, sA, B, N, sB, b, C, N, sC, batch, ds);
   }
   // C(MxN) = a A B^H, A (M x K), B stored (N x K)
   void nc(cudaStream_t st, int M, int N, int Kd, const cplx* A, int64_t sA, const cplx* B, int64_t sB, cplx* C,
-          int64_t sC, int batch, cplx a = ONE, cplx b = ZERO) {
-    mm(st, 'N', 'C', M, N, Kd, a, A, Kd, sA, B, Kd, sB, b, C, N, sC, batch);
+          int64_t sC, int batch, cplx a = ONE, cplx b = ZERO, const double* ds = nullptr) {
+    mm(st, 'N', 'C', M, N, Kd, a, A, Kd, sA, B, Kd, sB, b, C, N, sC, batch, ds);
   }
 
   // ------------------------------------------------------------- plan --
@@ -418,7 +422,6 @@ struct Engine {
       }
     }
     arena_bytes = o;
-    h_s.assign(s_index, 1.0);
   }
 
   // Fresh device status word for one cuSOLVER call; fold it into `acc` afterwards.
@@ -596,7 +599,7 @@ struct Engine {
     }
     for (cudaStream_t x : {st1, st2, stg, stf, sth, stc})
       if (x) cudaStreamSynchronize(x);
-    drop_graphs(stc);
+    drop_graphs(stc, true);
     drop_chain_cache(stc);
     cudaStreamSynchronize(stc);
     if (d_init) cudaFree(d_init);
@@ -1178,6 +1181,7 @@ struct Engine {
     if (fwd_out) check_dirs(st, gates, fwd_V, fwd_nb);
     primal_valid = false;
     ti_valid = false;
+    applies_at_point = 0;
     drop_graphs(st);
     drop_chain_cache(st);
     n_fallback = 0;
@@ -1285,13 +1289,6 @@ struct Engine {
                 if (abort) throw std::runtime_error("fused step: primal pass failed");
               }
               TN_CUDA(cudaStreamWaitEvent(stf, ev_snap[0][li + 1], 0));
-              // the layer's frozen s (host scalars of tangent_step), read on a side stream
-              TN_CUDA(cudaStreamWaitEvent(sth, ev_snap[0][li + 1], 0));
-              for (const Step& s : bot.steps[li])
-                if (s.type == PAIR)
-                  TN_CUDA(cudaMemcpyAsync(&h_s[s.s_index], at<double>(s.o_s), sizeof(double),
-                                          cudaMemcpyDeviceToHost, sth));
-              TN_CUDA(cudaStreamSynchronize(sth));
             });
           } catch (...) {
             fwd_err = std::current_exception();
@@ -1344,12 +1341,7 @@ struct Engine {
     cplx* T11 = overlap(st, pool, snap_ptrs(top, D), top.snap[D].p, snap_ptrs(bot, 0), bot.snap[0].p);
     finish_cost(st, at<double>(o_scal), T11);
     gradient_post(st, K, at(o_gates), at(o_E), at<double>(o_scal), at(o_gradf), grad_R);
-    // host copies: scalars/diag, frozen s, solver info
-    for (SidePlan* sp : {&bot, &top})
-      for (auto& ls : sp->steps)
-        for (Step& s : ls)
-          if (s.type == PAIR)
-            TN_CUDA(cudaMemcpyAsync(&h_s[s.s_index], at<double>(s.o_s), sizeof(double), cudaMemcpyDeviceToHost, st));
+    // host copies: scalars/diag, solver info
     int hinfo[n_info];
     TN_CUDA(cudaMemcpyAsync(hinfo, info, sizeof(hinfo), cudaMemcpyDeviceToHost, st));
     double sc[8];
@@ -1412,11 +1404,6 @@ struct Engine {
     cplx* T11 = overlap(st, pool, snap_ptrs(top, D), top.snap[D].p, snap_ptrs(bot, 0), bot.snap[0].p);
     finish_cost(st, at<double>(o_scal), T11);
     gradient_post(st, K, at(o_gates), at(o_E), at<double>(o_scal), at(o_gradf), grad_R);
-    for (SidePlan* sp : {&bot, &top})
-      for (auto& ls : sp->steps)
-        for (Step& x : ls)
-          if (x.type == PAIR)
-            TN_CUDA(cudaMemcpyAsync(&h_s[x.s_index], at<double>(x.o_s), sizeof(double), cudaMemcpyDeviceToHost, st));
     double sc[8];
     TN_CUDA(cudaMemcpyAsync(sc, at<double>(o_scal), 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
     TN_CUDA(cudaMemcpyAsync(sc + 3, at<double>(o_diag), 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1613,7 +1600,7 @@ struct Engine {
   // Inside a stream capture only an already-built cache is used: recording
   // there would store graph-owned allocations in it.
   ChainCache* chain_cache_for(int side, cudaStream_t st) {
-    if (!chain_cache_enabled) return nullptr;
+    if (!chain_cache_enabled || no_cache) return nullptr;
     ChainCache& c = chain_cache[side];
     if (c.built) return &c;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -1648,7 +1635,7 @@ struct Engine {
   template <class F>
   cplx* memo(cudaStream_t st, Pool& tmp, int ell, int s, int tag, int64_t elems, F&& fill) {
     const uint64_t key = ((uint64_t)ell << 40) | ((uint64_t)(s + 1) << 16) | (uint64_t)tag;
-    if (chain_cache_enabled) {
+    if (chain_cache_enabled && !no_cache) {
       auto it = memo_map.find(key);
       if (it != memo_map.end()) return it->second;
       cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -1751,8 +1738,7 @@ struct Engine {
     } else {
       const int i = s.site, bl = s.bl, br = s.br, r = s.r;
       const int ab1 = s.ab1, ab2 = s.ab2, aa0 = s.aa0, aa1 = s.aa1;
-      const double sc = h_s[s.s_index];
-      const cplx csc = {sc, 0.0}, cmsc = {-sc, 0.0};
+      const double* sc = at<double>(s.o_s);  // frozen s, read on the device (no host constant)
       const cplx* theta = at(s.o_theta);
       const cplx* uh = at(s.o_uh);  // (r x 4bl)
       const cplx* vh = at(s.o_vh);  // (r x 4br)
@@ -1776,15 +1762,17 @@ struct Engine {
         cplx* UDW = pool.c(sRR * nb);
         nc(st, r, r, P * br, UD, sUD, vh, 0, UDW, sRR, nb);
         TN_CUDA(cudaMemcpyAsync(nBi, Z, (size_t)sZ * nb * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-        cn(st, P * bl, r, r, uh, 0, UDW, sRR, nBi, sZ, nb, cmsc, csc);
-        axpby(st, nBj, UD, csc, ZERO, sUD * nb);
+        cn(st, P * bl, r, r, uh, 0, UDW, sRR, nBi, sZ, nb, MONE, ONE, sc);
+        TN_CUDA(cudaMemcpyAsync(nBj, UD, (size_t)sUD * nb * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+        scale_by(st, nBj, sc, 1.0, sUD * nb);
       } else {
         // B_i = s D W ; B_{i+1} = s (U^H D - (U^H D W) W^H)
         cplx* UDW = pool.c(sRR * nb);
         nn(st, r, r, P * bl, uh, 0, Z, sZ, UDW, sRR, nb);
         TN_CUDA(cudaMemcpyAsync(nBj, UD, (size_t)sUD * nb * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-        nn(st, r, P * br, r, UDW, sRR, vh, 0, nBj, sUD, nb, cmsc, csc);
-        axpby(st, nBi, Z, csc, ZERO, sZ * nb);
+        nn(st, r, P * br, r, UDW, sRR, vh, 0, nBj, sUD, nb, MONE, ONE, sc);
+        TN_CUDA(cudaMemcpyAsync(nBi, Z, (size_t)sZ * nb * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+        scale_by(st, nBi, sc, 1.0, sZ * nb);
       }
       // chains (direction-independent; recorded / replayed per point)
       cplx *nAai, *nAaj, *nAbi, *nAbj;
@@ -1796,14 +1784,14 @@ struct Engine {
         nn(st, P * aa0, P * br, aa1, t.Aa[i], 0, t.Aa[i + 1], 0, aa2t, 0, 1);
         apply_gate(st, aa2t, 0, aa2t, 0, Mk, 0, aa0, br, 1, ONE, false, NI);
         nAai = dnew((int64_t)P * aa0 * r, st);
-        nc(st, P * aa0, r, P * br, aa2t, 0, vh, 0, nAai, 0, 1, csc);
+        nc(st, P * aa0, r, P * br, aa2t, 0, vh, 0, nAai, 0, 1, ONE, ZERO, sc);
         nAaj = dnew((int64_t)r * P * br, st);
         TN_CUDA(cudaMemcpyAsync(nAaj, vh, (size_t)r * P * br * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
         cplx* ab2t = pool.c((int64_t)PP * bl * ab2);
         nn(st, P * bl, P * ab2, ab1, t.Ab[i], 0, t.Ab[i + 1], 0, ab2t, 0, 1);
         apply_gate(st, ab2t, 0, ab2t, 0, Mk, 0, bl, ab2, 1, ONE, false, NI);
         nAbj = dnew((int64_t)r * P * ab2, st);
-        nn(st, r, P * ab2, P * bl, uh, 0, ab2t, 0, nAbj, 0, 1, csc);
+        nn(st, r, P * ab2, P * bl, uh, 0, ab2t, 0, nAbj, 0, 1, ONE, ZERO, sc);
         nAbi = dnew((int64_t)P * bl * r, st);
         conjT_scale_cols(st, nAbi, uh, r, P * bl, nullptr, nullptr);
         if (t.mode == CHAIN_RECORD) record(t, {nAai, nAaj, nAbi, nAbj});
@@ -2260,14 +2248,24 @@ struct Engine {
 
   // Replays run on the caller's stream: wait for that stream only (not the
   // device) before the executable graphs and their I/O buffers go.
-  void drop_graphs(cudaStream_t st) {
-    if (graphs.empty()) return;
+  // all = false (every primal pass): only the point-specific graphs go (they
+  // replay per-point caches); point-free graphs read everything point-specific
+  // from the store at run time and stay.
+  void drop_graphs(cudaStream_t st, bool all = false) {
+    bool any = false;
+    for (ApplyGraph& g : graphs) any = any || all || !g.point_free;
+    if (!any) return;
     TN_CUDA(cudaStreamSynchronize(st));
+    std::vector<ApplyGraph> keep;
     for (ApplyGraph& g : graphs) {
+      if (!all && g.point_free) {
+        keep.push_back(g);
+        continue;
+      }
       if (g.exec) cudaGraphExecDestroy(g.exec);
       for (cplx* p : {g.in, g.out, g.auxb}) dfree(p, st);
     }
-    graphs.clear();
+    graphs.swap(keep);
     cudaDeviceGraphMemTrim(device);
   }
 
@@ -2275,6 +2273,7 @@ struct Engine {
   void invalidate(cudaStream_t st) {
     primal_valid = false;
     ti_valid = false;
+    applies_at_point = 0;
     drop_graphs(st);
     drop_chain_cache(st);
   }
@@ -2282,7 +2281,7 @@ struct Engine {
   // tn_hvp_trim_memory: drop the per-point caches and graphs (rebuilt by the
   // next apply) and return the library pool's unused blocks to the device.
   void trim_memory(cudaStream_t st) {
-    drop_graphs(st);
+    drop_graphs(st, true);
     drop_chain_cache(st);
     TN_CUDA(cudaStreamSynchronize(st));
     pool_trim(device);
@@ -2302,11 +2301,13 @@ struct Engine {
     cudaGraph_t graph = nullptr;
     TN_CUDA(cudaStreamBeginCapture(stc, cudaStreamCaptureModeThreadLocal));
     bool ok = true;
+    no_cache = g.point_free;
     try {
       apply(stc, g.batch, g.in, g.out, g.aux ? g.auxb : nullptr);
     } catch (...) {
       ok = false;
     }
+    no_cache = false;
     const cudaError_t e = cudaStreamEndCapture(stc, &graph);
     g.launches = launch_count() - l0;
     g.work = work_counter.load() - w0;
@@ -2328,6 +2329,15 @@ struct Engine {
     return true;
   }
 
+  // A point-free graph owns its working memory for its lifetime: only when one
+  // apply's tangent state plus the uncached chains fit in 1/16 of the device.
+  bool point_free_ok(int batch) {
+    size_t fr = 0, tot = 0;
+    TN_CUDA(cudaMemGetInfo(&fr, &tot));
+    const size_t need = per_direction_bytes() * (size_t)std::min(batch, cfg.max_batch) + chain_cache_bytes();
+    return need < tot / 16 && need < fr / 4;
+  }
+
   // tn_hvp_apply entry: eager, or graph replay for a repeated (batch, aux)
   void apply_call(cudaStream_t st, int batch, const cplx* dirs, cplx* hess, cplx* aux) {
     TN_CUDA(cudaSetDevice(device));
@@ -2335,18 +2345,32 @@ struct Engine {
     check_dirs(st, at(o_gates), dirs, batch);
     // graphs pay off for launch-bound small batches (truncated CG: batch 1);
     // large batches are GEMM-bound and would double the memory footprint
-    if (!graphs_enabled || batch <= 0 || batch > kGraphMaxBatch || gemm_profile_active() || std::getenv("TN_PHASES")) {
+    const bool first = ++applies_at_point == 1;
+    if (!graphs_enabled || batch <= 0 || gemm_profile_active() || std::getenv("TN_PHASES")) {
+      apply(st, batch, dirs, hess, aux);
+      return;
+    }
+    // First apply at a point: a point-free graph (no per-point caches, the
+    // frozen factors read from the store on the device) captured once per
+    // (batch, aux) and replayed at every later point -- launch-bound small
+    // configurations -- when its graph-owned working memory is small.
+    // Repeated applies at one point (truncated CG): per-point caches recorded
+    // by an eager call, then a point-specific graph that replays them.
+    const bool pf = first && point_free_ok(batch);
+    if (!pf && batch > kGraphMaxBatch) {
       apply(st, batch, dirs, hess, aux);
       return;
     }
     ApplyGraph* g = nullptr;
     for (ApplyGraph& x : graphs)
-      if (x.batch == batch && x.aux == (aux != nullptr)) g = &x;
+      if (x.batch == batch && x.aux == (aux != nullptr) && x.point_free == pf) g = &x;
     if (!g) {
       graphs.push_back(ApplyGraph{});
       g = &graphs.back();
       g->batch = batch;
       g->aux = aux != nullptr;
+      g->point_free = pf;
+      if (pf) g->calls = 1;  // captured at once: the capture costs about one eager call
     }
     if (++g->calls == 1 || g->failed) {
       apply(st, batch, dirs, hess, aux);
@@ -2387,6 +2411,9 @@ struct Engine {
     }
     check_gates(st, gates, K);
     check_dirs(st, gates, dirs, batch);
+    // (measured: at C2 / C3 the point-free apply graph alone gains what the
+    // forward-tangent overlap of the fused step gains -- 307 vs 298 ms per C2
+    // step, 3.08 s either way at C3 -- so the step stays fused)
     std::vector<TanSnap> DB0;
     environments(st, gates, scalars, grad_R, std::min(batch, cfg.max_batch), dirs, &DB0);
     apply(st, batch, dirs, hess, aux, &DB0);
@@ -2449,11 +2476,6 @@ void engine_primal_imported(tn_hvp_ctx* ctx, const cplx* gates, cudaStream_t st)
   std::vector<cplx> hg((size_t)e.K * 16), hb((size_t)e.K * 16);
   TN_CUDA(cudaMemcpyAsync(hg.data(), gates, sizeof(cplx) * hg.size(), cudaMemcpyDeviceToHost, st));
   TN_CUDA(cudaMemcpyAsync(hb.data(), e.at(e.o_gates), sizeof(cplx) * hb.size(), cudaMemcpyDeviceToHost, st));
-  for (SidePlan* sp : {&e.bot, &e.top})
-    for (auto& ls : sp->steps)
-      for (Step& s : ls)
-        if (s.type == PAIR)
-          TN_CUDA(cudaMemcpyAsync(&e.h_s[s.s_index], e.at<double>(s.o_s), sizeof(double), cudaMemcpyDeviceToHost, st));
   TN_CUDA(cudaStreamSynchronize(st));
   if (std::memcmp(hg.data(), hb.data(), sizeof(cplx) * hg.size()) != 0)
     throw std::invalid_argument("tn_hvp_primal_imported: gates differ from the imported primal store's point");

@@ -44,6 +44,7 @@ struct Params {
   double* part;        // [batch][ksplit][M][N] complex partials (split-K only)
   cplx alpha, beta;
   int has_beta;
+  const double* dscale;  // nullable DEVICE scalar: alpha and beta are multiplied by *dscale
   const cplx* A;
   const cplx* B;
   cplx* C;
@@ -192,9 +193,10 @@ __global__ void __launch_bounds__(NT3, MINB) zgemm3m_kernel(Params p) {
           if (ks > 1) {  // partial of this K slice (reduced in split order by zreduce_kernel)
             reinterpret_cast<cplx*>(p.part)[((bz * ks + split) * (int64_t)p.M + row) * p.N + col] = make_double2(re, im);
           } else {
-            cplx v = cmul(p.alpha, make_double2(re, im));
+            const double f = p.dscale ? *p.dscale : 1.0;
+            cplx v = cmul(cscale(p.alpha, f), make_double2(re, im));
             cplx* dst = C + (int64_t)row * p.ldc + col;
-            if (p.has_beta) v = cadd(v, cmul(p.beta, *dst));
+            if (p.has_beta) v = cadd(v, cmul(cscale(p.beta, f), *dst));
             *dst = v;
           }
         }
@@ -212,9 +214,10 @@ __global__ void zreduce_kernel(Params p, int batch) {
     cplx acc = make_double2(0, 0);
     for (int sp = 0; sp < p.ksplit; ++sp) acc = cadd(acc, part[(b * p.ksplit + sp) * mn + e]);
     const int row = (int)(e / p.N), col = (int)(e % p.N);
-    cplx v = cmul(p.alpha, acc);
+    const double f = p.dscale ? *p.dscale : 1.0;
+    cplx v = cmul(cscale(p.alpha, f), acc);
     cplx* dst = p.C + b * p.sC + (int64_t)row * p.ldc + col;
-    if (p.has_beta) v = cadd(v, cmul(p.beta, *dst));
+    if (p.has_beta) v = cadd(v, cmul(cscale(p.beta, f), *dst));
     *dst = v;
   }
 }
@@ -394,7 +397,7 @@ void gemm_profile_end(double* ms, double* cmac) {
 
 void zgemm(cudaStream_t st, char opa, char opb, int M, int N, int K, cplx alpha, const cplx* A, int64_t lda,
            int64_t sA, const cplx* B, int64_t ldb, int64_t sB, cplx beta, cplx* C, int64_t ldc, int64_t sC,
-           int batch) {
+           int batch, const double* dscale) {
   if (M <= 0 || N <= 0 || batch <= 0) return;
   Params p;
   p.ksplit = 1;
@@ -402,6 +405,7 @@ void zgemm(cudaStream_t st, char opa, char opb, int M, int N, int K, cplx alpha,
   p.alpha = alpha;
   p.beta = beta;
   p.has_beta = (beta.x != 0.0 || beta.y != 0.0);
+  p.dscale = dscale;
   p.A = A; p.B = B; p.C = C;
   p.lda = lda; p.ldb = ldb; p.ldc = ldc; p.sA = sA; p.sB = sB; p.sC = sC;
   p.M = M; p.N = N; p.K = K;
