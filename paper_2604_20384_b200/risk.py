@@ -101,6 +101,17 @@ class EmpiricalRisk:
         axpby(1.0, acc[:1], 1.0, risk)              # 1 + mean f  (real part)
         return torch.view_as_real(risk)[:, 0], g
 
+    def cost(self, gates: torch.Tensor):
+        """Risk at trial gates (per-sample top sweeps only, tn_hvp_cost; the
+        stored points are untouched) -> [1] float64 = 1 + mean_s f_s."""
+        acc = torch.zeros(4, dtype=torch.complex128, device=self.device)
+        for sc in self._each(lambda eng: eng.cost(gates)):
+            axpby(1.0 / self.S, torch.view_as_complex(sc.view(4, 2)), 1.0, acc)
+        self._reduce(acc)
+        risk = torch.ones(1, dtype=torch.complex128, device=self.device)
+        axpby(1.0, acc[:1], 1.0, risk)
+        return torch.view_as_real(risk)[:, 0]
+
     def apply(self, dirs: torch.Tensor):
         """Riemannian HVPs of the risk for dirs [B,K,4,4] -> [B,K,4,4]."""
         H = torch.zeros_like(dirs)

@@ -91,3 +91,30 @@ def test_state_mode_rejects_operator_calls():
         eng.set_product_state(torch.zeros(4, 2, dtype=torch.complex128, device="cuda"))
     assert e.value.status == N.TN_EINVAL
     eng.close()
+
+
+def test_trust_region_on_the_empirical_risk():
+    """The paper's training loop: Riemannian trust
+    region with truncated CG on the sampled-state risk, every f, gradient and
+    HVP from the state-mode engines.  The risk's cost() equals its primal pass
+    at the same gates, accepted steps decrease the risk, iterates stay unitary."""
+    from paper_2604_20384_b200.risk import EmpiricalRisk
+    from paper_2604_20384_b200.trust_region import TRParams, TrustRegion
+    cid, n, D, chi, S = 541, 8, 4, 8, 3
+    cfg = C.small_case(cid, n, D, chi, batch=1)
+    ref = [a.numpy() for a in reference_mpo(C.reference_layers(cfg), n, 64)]
+    psis = SMP.haar_product_states(cid, S, n)
+    dev = torch.device("cuda")
+    labels = [[torch.tensor(a, device=dev) for a in SMP.label_mps(ref, p)] for p in psis]
+    er = EmpiricalRisk(n, D, chi, labels, psis, max_batch=1)
+    x0 = torch.tensor(C.trotter_init_gates(cfg, 0), device=dev)
+    r0, _ = er.environments(x0)
+    assert abs(er.cost(x0).item() - r0.item()) <= 1e-12 * abs(r0.item())
+    x, f, tr = TrustRegion(er, TRParams(outer=6, max_hvp=10)).run(x0)
+    acc = [r for r in tr.records if r.get("accepted")]
+    assert acc and f < r0.item()
+    fs = [tr.records[0]["f"]] + [r["f_trial"] for r in acc]
+    assert all(b <= a + 1e-14 for a, b in zip(fs, fs[1:]))
+    Xn = x.cpu().numpy()
+    assert np.abs(np.einsum("kba,kbc->kac", Xn.conj(), Xn) - np.eye(4)).max() < 1e-12
+    er.close()
