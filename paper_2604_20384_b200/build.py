@@ -53,7 +53,7 @@ def build(verbose: bool = False) -> str:
             if verbose and r.stderr:
                 print(r.stderr, file=sys.stderr)
     if _stale(LIB, objs):
-        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcusolver", "-lcudart"])
+        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcusolver", "-lcublas", "-lcudart"])
     os.makedirs(BIN, exist_ok=True)
     peak = os.path.join(BIN, "fp64_peak")
     src = os.path.join(CSRC, "fp64_peak.cu")

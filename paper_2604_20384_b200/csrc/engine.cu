@@ -14,6 +14,7 @@
 //    eq:overlap-hvp) -- Algorithm 1's two passes
 //     at layer granularity, forward tangent cached, backward
 //    tangent on the fly.
+#include <cublas_v2.h>
 #include <cusolverDn.h>
 
 #include <algorithm>
@@ -158,11 +159,17 @@ struct Engine {
   struct Solver {
     cusolverDnHandle_t h = nullptr;
     cusolverDnParams_t prm = nullptr;
+    cublasHandle_t bl = nullptr;  // triangular solves of CholeskyQR2 (created on first use)
+    int lwork_potrf = 0;
     std::vector<char> host_ws;
   };
   Solver sol[2];
   int lwork_heevd = 0;
   std::atomic<int> n_fallback{0}, n_deflate{0}, n_noise{0};
+  const bool lowdin_lq = std::getenv("TN_NO_LOWDIN_LQ") == nullptr;
+  const bool cholqr = std::getenv("TN_NO_CHOLQR") == nullptr;
+  static constexpr int kCholMin = 32;  // below: the Householder panel is as fast
+  std::atomic<int> n_cholqr_fallback{0};
   size_t svd_dws = 0, svd_hws = 0;
   int lwork_geqrf = 0, lwork_ungqr = 0;
   cudaStream_t st2 = nullptr, st1 = nullptr;  // top / bottom sweep streams (non-blocking)
@@ -527,15 +534,25 @@ struct Engine {
     }
     TN_CUDA(cudaMalloc(&ref, e * sizeof(cplx)));
     TN_CUDA(cudaMemcpyAsync(ref, ref_mpo, e * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-    TN_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
-    TN_CUDA(cudaStreamCreateWithFlags(&st1, cudaStreamNonBlocking));
+    // Stream priorities: the two primal sweeps are latency-bound chains (the
+    // critical path of a step), the layer environments and the fused step's
+    // forward tangents are throughput work that fills in behind them.
+    int prio_lo = 0, prio_hi = 0;
+    TN_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    const bool use_prio = std::getenv("TN_NO_STREAM_PRIO") == nullptr;
+    auto mkstream = [&](cudaStream_t* s, int level) {  // level 0 = highest
+      const int pr = use_prio ? (int)std::min<int64_t>(prio_lo, (int64_t)prio_hi + level) : prio_lo;
+      TN_CUDA(cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, pr));
+    };
+    mkstream(&st2, 0);
+    mkstream(&st1, 0);
     TN_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     TN_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     TN_CUDA(cudaEventCreateWithFlags(&ev_join1, cudaEventDisableTiming));
-    TN_CUDA(cudaStreamCreateWithFlags(&stg, cudaStreamNonBlocking));
-    TN_CUDA(cudaStreamCreateWithFlags(&stf, cudaStreamNonBlocking));
-    TN_CUDA(cudaStreamCreateWithFlags(&stc, cudaStreamNonBlocking));
-    TN_CUDA(cudaStreamCreateWithFlags(&sth, cudaStreamNonBlocking));
+    mkstream(&stg, 1);
+    mkstream(&stf, 1 << 20);  // lowest (the default priority, like the caller's stream)
+    mkstream(&stc, 1 << 20);
+    mkstream(&sth, 1 << 20);
     TN_CUDA(cudaEventCreateWithFlags(&ev_joinf, cudaEventDisableTiming));
     TN_CUDA(cudaEventCreateWithFlags(&ev_joing, cudaEventDisableTiming));
     for (auto& v : ev_snap) {
@@ -609,6 +626,7 @@ struct Engine {
     for (Solver& so : sol) {
       if (so.prm) cusolverDnDestroyParams(so.prm);
       if (so.h) cusolverDnDestroy(so.h);
+      if (so.bl) cublasDestroy(so.bl);
     }
     for (cudaEvent_t e : {ev_fork, ev_join, ev_join1, ev_joing, ev_joinf})
       if (e) cudaEventDestroy(e);
@@ -757,8 +775,67 @@ struct Engine {
     std::vector<int> b;  // bonds
   };
 
+  // CholeskyQR2 of a row-major P (rows x cols): two passes of Gram matrix (DMMA
+  // GEMM) -> potrf -> triangular solve instead of a Householder panel
+  // factorisation (geqr2 is one latency-bound CTA: 1.5 ms for 1024 x 256).
+  //   right: rows >= cols, P = Q R, Q (rows x cols) column-orthonormal, T = R (cols x cols) upper;
+  //   left : rows <= cols, P = L Q, Q (rows x cols) row-orthonormal,    T = L (rows x rows) lower.
+  // Orthonormal to rounding when cond(P)^2 eps << 1.  Returns false when a Gram
+  // matrix is not numerically positive definite or the second pass is not a
+  // small correction (|T_2 - I| > 0.1): the caller falls back to Householder.
+  // One host read of the flag per call (the sweeps already return to the host per split).
+  bool cholqr2(cudaStream_t st, Solver& so, Pool& pool, const cplx* Pm, int rows, int cols, bool right, cplx* Q,
+               cplx* T) {
+    const int n = right ? cols : rows;
+    if (!so.bl) {
+      if (cublasCreate(&so.bl) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasCreate failed");
+    }
+    if (cublasSetStream(so.bl, st) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasSetStream failed");
+    TN_SOLVER(cusolverDnSetStream(so.h, st));
+    const cublasFillMode_t uplo = right ? CUBLAS_FILL_MODE_LOWER : CUBLAS_FILL_MODE_UPPER;  // of the column-major view
+    int lw = 0;
+    TN_SOLVER(cusolverDnZpotrf_bufferSize(so.h, uplo, n, nullptr, n, &lw));
+    cplx* work = pool.c(std::max(lw, 1));
+    cplx* Gm[2] = {pool.c((int64_t)n * n), pool.c((int64_t)n * n)};
+    int* flag = (int*)pool.raw(sizeof(int));
+    TN_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+    TN_CUDA(cudaMemcpyAsync(Q, Pm, (size_t)rows * cols * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+    const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0);
+    for (int pass = 0; pass < 2; ++pass) {
+      cplx* G = Gm[pass];
+      if (right)
+        cn(st, n, n, rows, Q, 0, Q, 0, G, 0, 1);  // Q^H Q
+      else
+        nc(st, n, n, cols, Q, 0, Q, 0, G, 0, 1);  // Q Q^H
+      int* ci = call_info(pool, st);
+      // the row-major Hermitian G read column-major is conj(G): its Cholesky factor
+      // read back row-major is the upper R with G = R^H R (right) / the lower L with G = L L^H (left)
+      TN_SOLVER(cusolverDnZpotrf(so.h, uplo, n, (cuDoubleComplex*)G, n, (cuDoubleComplex*)work, lw, ci));
+      // Q <- Q R^{-1} (right) / L^{-1} Q (left), on the column-major view Q^T (cols x rows)
+      const cublasStatus_t bs =
+          right ? cublasZtrsm(so.bl, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, cols,
+                              rows, &one, (const cuDoubleComplex*)G, n, (cuDoubleComplex*)Q, cols)
+                : cublasZtrsm(so.bl, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, cols,
+                              rows, &one, (const cuDoubleComplex*)G, n, (cuDoubleComplex*)Q, cols);
+      if (bs != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasZtrsm status " + std::to_string((int)bs));
+      tri_keep(st, G, n, right);
+      chol_flag(st, G, n, right, ci, pass == 1, 0.1, flag);
+    }
+    if (right)
+      nn(st, n, n, n, Gm[1], 0, Gm[0], 0, T, 0, 1);  // R = R2 R1
+    else
+      nn(st, n, n, n, Gm[0], 0, Gm[1], 0, T, 0, 1);  // L = L1 L2
+    int hflag = 0;
+    TN_CUDA(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    TN_CUDA(cudaStreamSynchronize(st));
+    if (hflag) ++n_cholqr_fallback;
+    return hflag == 0;
+  }
+
   void qr_right(cudaStream_t st, Solver& so, Pool& pool, const cplx* P, int rows, int cols, int kq, cplx* Q, cplx* R, int* info) {
     // P row-major rows x cols -> Q (rows x kq) row-major, R (kq x cols) row-major
+    if (cholqr && kq == cols && rows >= cols && cols >= kCholMin && cholqr2(st, so, pool, P, rows, cols, true, Q, R))
+      return;
     cplx* cm = pool.c((int64_t)rows * cols);
     transpose(st, cm, P, rows, cols, false);  // column-major rows x cols
     cplx* tau = pool.c(std::min(rows, cols));
@@ -777,6 +854,8 @@ struct Engine {
 
   void lq_left(cudaStream_t st, Solver& so, Pool& pool, const cplx* P, int rows, int cols, int kq, cplx* Q, cplx* L, int* info) {
     // P row-major rows x cols = L (rows x kq) Q (kq x cols), Q row-orthonormal
+    if (cholqr && kq == rows && cols >= rows && rows >= kCholMin && cholqr2(st, so, pool, P, rows, cols, false, Q, L))
+      return;
     cplx* cm = pool.c((int64_t)rows * cols);
     TN_CUDA(cudaMemcpyAsync(cm, P, (size_t)rows * cols * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
     cplx* tau = pool.c(std::min(rows, cols));
@@ -850,7 +929,7 @@ struct Engine {
   // first-order rotation c_ij = (B_i B_j^H) / (s_j^2 - s_i^2) (one-sided Jacobi
   // across the cut), twice, then Loewdin re-orthonormalisation of the kept rows.
   void refine_kept(cudaStream_t st, Pool& pool, cplx* uhf, const double* S, const cplx* A, int R, int Cc, int mn,
-                   int r, int iters) {
+                   int r, int iters, bool kept_only = false) {
     const int nd = mn - r;
     if (nd <= 0 || iters <= 0) return;
     cplx* B = pool.c((int64_t)mn * Cc);
@@ -865,11 +944,34 @@ struct Engine {
       cn(st, r, R, nd, Cm, 0, uhf + (int64_t)r * R, 0, uhf, 0, 1, ONE, ONE);      // kept += C^H disc
       nn(st, nd, R, r, Cm, 0, old, 0, uhf + (int64_t)r * R, 0, 1, MONE, ONE);    // disc -= C kept_old
     }
-    // Loewdin re-orthonormalisation of the whole basis: U <- (3/2 - 1/2 U U^H) U
-    cplx* F = pool.c((int64_t)mn * mn);
-    nc(st, mn, mn, R, uhf, 0, uhf, 0, F, 0, 1);
-    TN_CUDA(cudaMemcpyAsync(old, uhf, (size_t)mn * R * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-    nn(st, mn, R, mn, F, 0, old, 0, uhf, 0, 1, {-0.5, 0.0}, {1.5, 0.0});
+    // Loewdin re-orthonormalisation U <- (3/2 - 1/2 U U^H) U of the whole basis, or
+    // (kept_only: the caller uses nothing but the kept rows afterwards) of the
+    // kept rows among themselves
+    const int no = kept_only ? r : mn;
+    cplx* F = pool.c((int64_t)no * no);
+    nc(st, no, no, R, uhf, 0, uhf, 0, F, 0, 1);
+    TN_CUDA(cudaMemcpyAsync(old, uhf, (size_t)no * R * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+    nn(st, no, R, no, F, 0, old, 0, uhf, 0, 1, {-0.5, 0.0}, {1.5, 0.0});
+  }
+
+  // W^H = row-orthonormal basis of the rows of Y (r x Cc), L = Y W (r x r), for
+  // Y = U_r^H A whose rows are mutually orthogonal up to the eigensolver's
+  // residual, <y_i, y_j> ~ eps sigma_1^2, with norms sigma_i (S, device): the
+  // row-scaled Yt = diag(1/sigma) Y has Yt Yt^H = I + O(eps (sigma_1/sigma_r)^2),
+  // so `steps` Newton-Schulz (Loewdin) steps Yt <- (3/2 - 1/2 Yt Yt^H) Yt (error e
+  // -> 3/2 e^2) orthonormalise it with GEMMs only -- no panel factorisation.
+  // Same row space as the LQ factor, another r x r gauge (outputs are invariant).
+  void lq_rows_lowdin(cudaStream_t st, Pool& pool, const cplx* Y, const double* S, int r, int Cc, int steps, cplx* Wh,
+                      cplx* L) {
+    rows_over_s(st, Wh, Y, S, r, Cc);
+    cplx* F = pool.c((int64_t)r * r);
+    cplx* old = pool.c((int64_t)r * Cc);
+    for (int it = 0; it < steps; ++it) {
+      nc(st, r, r, Cc, Wh, 0, Wh, 0, F, 0, 1);
+      TN_CUDA(cudaMemcpyAsync(old, Wh, (size_t)r * Cc * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+      nn(st, r, Cc, r, F, 0, old, 0, Wh, 0, 1, {-0.5, 0.0}, {1.5, 0.0});
+    }
+    nc(st, r, r, Cc, Y, 0, Wh, 0, L, 0, 1);
   }
 
   // Second Gram level for the low part of the spectrum: rows n_hi.. of uhf
@@ -967,6 +1069,7 @@ struct Engine {
           double* Sf = (double*)tmp.raw((size_t)P * s.bl * sizeof(double));
           svd_rowmajor(st, so, tmp, Acp, P * s.bl, P * s.br, Sf, uhf, info + 1, method);
           int iters = 0;
+          int lq_steps = 0;  // > 0: W_r^H by Newton-Schulz steps on the sigma-scaled rows (lq_rows_lowdin)
           if (s.r < P * s.bl) {  // something (discarded or null) is excluded
             // kept/excluded mixing of a Gram basis ~ eps sigma_top^2 / (sigma_{r-1}^2 - sigma_r^2)
             // (sigma_r = 0 for a null direction); first-order refinement converges
@@ -1016,11 +1119,17 @@ struct Engine {
               ++n_fallback;
             } else {
               iters = delta < 1e-8 ? 1 : delta < 1e-4 ? 2 : 4;
+              // row-orthogonality defect of the scaled Y ~ eps (sigma_1/sigma_{r-1})^2 (x100 margin);
+              // only plain Gram splits (no deflation level rewrote the low rows' scale)
+              if (lowdin_lq && top_i == 0 && hS[s.r - 1] > 0) {
+                const double e0 = 2.2e-14 * (hS[0] / hS[s.r - 1]) * (hS[0] / hS[s.r - 1]);
+                lq_steps = e0 < 1e-9 ? 1 : e0 < 1e-5 ? 2 : e0 < 1e-3 ? 3 : 0;
+              }
             }
           }
           TN_CUDA(cudaMemcpyAsync(S, Sf, (size_t)s.mn * sizeof(double), cudaMemcpyDeviceToDevice, st));
           double* sc = store ? at<double>(s.o_s) : (double*)tmp.raw(sizeof(double));
-          refine_kept(st, tmp, uhf, Sf, A, P * s.bl, P * s.br, nbas, s.r, iters);
+          refine_kept(st, tmp, uhf, Sf, A, P * s.bl, P * s.br, nbas, s.r, iters, /*kept_only=*/true);
           TN_CUDA(cudaMemcpyAsync(uh, uhf, (size_t)s.r * P * s.bl * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
           // Y = U_r^H A (= S_r W_r^H up to a kept-space rotation); LQ gives W_r^H
           cplx* Y = tmp.c((int64_t)s.r * P * s.br);
@@ -1032,7 +1141,10 @@ struct Engine {
             s_from_norms(st, nrm, S, s.mn, s.r, sc, diag);
           }
           cplx* Lq = tmp.c((int64_t)s.r * s.r);
-          lq_left(st, so, tmp, Y, s.r, P * s.br, s.r, vh, Lq, info);
+          if (lq_steps > 0)
+            lq_rows_lowdin(st, tmp, Y, Sf, s.r, P * s.br, lq_steps, vh, Lq);
+          else
+            lq_left(st, so, tmp, Y, s.r, P * s.br, s.r, vh, Lq, info);
           cplx* ni = dnew((int64_t)P * s.bl * s.r, st);
           cplx* nj = dnew((int64_t)s.r * P * s.br, st);
           if (s.lr) {  // (U_r, s U_r^H A), centre -> i+1

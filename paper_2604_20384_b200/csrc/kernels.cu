@@ -311,6 +311,23 @@ void scale_by(cudaStream_t st, cplx* y, const double* s, double pw, int64_t n) {
   count_launch();
 }
 
+__global__ void rows_over_s_kernel(cplx* dst, const cplx* src, const double* S, int64_t cols, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  for (; i < n; i += step) {
+    const double f = 1.0 / S[i / cols];
+    dst[i] = cplx{src[i].x * f, src[i].y * f};
+  }
+}
+
+void rows_over_s(cudaStream_t st, cplx* dst, const cplx* src, const double* S, int rows, int64_t cols) {
+  const int64_t n = (int64_t)rows * cols;
+  if (n == 0) return;
+  rows_over_s_kernel<<<nblocks(n), TPB, 0, st>>>(dst, src, S, cols, n);
+  TN_CUDA(cudaGetLastError());
+  count_launch();
+}
+
 void extract_env(cudaStream_t st, cplx* E, int64_t sE, const cplx* top, int64_t stop, const cplx* z, int64_t sz,
                  int T, int U, int batch, cplx alpha, int ni) {
   const int64_t pairs = (int64_t)T * U * ni * ni;
@@ -613,6 +630,51 @@ void tri_extract(cudaStream_t st, cplx* dst, const cplx* buf, int rows, int cols
   const int64_t n = (int64_t)rows * cols;
   if (!n) return;
   tri_kernel<<<nblocks(n), TPB, 0, st>>>(dst, buf, rows, cols, lda, upper ? 1 : 0);
+  TN_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+__global__ void tri_keep_kernel(cplx* __restrict__ M, int n, int upper) {
+  const int64_t tot = (int64_t)n * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < tot; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / n), j = (int)(idx % n);
+    if (upper ? (j < i) : (j > i)) M[idx] = make_double2(0, 0);
+  }
+}
+
+void tri_keep(cudaStream_t st, cplx* M, int n, bool upper) {
+  if (!n) return;
+  tri_keep_kernel<<<nblocks((int64_t)n * n), TPB, 0, st>>>(M, n, upper ? 1 : 0);
+  TN_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+// one block: flag |= (info != 0) | (near_identity && max |M - I| over the kept triangle > tol) | non-finite entry
+__global__ void chol_flag_kernel(const cplx* __restrict__ M, int n, int upper, const int* __restrict__ info,
+                                 int near_identity, double tol, int* __restrict__ flag) {
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = (*info != 0) ? 1 : 0;
+  __syncthreads();
+  int mine = 0;
+  const int64_t tot = (int64_t)n * n;
+  for (int64_t idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+    const int i = (int)(idx / n), j = (int)(idx % n);
+    if (upper ? (j < i) : (j > i)) continue;
+    const cplx v = M[idx];
+    if (!isfinite(v.x) || !isfinite(v.y)) mine = 1;
+    if (near_identity) {
+      const double dx = v.x - (i == j ? 1.0 : 0.0);
+      if (fabs(dx) > tol || fabs(v.y) > tol) mine = 1;
+    }
+  }
+  if (mine) atomicOr(&bad, 1);
+  __syncthreads();
+  if (threadIdx.x == 0 && bad) atomicOr(flag, 1);
+}
+
+void chol_flag(cudaStream_t st, const cplx* M, int n, bool upper, const int* info, bool near_identity, double tol,
+               int* flag) {
+  chol_flag_kernel<<<1, 1024, 0, st>>>(M, n, upper ? 1 : 0, info, near_identity ? 1 : 0, tol, flag);
   TN_CUDA(cudaGetLastError());
   count_launch();
 }

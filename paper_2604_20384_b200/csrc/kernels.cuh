@@ -11,6 +11,8 @@ void apply_gate(cudaStream_t st, cplx* out, int64_t sout, const cplx* x, int64_t
                 int X, int Y, int batch, cplx alpha, bool accumulate, int ni = 2);
 void axpby(cudaStream_t st, cplx* y, const cplx* x, cplx a, cplx b, int64_t n);   // y = a x + b y
 void scale_by(cudaStream_t st, cplx* y, const double* s, double pw, int64_t n);    // y *= s^pw (device s)
+// dst[i][j] = src[i][j] / S[i] (device S[rows]; rows x cols row-major)
+void rows_over_s(cudaStream_t st, cplx* dst, const cplx* src, const double* S, int rows, int64_t cols);
 // E[b] += alpha * sum conj(top[t,(o1 i1),(o2 i2),u]) z[b][t,(c1 i1),(c2 i2),u]
 void extract_env(cudaStream_t st, cplx* E, int64_t sE, const cplx* top, int64_t stop, const cplx* z, int64_t sz,
                  int T, int U, int batch, cplx alpha, int ni = 2);
@@ -30,6 +32,12 @@ void conjT_scale_cols(cudaStream_t st, cplx* dst, const cplx* uh, int r, int m, 
 // (lda): dst[i][j] = (j >= i) ? buf[i + j*lda] : 0          (upper = true)
 // Lower variant for LQ: dst[i][j] = (j <= i) ? buf[j + i*lda] : 0 (rows x cols = b x kq).
 void tri_extract(cudaStream_t st, cplx* dst, const cplx* buf, int rows, int cols, int64_t lda, bool upper);
+// In place on a row-major n x n matrix: zero the strictly lower (upper = true) or strictly upper triangle.
+void tri_keep(cudaStream_t st, cplx* M, int n, bool upper);
+// CholeskyQR bookkeeping: *flag |= 1 if *info != 0 (potrf), if the kept triangle of the
+// row-major n x n factor M has a non-finite entry, or (near_identity) if max |M - I| > tol.
+void chol_flag(cudaStream_t st, const cplx* M, int n, bool upper, const int* info, bool near_identity, double tol,
+               int* flag);
 // Vd[b][k] = V[b][k]^dag (4x4 each), n = batch*K matrices.
 void dagger4(cudaStream_t st, cplx* dst, const cplx* src, int64_t n);
 // out[0..2] = (max, min, max) of the two sides' diagnostics d[0..2], d[8..10]

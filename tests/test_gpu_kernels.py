@@ -203,6 +203,43 @@ def test_chain_cache_is_bitwise_uncached():
     cached.close()
 
 
+def test_gemm_orthonormalisations_match_householder():
+    """The GEMM-rich orthonormalisations of the primal sweeps -- CholeskyQR2 for
+    the centre moves and Newton-Schulz steps on the sigma-scaled rows of
+    Y = U_r^H A for W_r^H -- give the same outputs (f, grad_R, Hess_R are gauge
+    invariant) as an engine built with the Householder factorisations
+    (TN_NO_CHOLQR, TN_NO_LOWDIN_LQ), at C2 (chi = 64, truncating) and on a
+    small exact case; outputs also match with the kept-only Loewdin step."""
+    import os
+    from paper_2604_20384_b200.api import HVPEngine
+    from tests.helpers import rel
+    dev = torch.device("cuda")
+    cases = [(C.CONFIGS[2], C.reference_mpo(C.CONFIGS[2], device=dev), 0)]
+    from tn_inputs.reference import reference_mpo
+    small = C.small_case(85, 10, 6, 16, batch=3, first_offset=1)
+    cases.append((small, [a.to(dev) for a in reference_mpo(C.reference_layers(small), small.n, small.chi)], 1))
+    for cfg, ref, off in cases:
+        K = C.num_gates(cfg.n, cfg.depth, off)
+        Gn = C.haar_gates(cfg.cid, K)
+        G = torch.tensor(Gn, device=dev)
+        V = torch.tensor(C.tangent_directions(cfg.cid, Gn, 3), device=dev)
+        os.environ["TN_NO_CHOLQR"] = "1"
+        os.environ["TN_NO_LOWDIN_LQ"] = "1"
+        try:
+            house = HVPEngine(cfg.n, cfg.depth, cfg.chi, ref, off, max_batch=3)
+        finally:
+            del os.environ["TN_NO_CHOLQR"], os.environ["TN_NO_LOWDIN_LQ"]
+        fast = HVPEngine(cfg.n, cfg.depth, cfg.chi, ref, off, max_batch=3)
+        sc0, g0 = house.environments(G)
+        sc1, g1 = fast.environments(G)
+        H0, H1 = house.apply(V), fast.apply(V)
+        assert abs(sc0[0].item() - sc1[0].item()) <= 1e-11 * abs(sc0[0].item())
+        assert rel(g1.cpu().numpy(), g0.cpu().numpy()) < 1e-11
+        assert rel(H1.cpu().numpy(), H0.cpu().numpy()) < 1e-11
+        house.close()
+        fast.close()
+
+
 def test_point_free_graph_follows_the_point():
     """The point-free apply graph is captured at the first point and replayed
     at later points: it must read everything point-specific (store, frozen
