@@ -319,6 +319,15 @@ tn_status tn_zgemm(char opa, char opb, int32_t M, int32_t N, int32_t K, const do
  * context runs), and the bytes of the dominant kernel class; for rooflines. */
 tn_status tn_hvp_work(tn_hvp_ctx* ctx, double* cmac_per_direction, double* cmac_primal);
 
+/* Split statistics of the context's last primal pass (both sweeps), HOST
+ * int64[6]: [0] splits that fell back to the QR-iteration SVD, [1] extra Gram
+ * (deflation) levels, [2] cuts accepted inside the double-precision noise
+ * floor (reading X10), [3] low-rank blocks split by the range probe (numerical
+ * rank <= kept rank: no eigendecomposition), [4] centre
+ * moves whose CholeskyQR2 was rejected (Householder used), [5] pair steps.
+ * Diagnostics only; TN_EINVAL on a null argument. */
+tn_status tn_hvp_split_stats(tn_hvp_ctx* ctx, int64_t* out6);
+
 /* Number of kernels this library has launched since it was loaded (all
  * contexts, all streams) -- the bench's gpu_launches evidence. */
 int64_t tn_hvp_launch_count(void);

@@ -16,7 +16,7 @@ STATUS = {0: "TN_OK", 1: "TN_EINVAL", 2: "TN_ENOMEM", 3: "TN_ECUDA", 4: "TN_ENUM
 
 EXPORTS = ["tn_hvp_num_gates", "tn_hvp_setup", "tn_hvp_environments", "tn_hvp_apply", "tn_hvp_gradient_T",
            "tn_hvp_cost", "tn_hvp_primal_blob", "tn_hvp_primal_imported", "tn_riemannian_project", "tn_zgemm",
-           "tn_hvp_work", "tn_retract", "tn_tangent_dot", "tn_tangent_axpby", "tn_hvp_primal_copy",
+           "tn_hvp_work", "tn_hvp_split_stats", "tn_retract", "tn_tangent_dot", "tn_tangent_axpby", "tn_hvp_primal_copy",
            "tn_hvp_launch_count", "tn_gemm_profile", "tn_pauli_basis", "tn_pauli_coords", "tn_sym_eig",
            "tn_hvp_ti_environments", "tn_hvp_ti_apply", "tn_hvp_step", "tn_hvp_query", "tn_hvp_trim_memory",
            "tn_hvp_set_product_state", "tn_hvp_set_reference", "tn_mpo_tebd",
@@ -80,6 +80,8 @@ def lib():
         L.tn_zgemm.argtypes = [C.c_char, C.c_char, i32, i32, i32, C.POINTER(C.c_double), vp, i64, i64, vp, i64, i64,
                                C.POINTER(C.c_double), vp, i64, i64, i32, vp]
         L.tn_hvp_work.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.tn_hvp_split_stats.argtypes = [vp, C.POINTER(C.c_int64)]
+        L.tn_hvp_split_stats.restype = C.c_int
         L.tn_retract.argtypes = [i32, vp, vp, C.c_double, vp, vp]
         L.tn_tangent_dot.argtypes = [i64, i32, vp, vp, vp, vp]
         L.tn_tangent_axpby.argtypes = [i64, C.POINTER(C.c_double), vp, C.POINTER(C.c_double), vp, vp]
@@ -194,6 +196,12 @@ def tn_hvp_work(ctx):
     a, b = C.c_double(), C.c_double()
     check(lib().tn_hvp_work(ctx, C.byref(a), C.byref(b)), ctx)
     return a.value, b.value
+
+
+def tn_hvp_split_stats(ctx):
+    out = (C.c_int64 * 6)()
+    check(lib().tn_hvp_split_stats(ctx, out), ctx)
+    return list(out)
 
 
 def tn_retract(K, gates_ptr, xi_ptr, alpha, out_ptr, stream):

@@ -169,6 +169,13 @@ class HVPEngine:
         _require_cuda(gates, "gates")
         N.tn_hvp_primal_imported(self.ctx, gates.data_ptr(), _stream())
 
+    def split_stats(self):
+        """Last primal pass: dict of QR-iteration fallbacks, deflation levels, noise-floor cuts,
+        low-rank range-probe splits, rejected CholeskyQR2 moves and pair steps."""
+        keys = ("qr_iteration_fallbacks", "deflation_levels", "noise_floor_cuts", "low_rank_splits",
+                "cholqr_rejected", "pair_steps")
+        return dict(zip(keys, N.tn_hvp_split_stats(self.ctx)))
+
     def work(self):
         """(complex MACs per direction of the last apply, complex MACs of the last primal pass)."""
         return N.tn_hvp_work(self.ctx)

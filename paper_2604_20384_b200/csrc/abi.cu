@@ -241,6 +241,11 @@ tn_status tn_hvp_work(tn_hvp_ctx* ctx, double* per_dir, double* primal) {
   return guarded(ctx, [&] { tn::engine_work(ctx, per_dir, primal); });
 }
 
+tn_status tn_hvp_split_stats(tn_hvp_ctx* ctx, int64_t* out6) {
+  if (!ctx || !out6) return fail(ctx, TN_EINVAL, "tn_hvp_split_stats: null argument");
+  return guarded(ctx, [&] { tn::engine_split_stats(ctx, out6); });
+}
+
 tn_status tn_retract(int32_t K, const void* gates, const void* xi, double alpha, void* out, void* stream) {
   if (K < 0 || (K && (!gates || !xi || !out))) return fail(nullptr, TN_EINVAL, "tn_retract: bad argument");
   return guarded(nullptr, [&] {

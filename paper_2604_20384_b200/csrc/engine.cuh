@@ -34,6 +34,7 @@ void engine_tebd(int n, int ngates, const int32_t* sites, const cplx* gates, int
 void engine_set_product_state(tn_hvp_ctx* ctx, const cplx* psi, cudaStream_t st);
 void engine_set_reference(tn_hvp_ctx* ctx, const cplx* ref, cudaStream_t st);
 void engine_work(tn_hvp_ctx* ctx, double* per_dir, double* primal);
+void engine_split_stats(tn_hvp_ctx* ctx, int64_t* out6);
 void engine_query(const tn_hvp_config& cfg, const int32_t* ref_bonds, size_t* primal_bytes, size_t* work_bytes,
                   size_t* per_dir_bytes);
 void engine_destroy(tn_hvp_ctx* ctx);

@@ -679,6 +679,28 @@ void chol_flag(cudaStream_t st, const cplx* M, int n, bool upper, const int* inf
   count_launch();
 }
 
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {  // SplitMix64 finaliser
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+__global__ void fill_test_matrix_kernel(cplx* __restrict__ p, int64_t n, unsigned long long seed) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long a = mix64(seed + 2ULL * (unsigned long long)i * 0x9E3779B97F4A7C15ULL);
+    const unsigned long long b = mix64(seed + (2ULL * (unsigned long long)i + 1ULL) * 0x9E3779B97F4A7C15ULL);
+    p[i] = make_double2((double)(a >> 11) * (2.0 / 9007199254740992.0) - 1.0,
+                        (double)(b >> 11) * (2.0 / 9007199254740992.0) - 1.0);
+  }
+}
+
+void fill_test_matrix(cudaStream_t st, cplx* p, int64_t n, uint64_t seed) {
+  if (!n) return;
+  fill_test_matrix_kernel<<<nblocks(n), TPB, 0, st>>>(p, n, (unsigned long long)seed);
+  TN_CUDA(cudaGetLastError());
+  count_launch();
+}
+
 void dagger4(cudaStream_t st, cplx* dst, const cplx* src, int64_t n) {
   if (!n) return;
   dagger4_kernel<<<(int)((n * 16 + 255) / 256), 256, 0, st>>>(dst, src, n);

@@ -38,6 +38,9 @@ void tri_keep(cudaStream_t st, cplx* M, int n, bool upper);
 // row-major n x n factor M has a non-finite entry, or (near_identity) if max |M - I| > tol.
 void chol_flag(cudaStream_t st, const cplx* M, int n, bool upper, const int* info, bool near_identity, double tol,
                int* flag);
+// p[i] = uniform in (-1, 1)^2 from a counter-based hash of (seed, i): the fixed
+// test matrix of the low-rank range probe (not an input of the method).
+void fill_test_matrix(cudaStream_t st, cplx* p, int64_t n, uint64_t seed);
 // Vd[b][k] = V[b][k]^dag (4x4 each), n = batch*K matrices.
 void dagger4(cudaStream_t st, cplx* dst, const cplx* src, int64_t n);
 // out[0..2] = (max, min, max) of the two sides' diagnostics d[0..2], d[8..10]

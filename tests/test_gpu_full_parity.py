@@ -88,12 +88,14 @@ def test_full_size_parity(case):
     Gt, Vt = torch.tensor(G, device=dev), torch.tensor(V, device=dev)
     sc, gR, H = eng.step(Gt, Vt)                       # bench.py's step
     torch.cuda.synchronize()
+    split_stats = eng.split_stats()
     f = sc[0].item()
     T = complex(sc[1].item(), sc[2].item())
     gR, Hn = gR.cpu().numpy(), H.cpu().numpy()
     report = {"case": case, "t_reference_cpu_s": t_ref, "f_rel": abs(f - float(o["f"])) / abs(float(o["f"])),
               "T_rel": abs(T - complex(o["T"])) / abs(complex(o["T"])), "grad_R_rel": rel(gR, o["grad_R"]),
-              "grad_R_gate": gatewise(gR, o["grad_R"], TOL), "diag": sc[3:8].cpu().tolist()}
+              "grad_R_gate": gatewise(gR, o["grad_R"], TOL), "diag": sc[3:8].cpu().tolist(),
+              "split_stats": split_stats}
     assert report["f_rel"] <= TOL and report["T_rel"] <= TOL
     assert report["grad_R_rel"] <= TOL
     report["hess_R_rel"], report["hess_R_gate"] = {}, {}

@@ -74,6 +74,36 @@ def test_parity_small(cfg):
             assert abs(g["OM"][b] - o["OM"][b]) <= TOL * abs(o["OM"][b])
 
 
+def test_parity_low_entanglement_start():
+    """Trotter-initialised circuits (the X17 trust-region start, low
+    entanglement): many two-site blocks have numerical rank <= the kept rank
+    and are split by the range probe instead of an eigendecomposition
+    (tn_hvp_split_stats counts them).  Same parity bar against O3; a second
+    primal pass at the same point (hints learnt) gives the same outputs."""
+    from paper_2604_20384_b200.api import HVPEngine
+    cfg = C.small_case(205, 10, 6, 32, batch=2, t=0.3, steps=2)
+    ref, _, _ = workload(cfg)
+    K = C.num_gates(cfg.n, cfg.depth)
+    G = C.trotter_init_gates(cfg, 0)
+    V = C.tangent_directions(cfg.cid, G, 2)
+    o = oracle_outputs(cfg, ref, G, V)
+    dev = torch.device("cuda")
+    eng = HVPEngine(cfg.n, cfg.depth, cfg.chi, [a.to(dev) for a in ref], cfg.first_offset, max_batch=2)
+    Gt, Vt = torch.tensor(G, device=dev), torch.tensor(V, device=dev)
+    for rep in range(2):
+        sc, gR = eng.environments(Gt)
+        H = eng.apply(Vt)
+        st = eng.split_stats()
+        assert st["low_rank_splits"] > 0 and st["pair_steps"] == 2 * K, st
+        assert abs(sc[0].item() - o["f"]) <= TOL * abs(o["f"])
+        assert rel(gR.cpu().numpy(), o["grad_R"]) < TOL
+        gatewise(gR.cpu().numpy(), o["grad_R"], TOL)
+        for b in range(2):
+            assert rel(H[b].cpu().numpy(), o["HR"][b]) < TOL, (rep, b)
+            gatewise(H[b].cpu().numpy(), o["HR"][b], TOL)
+    eng.close()
+
+
 def test_parity_config1():
     """C1 (n = 6, exact MPO) against O3 and O2."""
     cfg = C.CONFIGS[1]
