@@ -24,6 +24,7 @@
 #include <functional>
 #include <mutex>
 #include <numeric>
+#include <cstdio>
 #include <cstdlib>
 #include <exception>
 #include <thread>
@@ -173,6 +174,8 @@ struct Engine {
   static constexpr int kCholMin = 32;  // below: the Householder panel is as fast
   std::atomic<int> n_cholqr_fallback{0}, n_lowrank{0};
   const bool lowrank_on = std::getenv("TN_NO_LOWRANK") == nullptr;
+  FILE* split_log = std::getenv("TN_SPLIT_LOG") ? fopen(std::getenv("TN_SPLIT_LOG"), "a") : nullptr;
+  std::mutex split_log_mu;
   std::vector<char> lowrank_hint;  // per pair step (s_index): try the range probe at the next pass
   cplx* d_omega = nullptr;         // fixed test matrix of the range probe (om_rows x om_cols)
   int om_rows = 0, om_cols = 0;
@@ -1194,6 +1197,18 @@ struct Engine {
               ++n_noise;
             }
             if (hint && in_noise) *hint = 1;  // rank <= r to ~1e-12: probe the range at the next pass
+            if (split_log) {  // diagnostic: spectrum profile of this split
+              int c4 = 0, c7 = 0, c10 = 0, c13 = 0;
+              for (int q = 0; q < R; ++q) {
+                c4 += hS[q] > 1e-4 * hS[0];
+                c7 += hS[q] > 1e-7 * hS[0];
+                c10 += hS[q] > 1e-10 * hS[0];
+                c13 += hS[q] > 1e-13 * hS[0];
+              }
+              std::lock_guard<std::mutex> g(split_log_mu);
+              fprintf(split_log, "%d %d %d %d %d %d %d %d %d %.3e %d\n", (int)is_top, s.s_index, R, P * s.br, s.r, c4, c7, c10,
+                      c13, delta, top_i);
+            }
             if (delta > 1e-2) {
               method = kQRIter;
               nbas = s.mn;

@@ -4,7 +4,8 @@ SURVEY.md §8(c.4) X11: the paper gives no construction for "a reference MPO
 truncated to chi"; this harness runs a plain TEBD of the Trotter layers on the
 identity operator I/2^{n/2} (site tensor delta_{oi}/sqrt(2), bond 1), gates on
 the OUT legs, mixed-canonical sweeps with QR centre moves, keep
-min(chi, #{sigma > 1e-14 sigma_max}) singular values per two-site split and
+min(chi, #{sigma > 1e-14 sigma_max}) singular values per two-site split (a cap
+that would cut a cluster of equal values drops the whole cluster) and
 rescale the kept values to the pre-truncation norm.  The result is returned
 right-canonical with the orthogonality centre at site 0 and unit Frobenius
 norm (a1: "U_ref/2^{n/2}, right-canonical, centre at site 0").
@@ -50,6 +51,22 @@ def _move_left(sites, c):
     sites[c - 1] = torch.einsum("apb,bc->apc", sites[c - 1], r.mH)
 
 
+CLUSTER_GAP = 1e-8
+
+
+def _keep_whole_multiplets(s, keep: int) -> int:
+    """A bond cut that falls inside a cluster of (numerically) equal singular
+    values -- the Schmidt multiplets of a symmetric model (XXZ: U(1)) -- keeps an
+    arbitrary part of the multiplet: WHICH operator comes out then depends on
+    the SVD routine's rounding, i.e. on the machine.  When the cap chi cuts such
+    a cluster (relative gap s[keep-1] - s[keep] <= CLUSTER_GAP s[keep-1]) the
+    whole cluster is dropped instead, so the generated reference is the same
+    operator on every machine (stored oracle outputs depend on it)."""
+    while 1 < keep < s.numel() and float(s[keep - 1] - s[keep]) <= CLUSTER_GAP * float(s[keep - 1]):
+        keep -= 1
+    return keep
+
+
 def tebd_out_legs(sites, layers, chi: int, tol: float = 1e-14):
     """Apply layers [(i, G), ...] to an MPO (centre at 0), truncating to chi."""
     dev = sites[0].device
@@ -72,12 +89,18 @@ def tebd_out_legs(sites, layers, chi: int, tol: float = 1e-14):
                 # WHICH reference MPO is generated, not its use downstream.
                 w, v = torch.linalg.eigh(th @ th.mH)
                 w, v = w.flip(0).clamp_min(0.0), v.flip(1)
-                keep = max(1, int(min(chi, int((w > (max(tol, 1e-7) ** 2) * w[0]).sum().item()))))
+                above = int((w > (max(tol, 1e-7) ** 2) * w[0]).sum().item())
+                keep = max(1, min(chi, above))
+                if keep < above:
+                    keep = _keep_whole_multiplets(w.sqrt().cpu(), keep)
                 u = v[:, :keep]
                 right = u.mH @ th
             else:
                 u, s, vh = torch.linalg.svd(th, full_matrices=False)
-                keep = max(1, int(min(chi, int((s > tol * s[0]).sum().item()))))
+                above = int((s > tol * s[0]).sum().item())
+                keep = max(1, min(chi, above))
+                if keep < above:                      # the cap cuts: never through a multiplet
+                    keep = _keep_whole_multiplets(s, keep)
                 u = u[:, :keep]
                 right = s[:keep, None].to(vh.dtype) * vh[:keep]
             right = right * (nrm / torch.linalg.vector_norm(right))
