@@ -96,3 +96,30 @@ def test_reference_mpo_is_the_trotter_product():
         m = a.reshape(a.shape[0], -1)
         assert np.abs(m @ m.conj().T - np.eye(a.shape[0])).max() < 1e-12
     assert mpo_bonds(sites)[0] == 1 and mpo_bonds(sites)[-1] == 1
+
+
+def test_reference_cap_never_cuts_a_multiplet():
+    """X25: a bond cap that would fall inside a cluster of equal singular
+    values drops the whole cluster (the truncated reference must be the same
+    operator on every machine).  Unit rule + a Heisenberg chain, whose SU(2)
+    multiplets are exactly degenerate: every kept bond spectrum ends at a gap."""
+    import torch
+    from tn_inputs import configs as C
+    from tn_inputs.reference import CLUSTER_GAP, _keep_whole_multiplets, reference_mpo
+    s = torch.tensor([1.0, 0.5, 0.5, 0.5 * (1 - 1e-12), 0.2, 0.1])
+    assert _keep_whole_multiplets(s, 3) == 1          # cap inside the 0.5 triplet: drop all of it
+    assert _keep_whole_multiplets(s, 4) == 4          # cap at the gap after the triplet
+    assert _keep_whole_multiplets(s, 5) == 5
+    assert _keep_whole_multiplets(s, 6) == 6          # nothing beyond: not a cut
+    cfg = C.small_case(77, 8, 2, 10, model=C.CONFIGS[2].model, t=0.5, steps=4)
+    full = reference_mpo(C.reference_layers(cfg), cfg.n, 256)
+    capped = reference_mpo(C.reference_layers(cfg), cfg.n, cfg.chi)
+    sf, sc = C.ref_schmidt_spectra([a.numpy() for a in full]), C.ref_schmidt_spectra([a.numpy() for a in capped])
+    shrunk = 0
+    for a, b in zip(sf, sc):
+        k = len(b)
+        assert k <= cfg.chi
+        shrunk += k < min(cfg.chi, len(a))
+        if k < len(a):                                # a real cut: it sits at a gap of the full spectrum
+            assert a[k - 1] - a[k] > CLUSTER_GAP * a[k - 1]
+    assert shrunk > 0                                 # the rule was exercised (chi = 10 cuts SU(2) multiplets)
