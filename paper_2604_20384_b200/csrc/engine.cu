@@ -176,7 +176,7 @@ struct Engine {
   const bool lowrank_on = std::getenv("TN_NO_LOWRANK") == nullptr;
   FILE* split_log = std::getenv("TN_SPLIT_LOG") ? fopen(std::getenv("TN_SPLIT_LOG"), "a") : nullptr;
   std::mutex split_log_mu;
-  std::vector<char> lowrank_hint;  // per pair step (s_index): try the range probe at the next pass
+  std::vector<char> lowrank_hint;  // per pair step (s_index): 1 = try the range probe at the next pass, 0 = not now, 2 = it failed here
   cplx* d_omega = nullptr;         // fixed test matrix of the range probe (om_rows x om_cols)
   int om_rows = 0, om_cols = 0;
   size_t svd_dws = 0, svd_hws = 0;
@@ -1140,7 +1140,7 @@ struct Engine {
                            ? &lowrank_hint[s.s_index]
                            : nullptr;
           bool lowrank = false;
-          if (hint && *hint) {
+          if (hint && *hint == 1) {
             lowrank = lowrank_split(st, so, tmp, A, P * s.bl, P * s.br, s.r, uh, info);
             if (lowrank) {
               ++n_lowrank;
@@ -1148,7 +1148,7 @@ struct Engine {
               TN_CUDA(cudaMemsetAsync(S, 0, (size_t)s.mn * sizeof(double), st));
               TN_CUDA(cudaMemcpyAsync(S, &one_d, sizeof(double), cudaMemcpyHostToDevice, st));
             } else {
-              *hint = 0;
+              *hint = 2;  // failed here: off for good (a noise-floor cut must not switch it back on every pass)
             }
           }
           if (!lowrank) {
@@ -1196,7 +1196,7 @@ struct Engine {
               delta = 1e-3;
               ++n_noise;
             }
-            if (hint && in_noise) *hint = 1;  // rank <= r to ~1e-12: probe the range at the next pass
+            if (hint && in_noise && *hint == 0) *hint = 1;  // rank <= r to ~1e-12: probe the range at the next pass
             if (split_log) {  // diagnostic: spectrum profile of this split
               int c4 = 0, c7 = 0, c10 = 0, c13 = 0;
               for (int q = 0; q < R; ++q) {

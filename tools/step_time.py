@@ -19,10 +19,15 @@ ap.add_argument("--max-batch", type=int, default=None)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--gates", default="haar")
 ap.add_argument("--tag", default="")
+ap.add_argument("--ref", default="torch", choices=["torch", "tebd"], help="reference built by tn_inputs (torch, GPU) or the library TEBD (bench.py)")
 a = ap.parse_args()
 cfg = C.CONFIGS[a.config]
 dev = torch.device("cuda")
-ref = C.reference_mpo(cfg, device=dev)
+if a.ref == "tebd":
+    from paper_2604_20384_b200.api import mpo_tebd
+    ref = mpo_tebd(cfg.n, C.reference_layers(cfg), cfg.chi)
+else:
+    ref = C.reference_mpo(cfg, device=dev)
 B = a.batch or cfg.batch
 K = C.num_gates(cfg.n, cfg.depth)
 Gn = C.haar_gates(cfg.cid, K) if a.gates == "haar" else C.trotter_init_gates(cfg, 0)
@@ -43,10 +48,16 @@ def timed(fn):
 
 out = {"config": cfg.name, "tag": a.tag, "batch": B, "step_s": [], "env_s": [], "apply_s": [],
        "env": {k: v for k, v in os.environ.items() if k.startswith("TN_")}}
+from paper_2604_20384_b200 import _native as N  # noqa: E402
 eng.step(G, V)
+out["stats_first"] = eng.split_stats()
+out["launches"] = []
 for _ in range(a.reps):
+    l0 = N.tn_hvp_launch_count()
     t, r = timed(lambda: eng.step(G, V))
     out["step_s"].append(round(t, 4))
+    out["launches"].append(N.tn_hvp_launch_count() - l0)
+out["stats"] = eng.split_stats()
 for _ in range(a.reps):
     t, r = timed(lambda: eng.environments(G))
     out["env_s"].append(round(t, 4))
