@@ -15,6 +15,7 @@
 //     at layer granularity, forward tangent cached, backward
 //    tangent on the fly.
 #include <cublas_v2.h>
+#include <cuda.h>
 #include <cusolverDn.h>
 
 #include <algorithm>
@@ -447,6 +448,63 @@ struct Engine {
     return p;
   }
 
+  CUgreenCtx green_ctx[2] = {nullptr, nullptr};
+  // Driver entry points through the runtime (the library does not link libcuda:
+  // it must load on a machine without a driver for the ABI tests).
+  template <class F>
+  static F driver_fn(const char* name) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &qr) != cudaSuccess || qr != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    return reinterpret_cast<F>(fn);
+  }
+  void destroy_green() {
+    auto destroy = driver_fn<CUresult (*)(CUgreenCtx)>("cuGreenCtxDestroy");
+    for (CUgreenCtx& g : green_ctx) {
+      if (g && destroy) destroy(g);
+      g = nullptr;
+    }
+  }
+  // st1 / st2 in two disjoint SM partitions of half the device each.
+  bool make_green_streams(int prio) {
+    auto dev_get = driver_fn<CUresult (*)(CUdevice*, int)>("cuDeviceGet");
+    auto get_res = driver_fn<CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType)>("cuDeviceGetDevResource");
+    auto split = driver_fn<CUresult (*)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*, unsigned,
+                                        unsigned)>("cuDevSmResourceSplitByCount");
+    auto gen_desc = driver_fn<CUresult (*)(CUdevResourceDesc*, CUdevResource*, unsigned)>("cuDevResourceGenerateDesc");
+    auto ctx_create = driver_fn<CUresult (*)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned)>("cuGreenCtxCreate");
+    auto stream_create = driver_fn<CUresult (*)(CUstream*, CUgreenCtx, unsigned, int)>("cuGreenCtxStreamCreate");
+    if (!dev_get || !get_res || !split || !gen_desc || !ctx_create || !stream_create) return false;
+    CUdevice dev;
+    CUdevResource all, parts[2], rem;
+    unsigned ng = 2;
+    if (dev_get(&dev, device) != CUDA_SUCCESS) return false;
+    if (get_res(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS) return false;
+    const unsigned half = (all.sm.smCount / 2) / 8 * 8;  // sm_90+: partitions are multiples of 8 SMs
+    if (half < 8) return false;
+    if (split(parts, &ng, &all, &rem, 0, half) != CUDA_SUCCESS || ng < 2) return false;
+    cudaStream_t out[2] = {nullptr, nullptr};
+    for (int i = 0; i < 2; ++i) {
+      CUdevResourceDesc d;
+      CUstream s = nullptr;
+      if (gen_desc(&d, &parts[i], 1) != CUDA_SUCCESS ||
+          ctx_create(&green_ctx[i], d, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
+          stream_create(&s, green_ctx[i], CU_STREAM_NON_BLOCKING, prio) != CUDA_SUCCESS) {
+        for (cudaStream_t x : out)
+          if (x) cudaStreamDestroy(x);
+        destroy_green();
+        return false;
+      }
+      out[i] = (cudaStream_t)s;
+    }
+    st1 = out[0];
+    st2 = out[1];
+    return true;
+  }
+
   // ------------------------------------------------------------ setup --
   // Host-only plan: layers, both sides' step lists with their static bond
   // profiles (a2/a3 keep rule, X7), and the primal-arena layout.
@@ -569,8 +627,27 @@ struct Engine {
       const int pr = use_prio ? (int)std::min<int64_t>(prio_lo, (int64_t)prio_hi + level) : prio_lo;
       TN_CUDA(cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, pr));
     };
-    mkstream(&st2, 0);
-    mkstream(&st1, 0);
+    // SM partitions for the two sweeps (CUDA green contexts): cuSOLVER's
+    // tridiagonalisation kernels take the whole GPU, so two eigensolves on
+    // plain streams run one after the other (Zheevd 512: 10.4 ms for two vs
+    // 5.9 ms for one); on disjoint halves of the SMs two n <= 512 solves
+    // overlap (7.9 ms for two, 6.7 ms for one: tools/green_probe.cu).  The
+    // n = 1024 solves of chi = 256 serialise in any case (30.5 ms for two), so
+    // partitions are used only when every Gram matrix is <= 512 wide.  Any
+    // failure here falls back to plain streams.
+    bool green = false;
+    {
+      int max_gram = 0;
+      for (SidePlan* sp : {&bot, &top})
+        for (auto& ls : sp->steps)
+          for (Step& x : ls)
+            if (x.type == PAIR) max_gram = std::max(max_gram, P * x.bl);
+      if (std::getenv("TN_NO_GREEN_CTX") == nullptr && max_gram > 64 && max_gram <= 512) green = make_green_streams(prio_hi);
+    }
+    if (!green) {
+      mkstream(&st2, 0);
+      mkstream(&st1, 0);
+    }
     TN_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     TN_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     TN_CUDA(cudaEventCreateWithFlags(&ev_join1, cudaEventDisableTiming));
@@ -661,6 +738,7 @@ struct Engine {
         if (e) cudaEventDestroy(e);
     for (cudaStream_t x : {st1, st2, stg, stf, sth, stc})
       if (x) cudaStreamDestroy(x);
+    destroy_green();
     if (arena && own_arena) cudaFree(arena);
     if (ref) cudaFree(ref);
     if (d_omega) cudaFree(d_omega);
