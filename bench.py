@@ -479,7 +479,8 @@ def main():
               "apply_only_hvps_per_s": B / (t_ap / 1e3),
               "apply_only": "SURVEY.md §8(d) HVPs/s: B directions / max-over-ranks apply time of the rank shares, "
                             "primal built once and excluded",
-              "apply_plus_broadcast_hvps_per_s": B / ((t_ap + (t_bc if world > 1 else 0.0)) / 1e3)}
+              "apply_plus_broadcast_hvps_per_s": B / ((t_ap + (t_bc if world > 1 else 0.0)) / 1e3),
+              "primal_split_paths": eng.split_stats()}
 
     peak, peak_src = fp64_peak()
     achieved = 8 * gemm_cmac / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
