@@ -2040,8 +2040,7 @@ struct Engine {
       cplx* Dt = pool.c(nD * nb);
       nn(st, P * bl, P * br, aa1, t.B[i], (int64_t)P * bl * aa1, t.Aa[i + 1], 0, Dt, nD, nb);
       nn(st, P * bl, P * br, ab1, t.Ab[i], 0, t.B[i + 1], (int64_t)ab1 * P * br, Dt, nD, nb, ONE, ONE);
-      apply_gate(st, Dt, nD, Dt, nD, Mk, 0, bl, br, nb, ONE, false, NI);
-      apply_gate(st, Dt, nD, theta, 0, VM + (int64_t)s.k * 16, KK, bl, br, nb, ONE, true, NI);
+      apply_gate2(st, Dt, nD, Dt, nD, Mk, 0, theta, 0, VM + (int64_t)s.k * 16, KK, bl, br, nb, NI);
       const int64_t sUD = (int64_t)r * P * br, sZ = (int64_t)P * bl * r, sRR = (int64_t)r * r;
       cplx* UD = pool.c(sUD * nb);
       nn(st, r, P * br, P * bl, uh, 0, Dt, nD, UD, sUD, nb);  // U^H D (uh is U^H, r x 4bl)

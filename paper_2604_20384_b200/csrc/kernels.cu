@@ -62,6 +62,52 @@ __global__ void apply_gate_kernel(cplx* out, int64_t sout, const cplx* x, int64_
   }
 }
 
+// out[b] = g1[b] x[b] + g2[b] y[b] on the out legs, one pass (the tangent update
+// D Theta = M D + V_M Theta: same arithmetic as apply_gate followed by an accumulating apply_gate)
+template <int NI>
+__global__ void apply_gate2_kernel(cplx* out, int64_t sout, const cplx* x, int64_t sx, const cplx* __restrict__ g1,
+                                   int64_t sg1, const cplx* __restrict__ y, int64_t sy, const cplx* __restrict__ g2,
+                                   int64_t sg2, int X, int Y, int batch) {
+  constexpr int P = 2 * NI;
+  const int64_t per = (int64_t)X * NI * NI * Y;
+  const int64_t total = per * batch;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = idx / per;
+    int64_t r = idx % per;
+    const int yy = (int)(r % Y);
+    r /= Y;
+    const int i12 = (int)(r % (NI * NI));
+    const int xx = (int)(r / (NI * NI));
+    const int i1 = i12 / NI, i2 = i12 % NI;
+    const int64_t base = (int64_t)xx * P * P * Y;
+    const cplx* xb = x + b * sx + base;
+    const cplx* yb = y + b * sy + base;
+    const cplx* ga = g1 + b * sg1;
+    const cplx* gb = g2 + b * sg2;
+    cplx ia[4], ib[4];
+    int64_t off[4];
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+      const int o1 = o >> 1, o2 = o & 1;
+      off[o] = ((int64_t)((o1 * NI + i1) * P + (o2 * NI + i2))) * Y + yy;
+      ia[o] = xb[off[o]];
+      ib[o] = yb[off[o]];
+    }
+    cplx* ob = out + b * sout + base;
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+      cplx a1 = make_double2(0, 0), a2 = make_double2(0, 0);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        a1 = cadd(a1, cmul(ga[o * 4 + c], ia[c]));
+        a2 = cadd(a2, cmul(gb[o * 4 + c], ib[c]));
+      }
+      ob[off[o]] = cadd(a1, a2);
+    }
+  }
+}
+
 __global__ void axpby_kernel(cplx* __restrict__ y, const cplx* __restrict__ x, cplx a, cplx b, int64_t n) {
   const bool read_y = b.x != 0.0 || b.y != 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -293,6 +339,18 @@ void apply_gate(cudaStream_t st, cplx* out, int64_t sout, const cplx* x, int64_t
   else
     apply_gate_kernel<1><<<nblocks(total), TPB, 0, st>>>(out, sout, x, sx, gate, sg, X, Y, batch, alpha,
                                                          accumulate ? 1 : 0);
+  TN_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+void apply_gate2(cudaStream_t st, cplx* out, int64_t sout, const cplx* x, int64_t sx, const cplx* g1, int64_t sg1,
+                 const cplx* y, int64_t sy, const cplx* g2, int64_t sg2, int X, int Y, int batch, int ni) {
+  const int64_t total = (int64_t)X * ni * ni * Y * batch;
+  if (total == 0) return;
+  if (ni == 2)
+    apply_gate2_kernel<2><<<nblocks(total), TPB, 0, st>>>(out, sout, x, sx, g1, sg1, y, sy, g2, sg2, X, Y, batch);
+  else
+    apply_gate2_kernel<1><<<nblocks(total), TPB, 0, st>>>(out, sout, x, sx, g1, sg1, y, sy, g2, sg2, X, Y, batch);
   TN_CUDA(cudaGetLastError());
   count_launch();
 }

@@ -9,6 +9,9 @@ namespace tn {
 // [X][2ni][2ni][Y]; accumulate adds to out.  In-place allowed.
 void apply_gate(cudaStream_t st, cplx* out, int64_t sout, const cplx* x, int64_t sx, const cplx* gate, int64_t sg,
                 int X, int Y, int batch, cplx alpha, bool accumulate, int ni = 2);
+// out[b] = g1[b] x[b] + g2[b] y[b] on the out legs in one pass (strides in elements, 0 = shared); out may alias x.
+void apply_gate2(cudaStream_t st, cplx* out, int64_t sout, const cplx* x, int64_t sx, const cplx* g1, int64_t sg1,
+                 const cplx* y, int64_t sy, const cplx* g2, int64_t sg2, int X, int Y, int batch, int ni = 2);
 void axpby(cudaStream_t st, cplx* y, const cplx* x, cplx a, cplx b, int64_t n);   // y = a x + b y
 void scale_by(cudaStream_t st, cplx* y, const double* s, double pw, int64_t n);    // y *= s^pw (device s)
 // dst[i][j] = src[i][j] / S[i] (device S[rows]; rows x cols row-major)
