@@ -79,6 +79,13 @@ def test_full_size_parity(case):
     for j, sv in enumerate(C.ref_schmidt_spectra([x.numpy() for x in ref_cpu])):
         want = rs[f"cut{j + 1}"]
         assert np.abs(sv - want).max() <= 1e-10 * want[0], f"reference differs at cut {j + 1}"
+    if "probe_mantissa" in rs.files:   # overlaps with fixed probe MPOs: equal Schmidt values do not imply equal operators
+        pm, pl = C.ref_probe_overlaps([x.numpy() for x in ref_cpu])
+        same = (np.abs(pl - rs["probe_log10"]).max() <= 1e-8
+                and np.abs(pm - rs["probe_mantissa"]).max() <= 1e-8 * np.abs(rs["probe_mantissa"]).max())
+        if not same:
+            pytest.skip(f"the reference MPO rebuilt on this machine is another operator than the one the stored "
+                        f"oracle outputs of {case} were computed on (probe overlaps differ: inputs, not outputs)")
     dev = torch.device("cuda")
     batch = max(cfg.batch, nd)
     V = C.tangent_directions(cfg.cid, G, batch)

@@ -159,3 +159,29 @@ def ref_schmidt_spectra(sites):
         out.append(_np.linalg.svd(r, compute_uv=False))
         c = _np.einsum("ab,bpc->apc", r, a[j + 1])
     return out
+
+
+def ref_probe_overlaps(sites, nprobe: int = 4, bond: int = 3):
+    """Overlaps <<X_j|R>> of an MPO R with `nprobe` fixed pseudo-random MPOs X_j of
+    bond dimension `bond` (numpy default_rng(1000 + j), one site tensor reused at
+    every site): gauge invariant like the Schmidt values, but they also tell
+    apart two operators with equal Schmidt values (e.g. different kept parts of a
+    degenerate multiplet).  Returns (unit-modulus-scaled complex mantissas,
+    log10 magnitudes) so that long chains neither overflow nor underflow."""
+    import numpy as _np
+    a = [_np.asarray(x, dtype=_np.complex128) for x in sites]
+    mant, logs = [], []
+    for j in range(nprobe):
+        rng = _np.random.default_rng(1000 + j)
+        x = (rng.standard_normal((bond, 4, bond)) + 1j * rng.standard_normal((bond, 4, bond))) / _np.sqrt(8.0 * bond)
+        env = _np.zeros((bond, a[0].shape[0]), dtype=_np.complex128)
+        env[0, :] = 1.0
+        lg = 0.0
+        for t in a:                                   # env[x, r] <- sum conj(X[x, p, x']) env[x, r] R[r, p, r']
+            env = _np.einsum("xr,xpy,rpq->yq", env, x.conj(), t, optimize=True)
+            nrm = _np.linalg.norm(env)
+            env /= nrm
+            lg += _np.log10(nrm)
+        mant.append(env[0, :].sum())
+        logs.append(lg)
+    return _np.array(mant), _np.array(logs)

@@ -20,7 +20,8 @@ a = ap.parse_args()
 cfg = C.full_parity_config(a.case)
 ref = [x.detach().resolve_conj().cpu().numpy() for x in C.reference_mpo(cfg, device="cpu")]
 spec = C.ref_schmidt_spectra(ref)
+probe_m, probe_l = C.ref_probe_overlaps(ref)
 np.savez_compressed(os.path.join(ROOT, "tests", "golden", f"full_{a.case}_ref.npz"),
-                    bonds=np.array([1] + [x.shape[2] for x in ref]),
+                    bonds=np.array([1] + [x.shape[2] for x in ref]), probe_mantissa=probe_m, probe_log10=probe_l,
                     **{f"cut{j + 1}": s for j, s in enumerate(spec)})
 print(a.case, "cuts", len(spec), "max bond", max(x.shape[2] for x in ref))
