@@ -1211,6 +1211,7 @@ struct Engine {
           double* Sf = (double*)tmp.raw((size_t)P * s.bl * sizeof(double));
           int iters = 0;
           int lq_steps = 0;  // > 0: W_r^H by Newton-Schulz steps on the sigma-scaled rows (lq_rows_lowdin)
+          bool y_ill = false;  // Y = U_r^H A known to be ill-conditioned (cut in the unresolved tail): Householder LQ
           // Low-rank blocks (numerical rank <= r): range probe instead of an
           // eigendecomposition.  Tried where the last pass at this step found it
           // (or a cut inside the noise floor); a failed probe switches it off.
@@ -1302,6 +1303,7 @@ struct Engine {
                 const double e0 = 2.2e-14 * (hS[0] / hS[s.r - 1]) * (hS[0] / hS[s.r - 1]);
                 lq_steps = e0 < 1e-9 ? 1 : e0 < 1e-5 ? 2 : e0 < 1e-3 ? 3 : 0;
               }
+              y_ill = top_i > 0 || !(hS[s.r - 1] > 1e-6 * hS[0]);
             }
           }
           TN_CUDA(cudaMemcpyAsync(S, Sf, (size_t)s.mn * sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -1322,7 +1324,7 @@ struct Engine {
           if (lq_steps > 0)
             lq_rows_lowdin(st, tmp, Y, Sf, s.r, P * s.br, lq_steps, vh, Lq);
           else  // (a low-rank Y is rank deficient: Householder only)
-            lq_left(st, so, tmp, Y, s.r, P * s.br, s.r, vh, Lq, info, /*allow_chol=*/!lowrank);
+            lq_left(st, so, tmp, Y, s.r, P * s.br, s.r, vh, Lq, info, /*allow_chol=*/!lowrank && !y_ill);
           cplx* ni = dnew((int64_t)P * s.bl * s.r, st);
           cplx* nj = dnew((int64_t)s.r * P * s.br, st);
           if (s.lr) {  // (U_r, s U_r^H A), centre -> i+1
