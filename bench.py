@@ -197,6 +197,8 @@ def oracle_baseline(cfg, ref_cpu, G, budget_s=10.0):
            "hvps_per_s_1thread": r1, "hvps_per_s_all_cores": ra, "nproc": ncores, "cpu_model": cpu_model(),
            "s_per_hvp_1thread_upper_bound": 1 / r1, "s_per_hvp_all_cores_upper_bound": 1 / ra}
     gpath = os.path.join(ROOT, "tests", "golden", f"full_c{cfg.cid}.json")
+    if not os.path.exists(gpath):   # per-direction oracle runs (tools/golden_full.py --only b)
+        gpath = os.path.join(ROOT, "tests", "golden", f"full_c{cfg.cid}_d0.json")
     if os.path.exists(gpath):
         with open(gpath) as f:
             g = json.load(f)
